@@ -1,0 +1,269 @@
+"""FastILU CPU oracle -- TEST INFRASTRUCTURE ONLY.
+
+Plain, slow, obviously-correct fp64 implementation of what the FastILU hot
+path computes (arXiv 2506.05793 Section 5), used to prove
+parity of the CUDA path.  Only tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / `--impl reference` legs may import this package; the product
+package (paper_2506_05793_b200) never does, and this package never imports
+the product.  Arithmetic lives in fastilu_oracle.c (compiled -O2
+-ffp-contract=off, single thread); this file only marshals arrays.
+
+Pins (tests/test_oracle_*.py, `-m "not gpu"`):
+  * symbolic ILU(k): the ten nnz/n values printed in tab:fastilu_nx16/32
+    (PAPER.md:596, 660); brute-force fill-path levels on tiny graphs; closed
+    forms; k=0 => S = pattern(A); tridiagonal => no fill; dense => dense.
+  * exact ILU: tridiagonal ILU(0) == Thomas LU bitwise; dense KIJ elimination
+    with dropping == IKJ bitwise; k >= n => LAPACK getrf within 1e-14.
+  * sweeps: reach the exact ILU bitwise within the dependency-DAG depth;
+    residual non-increasing above the roundoff floor; diagonal A immediate.
+  * trisolve: == substitution after nlevels sweeps (bitwise), T = I, 1 sweep
+    = D^-1 b; substitution == scipy solve_triangular.
+Functions here are all pinned; none is "parity unpinned".
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "fastilu_oracle.c")
+_LIB = os.path.join(_HERE, "build", "libfastilu_oracle.so")
+
+STATUS = {0: "OK", 1: "INVALID_ARG", 2: "BAD_MATRIX", 3: "MISSING_DIAG",
+          4: "ZERO_DIAG", 5: "ZERO_PIVOT", 9: "OOM"}
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code, index):
+        super().__init__(f"oracle status {STATUS.get(code, code)} at index {index}")
+        self.code = code
+        self.status = STATUS.get(code, str(code))
+        self.index = index
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle C library with gcc (plain -O2, no FMA contraction)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        os.makedirs(os.path.dirname(_LIB), exist_ok=True)
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c11",
+                               "-fPIC", "-shared", "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+_lib = None
+I64P = C.POINTER(C.c_int64)
+I32P = C.POINTER(C.c_int32)
+F64P = C.POINTER(C.c_double)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = C.CDLL(build())
+        L = _lib
+        L.orc_validate.argtypes = [C.c_int64, I64P, I32P, I64P]
+        L.orc_symbolic.argtypes = [C.c_int64, I64P, I32P, C.c_int, C.POINTER(I64P),
+                                   C.POINTER(I32P), C.POINTER(I32P), I64P]
+        L.orc_free.argtypes = [C.c_void_p]
+        L.orc_scale_init.argtypes = [C.c_int64, I64P, I32P, F64P, I64P, I32P, F64P, F64P, F64P, I64P]
+        L.orc_bad_diagonal.argtypes = [C.c_int64, I64P, I32P, F64P]
+        L.orc_bad_diagonal.restype = C.c_int64
+        L.orc_sweep.argtypes = [C.c_int64, I64P, I32P, F64P, F64P, F64P, C.c_double, F64P]
+        L.orc_sweep.restype = None
+        L.orc_compute.argtypes = [C.c_int64, I64P, I32P, F64P, I64P, I32P, C.c_int, C.c_double,
+                                  F64P, F64P, F64P, F64P, I64P]
+        L.orc_exact_ilu.argtypes = [C.c_int64, I64P, I32P, F64P, F64P, I64P]
+        for f in ("orc_jacobi_lower", "orc_jacobi_upper"):
+            getattr(L, f).argtypes = [C.c_int64, I64P, I32P, F64P, F64P, C.c_int, C.c_double, F64P]
+            getattr(L, f).restype = None
+        L.orc_apply.argtypes = [C.c_int64, I64P, I32P, F64P, F64P, F64P, C.c_int, C.c_double, F64P]
+        L.orc_apply.restype = None
+        for f in ("orc_subst_lower", "orc_subst_upper"):
+            getattr(L, f).argtypes = [C.c_int64, I64P, I32P, F64P, F64P, F64P]
+            getattr(L, f).restype = None
+    return _lib
+
+
+def _p(a, t):
+    return a.ctypes.data_as(t)
+
+
+def _i64(a):
+    return np.ascontiguousarray(a, dtype=np.int64)
+
+
+def _i32(a):
+    return np.ascontiguousarray(a, dtype=np.int32)
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+class Pattern:
+    """ILU(k) pattern S: row_ptr int64, col_idx int32, level int32 (row-wise, sorted)."""
+
+    def __init__(self, row_ptr, col_idx, level):
+        self.row_ptr, self.col_idx, self.level = row_ptr, col_idx, level
+        self.n = row_ptr.shape[0] - 1
+
+    @property
+    def nnz(self):
+        return int(self.row_ptr[-1])
+
+
+def validate(row_ptr, col_idx):
+    rp, ci = _i64(row_ptr), _i32(col_idx)
+    bad = C.c_int64(-1)
+    st = lib().orc_validate(rp.shape[0] - 1, _p(rp, I64P), _p(ci, I32P), C.byref(bad))
+    return st, bad.value
+
+
+def symbolic(row_ptr, col_idx, k: int) -> Pattern:
+    """Symbolic ILU(k) by the sum rule, row-wise, ascending pivots (reading R7)."""
+    rp, ci = _i64(row_ptr), _i32(col_idx)
+    n = rp.shape[0] - 1
+    orp, oci, olev = I64P(), I32P(), I32P()
+    bad = C.c_int64(-1)
+    st = lib().orc_symbolic(n, _p(rp, I64P), _p(ci, I32P), int(k), C.byref(orp), C.byref(oci),
+                            C.byref(olev), C.byref(bad))
+    if st != 0:
+        raise OracleError(st, bad.value)
+    nnz = orp[n]
+    srp = np.ctypeslib.as_array(orp, shape=(n + 1,)).copy()
+    sci = np.ctypeslib.as_array(oci, shape=(max(nnz, 1),))[:nnz].copy()
+    slev = np.ctypeslib.as_array(olev, shape=(max(nnz, 1),))[:nnz].copy()
+    for p in (orp, oci, olev):
+        lib().orc_free(C.cast(p, C.c_void_p))
+    return Pattern(srp, sci, slev)
+
+
+def scale_init(a, pat: Pattern):
+    """Returns (s, ahat_S, vals0_S) -- readings R4, R5."""
+    rp, ci, av = _i64(a.row_ptr), _i32(a.col_idx), _f64(a.values)
+    n = a.n
+    s = np.empty(n)
+    ahat = np.empty(pat.nnz)
+    vals = np.empty(pat.nnz)
+    bad = C.c_int64(-1)
+    st = lib().orc_scale_init(n, _p(rp, I64P), _p(ci, I32P), _p(av, F64P), _p(pat.row_ptr, I64P),
+                              _p(pat.col_idx, I32P), _p(s, F64P), _p(ahat, F64P), _p(vals, F64P),
+                              C.byref(bad))
+    if st != 0:
+        raise OracleError(st, bad.value)
+    return s, ahat, vals
+
+
+def sweep(pat: Pattern, ahat, old, omega: float = 1.0):
+    """One synchronous sweep; returns (new, r(s-1))."""
+    ahat, old = _f64(ahat), _f64(old)
+    out = np.empty_like(old)
+    r = C.c_double(0.0)
+    lib().orc_sweep(pat.n, _p(pat.row_ptr, I64P), _p(pat.col_idx, I32P), _p(ahat, F64P),
+                    _p(old, F64P), _p(out, F64P), float(omega), C.byref(r))
+    return out, r.value
+
+
+def bad_diagonal(pat: Pattern, vals) -> int:
+    vals = _f64(vals)
+    return int(lib().orc_bad_diagonal(pat.n, _p(pat.row_ptr, I64P), _p(pat.col_idx, I32P),
+                                      _p(vals, F64P)))
+
+
+class Factors:
+    def __init__(self, pat, s, ahat, vals, resid):
+        self.pattern, self.s, self.ahat, self.vals, self.resid = pat, s, ahat, vals, resid
+
+
+def compute(a, k: int, nsweeps: int, omega: float = 1.0, pat: Pattern | None = None) -> Factors:
+    """Symbolic + scale/init + nsweeps synchronous sweeps (whole FastILU compute)."""
+    if pat is None:
+        pat = symbolic(a.row_ptr, a.col_idx, k)
+    rp, ci, av = _i64(a.row_ptr), _i32(a.col_idx), _f64(a.values)
+    n = a.n
+    s = np.empty(n)
+    ahat = np.empty(pat.nnz)
+    vals = np.empty(pat.nnz)
+    hist = np.zeros(max(nsweeps, 1))
+    bad = C.c_int64(-1)
+    st = lib().orc_compute(n, _p(rp, I64P), _p(ci, I32P), _p(av, F64P), _p(pat.row_ptr, I64P),
+                           _p(pat.col_idx, I32P), int(nsweeps), float(omega), _p(s, F64P),
+                           _p(ahat, F64P), _p(vals, F64P), _p(hist, F64P), C.byref(bad))
+    if st != 0:
+        raise OracleError(st, bad.value)
+    return Factors(pat, s, ahat, vals, hist[:nsweeps].copy())
+
+
+def exact_ilu(pat: Pattern, ahat):
+    ahat = _f64(ahat)
+    vals = np.empty_like(ahat)
+    bad = C.c_int64(-1)
+    st = lib().orc_exact_ilu(pat.n, _p(pat.row_ptr, I64P), _p(pat.col_idx, I32P), _p(ahat, F64P),
+                             _p(vals, F64P), C.byref(bad))
+    if st != 0:
+        raise OracleError(st, bad.value)
+    return vals
+
+
+def jacobi_lower(pat: Pattern, vals, y, ntri: int, omega: float = 1.0):
+    vals, y = _f64(vals), _f64(y)
+    z = np.empty(pat.n)
+    lib().orc_jacobi_lower(pat.n, _p(pat.row_ptr, I64P), _p(pat.col_idx, I32P), _p(vals, F64P),
+                           _p(y, F64P), int(ntri), float(omega), _p(z, F64P))
+    return z
+
+
+def jacobi_upper(pat: Pattern, vals, z, ntri: int, omega: float = 1.0):
+    vals, z = _f64(vals), _f64(z)
+    w = np.empty(pat.n)
+    lib().orc_jacobi_upper(pat.n, _p(pat.row_ptr, I64P), _p(pat.col_idx, I32P), _p(vals, F64P),
+                           _p(z, F64P), int(ntri), float(omega), _p(w, F64P))
+    return w
+
+
+def apply(f: Factors, b, ntri: int, omega_tri: float = 1.0):
+    """x = s o U^-1 L^-1 (s o b) with ntri Jacobi sweeps per factor (R5, R6)."""
+    b = _f64(b)
+    s = _f64(f.s)
+    x = np.empty(f.pattern.n)
+    p = f.pattern
+    lib().orc_apply(p.n, _p(p.row_ptr, I64P), _p(p.col_idx, I32P), _p(_f64(f.vals), F64P),
+                    _p(s, F64P), _p(b, F64P), int(ntri), float(omega_tri), _p(x, F64P))
+    return x
+
+
+def subst_lower(pat: Pattern, vals, y):
+    vals, y = _f64(vals), _f64(y)
+    z = np.empty(pat.n)
+    lib().orc_subst_lower(pat.n, _p(pat.row_ptr, I64P), _p(pat.col_idx, I32P), _p(vals, F64P),
+                          _p(y, F64P), _p(z, F64P))
+    return z
+
+
+def subst_upper(pat: Pattern, vals, z):
+    vals, z = _f64(vals), _f64(z)
+    w = np.empty(pat.n)
+    lib().orc_subst_upper(pat.n, _p(pat.row_ptr, I64P), _p(pat.col_idx, I32P), _p(vals, F64P),
+                          _p(z, F64P), _p(w, F64P))
+    return w
+
+
+def windowed(a_full, plane: int, lo_plane: int, hi_plane: int, k: int, nsweeps: int,
+             b_full=None, ntri: int = 0, omega: float = 1.0, omega_tri: float = 1.0):
+    """Windowed oracle for stencil problems in natural z-plane order (DESIGN.md "windowed
+    oracle"): runs the whole path on rows/cols of planes [lo_plane, hi_plane) of `a_full`
+    and returns (row_lo, row_hi) of the window plus the Factors / x for the window.
+    Callers compare only planes far enough from the cut (margins in DESIGN.md)."""
+    from problems import submatrix  # data slicing only, no method arithmetic
+    lo, hi = lo_plane * plane, hi_plane * plane
+    sub = submatrix(a_full, lo, hi)
+    f = compute(sub, k, nsweeps, omega)
+    x = None
+    if b_full is not None:
+        x = apply(f, np.asarray(b_full)[lo:hi], ntri, omega_tri)
+    return lo, hi, f, x
