@@ -1,0 +1,307 @@
+#!/usr/bin/env python
+"""FastILU benchmark (BASELINE.json metric: FastILU sweep nnz-updates/s and trisolve GB/s vs HBM
+peak).  One step = one pass of the whole hot path on one synthetic matrix: fastilu_compute
+(scale + init + nsweeps synchronous sweeps) then fastilu_apply (ntri Jacobi sweeps for L and
+for U).  Inputs (A, b) are resident in HBM before the timed region; the working set (tens of GB)
+exceeds the 126 MB L2, so no explicit flush is needed between steps for the default workload.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME] [--impl ours|reference]
+
+Prints ONE JSON line on rank 0.  `value` = nnz(S) * nsweeps * N / (device time of one step, max
+over ranks).  Extra keys: sweep-only rate, trisolve and composite GB/s, the dominant kernel's
+roofline, e2e through host buffers, and the oracle timed on a bounded sample (cpu_baseline).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import problems as P  # noqa: E402
+
+METRIC = "FastILU sweep nnz-updates/s and trisolve GB/s vs HBM peak, 1/2/4/8 B200"
+UNIT = "nnz-updates/s"
+SV, SI = 8, 4
+
+
+def byte_model(n, nnz_A, nnz_S, nnz_Ls, ns, nt):
+    """Algorithmic bytes."""
+    sp = 4 if nnz_S < 2**31 else 8
+    B_f = nnz_S * (2 * SV + SI) + nnz_A * SV + 2 * (n + 1) * sp
+    B_L = nnz_Ls * (SV + SI) + (n + 1) * sp + 3 * n * SV
+    B_U = B_L + n * SV
+    B_init = nnz_A * (SV + SI) + nnz_S * SV + n * SV
+    # first L sweep (z0 = 0): y = s o b, z1 = w y -> 4 n words; first U sweep: w1 = z / u_ii
+    B_apply = (nt - 1) * (B_L + B_U) + 4 * n * SV + 3 * n * SV
+    return dict(B_f=B_f, B_L=B_L, B_U=B_U, B_init=B_init, B_apply=B_apply)
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(dev), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[1]))
+                smax.append(float(r[2]))
+                for nm, v in zip(names, r[5:9]):
+                    if v.strip().lower() in ("active", "1"):
+                        reasons.add(nm)
+            except (ValueError, IndexError):
+                continue
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def build_matrix(kind, g):
+    t = time.perf_counter()
+    a = P.make(kind, g)
+    return a, time.perf_counter() - t
+
+
+def cpu_sample(kind, g, k, ns, nt, planes):
+    """Oracle on a bounded sample of the workload: a g x g x planes slab of the same stencil."""
+    import oracle
+    sub = P.make(kind, g, gz=planes)
+    pat = oracle.symbolic(sub.row_ptr, sub.col_idx, k)
+    b = P.rhs_positive(sub.n)
+    t0 = time.perf_counter()
+    f = oracle.compute(sub, k, ns, pat=pat)
+    oracle.apply(f, b, nt)
+    dt = time.perf_counter() - t0
+    return dict(value=pat.nnz * ns / dt, seconds=dt, nnz_S=pat.nnz, n=sub.n,
+                sample=f"{kind} {g}x{g}x{planes} slab, ILU({k}), {ns} sweeps + {nt}/{nt} "
+                       f"trisweeps, scale/init+sweeps+apply timed (symbolic excluded)")
+
+
+def run_reference(args, wl):
+    kind, g, k, ns, nt = wl
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    planes = args.cpu_planes or default_cpu_planes(kind, g, k)
+    for _ in range(args.warmup):
+        cpu_sample(kind, g, k, ns, nt, planes)
+    vals, secs = [], []
+    for _ in range(args.steps):
+        r = cpu_sample(kind, g, k, ns, nt, planes)
+        vals.append(r["value"])
+        secs.append(r["seconds"])
+    v = float(np.median(vals))
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * float(np.median(secs)), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.workload, "sample_planes": planes},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": r["sample"]},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def default_cpu_planes(kind, g, k):
+    # ~10-20 s of single-thread oracle work per sample
+    per_plane = {"7pt": 7, "aniso7pt": 7, "27pt": {0: 27, 1: 63, 2: 115}.get(k, 200)}[kind] * g * g
+    return int(max(2, min(g, 4_000_000 // max(per_plane, 1))))
+
+
+def run_ours(args, wl):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2506_05793_b200 as F
+
+    kind, g, k, ns, nt = wl
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+
+    a, t_gen = build_matrix(kind, g)
+    t0 = time.perf_counter()
+    f = F.FastILU(a.row_ptr, a.col_idx, a.values, k, device=local, stream=stream.cuda_stream)
+    t_setup = time.perf_counter() - t0
+    n, nnz_S, nnz_A = f.n, f.nnz_S, f.nnz_A
+    rp, ci, _ = f.pattern()
+    rows = np.repeat(np.arange(n), np.diff(rp))
+    nnz_Ls = int(np.count_nonzero(ci < rows))
+    del rows, rp, ci
+    bm = byte_model(n, nnz_A, nnz_S, nnz_Ls, ns, nt)
+    b = torch.tensor(P.rhs_positive(n), device=dev)
+    x = torch.empty_like(b)
+
+    def step():
+        f.compute(ns)
+        f.apply(b, x, nt)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = Clocks(local)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t_sweeps, t_apply, t_init = [], [], []
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+        tm = f.timings()  # library CUDA events on this stream (compute synchronised)
+        t_sweeps.append(tm["sweeps_ms"])
+        t_init.append(tm["init_ms"])
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    # apply alone (events inside the library), measured on the last step
+    t_apply = f.timings()["apply_ms"]
+    if world > 1:
+        tt = torch.tensor([ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+        dist.barrier()
+    sweep_ms = float(np.mean(t_sweeps))
+    value = nnz_S * ns * world / (ms * 1e-3)
+    peak, peak_src = peaks()
+    per_launch_ms = sweep_ms / max(ns, 1)
+    achieved = bm["B_f"] / (per_launch_ms * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get(args.workload, {}).get("sweep_dram_bytes")
+
+    # e2e through host buffers: H2D of A's values and b, compute, apply, D2H of x, every step
+    e2e = None
+    if not args.no_e2e:
+        av = torch.from_numpy(a.values).pin_memory().numpy()
+        bh = torch.from_numpy(P.rhs_positive(n)).pin_memory().numpy()
+        xh = torch.empty(n, dtype=torch.float64).pin_memory().numpy()
+        f.set_values(av)
+        f.compute(ns)
+        f.apply_host(bh, nt, out=xh)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ke = max(1, min(args.steps, 5))
+        e0.record(stream)
+        for _ in range(ke):
+            f.set_values(av)
+            f.compute(ns)
+            f.apply_host(bh, nt, out=xh)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1) / ke
+        if world > 1:
+            tt = torch.tensor([ems], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ems = float(tt.item())
+        e2e = {"value": nnz_S * ns * world / (ems * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": int(a.values.nbytes + 8 * n), "d2h_bytes_per_step": int(8 * n),
+               "ms_per_step": ems}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        planes = args.cpu_planes or default_cpu_planes(kind, g, k)
+        r = cpu_sample(kind, g, k, ns, nt, planes)
+        cpu = {"value": r["value"], "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": r["sample"]}
+
+    launches_per_step = 2 + 2 * ns + 2 * nt
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded stencil generator, b ~ U[0.5,1.5))",
+            "config": {"workload": args.workload, "grid": g, "stencil": kind, "level_k": k,
+                       "nsweeps": ns, "ntrisweeps": nt, "n": n, "nnz_A": nnz_A, "nnz_S": nnz_S,
+                       "parallelism": f"rows{world}" if world > 1 else "1gpu",
+                       "l2": "working set >> 126 MB L2 (no flush needed)"},
+            "sweep_nnz_updates_per_s": nnz_S * ns / (sweep_ms * 1e-3),
+            "sweep_ms": sweep_ms, "init_ms": float(np.mean(t_init)), "apply_ms": t_apply,
+            "trisolve_gbs": bm["B_apply"] / (t_apply * 1e-3) / 1e9 if t_apply > 0 else None,
+            "composite_gbs": (bm["B_init"] + ns * bm["B_f"] + bm["B_apply"]) / (ms * 1e-3) / 1e9,
+            "roofline": {"bound": "hbm", "kernel": "sweep_kernel", "achieved": achieved,
+                         "peak": peak, "peak_source": peak_src, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "algorithmic_bytes_per_launch": bm["B_f"]},
+            "clocks": clk, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
+            "cpu_baseline": cpu,
+            "setup_s": {"generate": t_gen, "create": t_setup},
+        }
+        print(json.dumps(line), flush=True)
+    f.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c4_27pt_256_ilu1", choices=sorted(P.WORKLOADS))
+    ap.add_argument("--nsweeps", type=int, default=None)
+    ap.add_argument("--ntri", type=int, default=None)
+    ap.add_argument("--cpu-planes", type=int, default=None)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    kind, g, k, ns, nt = P.WORKLOADS[args.workload]
+    ns = args.nsweeps if args.nsweeps is not None else ns
+    nt = args.ntri if args.ntri is not None else nt
+    wl = (kind, g, k, ns, nt)
+    if args.impl == "reference":
+        run_reference(args, wl)
+    else:
+        run_ours(args, wl)
+
+
+if __name__ == "__main__":
+    main()

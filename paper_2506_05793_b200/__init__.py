@@ -1,0 +1,256 @@
+"""paper_2506_05793_b200 -- B200-native FastILU (arXiv 2506.05793, Section 5).
+
+Thin ctypes binding over the C ABI in include/fastilu.h (libfastilu_b200.so).  This module only
+marshals arguments: every step of the hot path runs in the library's CUDA kernels, and there is
+no CPU fallback -- if the shared library is missing the import of any entry point raises.
+PyTorch is used by callers for device memory and streams (tensor.data_ptr(), stream handles).
+
+ABI names are re-exported unchanged (fastilu_create, fastilu_compute, fastilu_apply, ...); the
+`FastILU` class is a convenience wrapper around one handle.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import re
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libfastilu_b200.so")
+HEADER = os.path.join(os.path.dirname(_HERE), "include", "fastilu.h")
+
+STATUS_NAMES = ["OK", "INVALID_ARG", "BAD_MATRIX", "MISSING_DIAG", "ZERO_DIAG", "ZERO_PIVOT",
+                "STATE", "CUDA", "NCCL", "OOM", "UNSUPPORTED"]
+COMM_NONE, COMM_NCCL, COMM_LOCAL = 0, 1, 2
+
+
+class FastILUError(RuntimeError):
+    def __init__(self, code: int, index: int = -1, what: str = ""):
+        self.code = code
+        self.status = STATUS_NAMES[code] if 0 <= code < len(STATUS_NAMES) else str(code)
+        self.index = index
+        super().__init__(f"{what}: FASTILU_ERR_{self.status} (index {index})")
+
+
+class Options(C.Structure):
+    """Mirror of fastilu_options (include/fastilu.h)."""
+    _fields_ = [("omega", C.c_double), ("omega_tri", C.c_double), ("device", C.c_int),
+                ("stream", C.c_void_p), ("num_threads", C.c_int), ("rank", C.c_int),
+                ("nranks", C.c_int), ("comm_kind", C.c_int), ("nccl_unique_id", C.c_void_p),
+                ("group", C.c_void_p), ("global_n", C.c_int64), ("row_begin", C.c_int64),
+                ("n_lead", C.c_int64)]
+
+
+I64P = C.POINTER(C.c_int64)
+I32P = C.POINTER(C.c_int32)
+I8P = C.POINTER(C.c_int8)
+F64P = C.POINTER(C.c_double)
+H = C.c_void_p
+
+_SIGS = {
+    "fastilu_default_options": (None, [C.POINTER(Options)]),
+    "fastilu_create": (C.c_int, [C.POINTER(H), C.c_int64, I64P, I32P, F64P, C.c_int,
+                                 C.POINTER(Options)]),
+    "fastilu_required_lead_rows": (C.c_int64, [C.c_int64, C.c_int]),
+    "fastilu_set_values": (C.c_int, [H, F64P]),
+    "fastilu_set_values_device": (C.c_int, [H, C.c_void_p]),
+    "fastilu_compute": (C.c_int, [H, C.c_int]),
+    "fastilu_apply": (C.c_int, [H, C.c_void_p, C.c_void_p, C.c_int]),
+    "fastilu_apply_host": (C.c_int, [H, F64P, F64P, C.c_int]),
+    "fastilu_destroy": (C.c_int, [H]),
+    "fastilu_get_sizes": (C.c_int, [H, I64P, I64P, I64P]),
+    "fastilu_get_pattern": (C.c_int, [H, I64P, I32P, I8P]),
+    "fastilu_get_factors": (C.c_int, [H, F64P, F64P]),
+    "fastilu_get_residual_history": (C.c_int, [H, F64P, C.c_int, C.POINTER(C.c_int)]),
+    "fastilu_get_timings": (C.c_int, [H, F64P]),
+    "fastilu_status_string": (C.c_char_p, [C.c_int]),
+    "fastilu_error_index": (C.c_int64, [H]),
+    "fastilu_symbolic": (C.c_int, [C.c_int64, I64P, I32P, C.c_int, C.c_int, I64P, I64P, I32P,
+                                   I8P, I64P]),
+    "fastilu_group_create": (C.c_int, [C.POINTER(H), C.c_int]),
+    "fastilu_group_destroy": (C.c_int, [H]),
+    "fastilu_nccl_unique_id": (C.c_int, [C.c_void_p]),
+}
+
+_lib = None
+
+
+def lib():
+    """Load libfastilu_b200.so (raises if it was not built: there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run `python -m paper_2506_05793_b200.build` "
+                              "(the FastILU hot path exists only as CUDA kernels)")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def header_functions() -> list[str]:
+    """Function names declared in include/fastilu.h."""
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(fastilu_[a-z_0-9]+)\s*\(", txt)))
+
+
+def _p(a, t):
+    return a.ctypes.data_as(t)
+
+
+def _check(code, what, h=None):
+    if code != 0:
+        idx = lib().fastilu_error_index(h) if h else -1
+        raise FastILUError(code, idx, what)
+
+
+def _ptr(t):
+    """Device pointer of a torch tensor or an int."""
+    return t if isinstance(t, int) else t.data_ptr()
+
+
+# ---------------------------------------------------------------- ABI names (thin wrappers)
+def fastilu_default_options() -> Options:
+    o = Options()
+    lib().fastilu_default_options(C.byref(o))
+    return o
+
+
+def fastilu_required_lead_rows(bandwidth: int, level_k: int) -> int:
+    return int(lib().fastilu_required_lead_rows(int(bandwidth), int(level_k)))
+
+
+def fastilu_symbolic(row_ptr, col_idx, level_k: int, num_threads: int = 0):
+    """Host-only symbolic ILU(k) -> (row_ptr int64, col_idx int32, level int8)."""
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    ci = np.ascontiguousarray(col_idx, dtype=np.int32)
+    n = rp.shape[0] - 1
+    nnz = C.c_int64(0)
+    bad = C.c_int64(-1)
+    st = lib().fastilu_symbolic(n, _p(rp, I64P), _p(ci, I32P), int(level_k), int(num_threads),
+                                C.byref(nnz), None, None, None, C.byref(bad))
+    if st:
+        raise FastILUError(st, bad.value, "fastilu_symbolic")
+    orp = np.empty(n + 1, dtype=np.int64)
+    oci = np.empty(max(nnz.value, 1), dtype=np.int32)
+    olev = np.empty(max(nnz.value, 1), dtype=np.int8)
+    st = lib().fastilu_symbolic(n, _p(rp, I64P), _p(ci, I32P), int(level_k), int(num_threads),
+                                C.byref(nnz), _p(orp, I64P), _p(oci, I32P), _p(olev, I8P),
+                                C.byref(bad))
+    if st:
+        raise FastILUError(st, bad.value, "fastilu_symbolic")
+    return orp, oci[:nnz.value], olev[:nnz.value]
+
+
+def fastilu_status_string(code: int) -> str:
+    return lib().fastilu_status_string(int(code)).decode()
+
+
+class FastILU:
+    """One fastilu_handle: create (symbolic + layouts) / compute / apply / destroy."""
+
+    def __init__(self, row_ptr, col_idx, values, level_k: int, *, omega: float = 1.0,
+                 omega_tri: float = 1.0, device: int = -1, stream=None, num_threads: int = 0,
+                 rank: int = 0, nranks: int = 1, comm_kind: int = COMM_NONE,
+                 nccl_unique_id: bytes | None = None, group=None, global_n: int = -1,
+                 row_begin: int = 0, n_lead: int = 0, n: int | None = None):
+        L = lib()
+        self._h = H()
+        o = fastilu_default_options()
+        o.omega, o.omega_tri, o.device = float(omega), float(omega_tri), int(device)
+        o.stream = stream
+        o.num_threads = int(num_threads)
+        o.rank, o.nranks, o.comm_kind = int(rank), int(nranks), int(comm_kind)
+        self._uid = C.create_string_buffer(nccl_unique_id, 128) if nccl_unique_id else None
+        o.nccl_unique_id = C.cast(self._uid, C.c_void_p) if self._uid is not None else None
+        o.group = group
+        o.global_n, o.row_begin, o.n_lead = int(global_n), int(row_begin), int(n_lead)
+        self._rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+        self._ci = np.ascontiguousarray(col_idx, dtype=np.int32)
+        vals = None if values is None else np.ascontiguousarray(values, dtype=np.float64)
+        nrows = (self._rp.shape[0] - 1 - int(n_lead)) if n is None else int(n)
+        st = L.fastilu_create(C.byref(self._h), nrows, _p(self._rp, I64P), _p(self._ci, I32P),
+                              None if vals is None else _p(vals, F64P), int(level_k),
+                              C.byref(o))
+        if st:
+            idx = L.fastilu_error_index(self._h)
+            L.fastilu_destroy(self._h)
+            self._h = None
+            raise FastILUError(st, idx, "fastilu_create")
+        n_, s_, a_ = C.c_int64(), C.c_int64(), C.c_int64()
+        L.fastilu_get_sizes(self._h, C.byref(n_), C.byref(s_), C.byref(a_))
+        self.n, self.nnz_S, self.nnz_A = n_.value, s_.value, a_.value
+        self.level_k = level_k
+
+    # -- numeric phase
+    def set_values(self, values):
+        v = np.ascontiguousarray(values, dtype=np.float64)
+        _check(lib().fastilu_set_values(self._h, _p(v, F64P)), "fastilu_set_values", self._h)
+
+    def set_values_device(self, values_dev):
+        _check(lib().fastilu_set_values_device(self._h, _ptr(values_dev)),
+               "fastilu_set_values_device", self._h)
+
+    def compute(self, nsweeps: int):
+        _check(lib().fastilu_compute(self._h, int(nsweeps)), "fastilu_compute", self._h)
+
+    def apply(self, b, x, ntrisweeps: int):
+        """b, x: float64 CUDA tensors (or raw device pointers) of length n; x may alias b."""
+        _check(lib().fastilu_apply(self._h, _ptr(b), _ptr(x), int(ntrisweeps)), "fastilu_apply",
+               self._h)
+
+    def apply_host(self, b, ntrisweeps: int, out=None):
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        x = np.empty(self.n) if out is None else out
+        _check(lib().fastilu_apply_host(self._h, _p(b, F64P), _p(x, F64P), int(ntrisweeps)),
+               "fastilu_apply_host", self._h)
+        return x
+
+    # -- introspection
+    def pattern(self):
+        rp = np.empty(self.n + 1, dtype=np.int64)
+        ci = np.empty(max(self.nnz_S, 1), dtype=np.int32)
+        lev = np.empty(max(self.nnz_S, 1), dtype=np.int8)
+        _check(lib().fastilu_get_pattern(self._h, _p(rp, I64P), _p(ci, I32P), _p(lev, I8P)),
+               "fastilu_get_pattern", self._h)
+        return rp, ci[:self.nnz_S], lev[:self.nnz_S]
+
+    def factors(self):
+        v = np.empty(max(self.nnz_S, 1))
+        s = np.empty(max(self.n, 1))
+        _check(lib().fastilu_get_factors(self._h, _p(v, F64P), _p(s, F64P)),
+               "fastilu_get_factors", self._h)
+        return v[:self.nnz_S], s[:self.n]
+
+    def residual_history(self, cap: int = 4096):
+        h = np.empty(cap)
+        c = C.c_int(0)
+        _check(lib().fastilu_get_residual_history(self._h, _p(h, F64P), cap, C.byref(c)),
+               "fastilu_get_residual_history", self._h)
+        return h[:c.value].copy()
+
+    def timings(self):
+        t = np.zeros(3)
+        _check(lib().fastilu_get_timings(self._h, _p(t, F64P)), "fastilu_get_timings", self._h)
+        return {"init_ms": t[0], "sweeps_ms": t[1], "apply_ms": t[2]}
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().fastilu_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()

@@ -1,0 +1,68 @@
+// Private device-side launch interface of libfastilu_b200 (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace fastilu {
+
+// Local layout: rows of S are stored row-major in one CSR
+// (strict-lower part = L without its unit diagonal, then the diagonal, then the strict upper
+// part of U), local row r <-> global row lbase + r.  Local rows [0, G) are ghost rows of the
+// lower neighbour (multi-GPU only), [G, G + n) are owned.  Column indices are LOCAL
+// (global - lbase); vectors are extended [G ghost | n owned | H upper ghost].
+struct DevPattern {
+  const int64_t *rp;    // nloc + 1
+  const int32_t *ci;    // nnz_loc, local columns
+  const int32_t *dloc;  // nloc: offset of the diagonal inside the row (= #L entries)
+};
+
+struct SweepCfg {
+  int G;        // lanes per row group (8, 16, 32)
+  int warps;    // warps per block
+  int cap_m;    // smem capacity for the row's entries
+  int P;        // pivots staged per chunk
+  int cap_st;   // smem capacity for staged U-row entries per group (P * maxU)
+  int grid;     // blocks
+  size_t smem;  // dynamic smem per block
+};
+
+struct ErrFlags {
+  unsigned long long zero_diag;   // min local row with a_ii == 0
+  unsigned long long zero_pivot;  // min local row with u_ii == 0 / non-finite in an iterate
+};
+
+cudaError_t launch_scale(const int64_t *arp, const int32_t *adiag, const double *aval,
+                         int64_t r0, int64_t r1, double *s, double *ad, ErrFlags *err,
+                         cudaStream_t st);
+
+cudaError_t launch_init(const DevPattern &P, const int64_t *arp, const int32_t *aci,
+                        const int32_t *apos, const double *aval, const double *s,
+                        const double *ad, int64_t r0, int64_t r1, double *ahat, double *vals,
+                        double *udiag, ErrFlags *err, int G, cudaStream_t st);
+
+cudaError_t launch_sweep(const DevPattern &P, const double *ahat, const double *old,
+                         double *out, const double *udiag_old, double *udiag_new, int64_t r0,
+                         int64_t r1, double omega, double *partials, ErrFlags *err,
+                         const SweepCfg &cfg, cudaStream_t st);
+
+cudaError_t launch_reduce(const double *partials, int np, double *dst, cudaStream_t st);
+
+// y = s o b (b indexed by owned row), z1 = omega * y
+cudaError_t launch_trisolve_first_L(const double *b, const double *s, double *y, double *z,
+                                    int64_t r0, int64_t r1, int64_t G, double omega,
+                                    cudaStream_t st);
+// w1 = omega * z / u_ii; if final: x[r - G] = s * w1
+cudaError_t launch_trisolve_first_U(const double *z, const double *udiag, const double *s,
+                                    double *w, double *x, int64_t r0, int64_t r1, int64_t G,
+                                    double omega, bool final, cudaStream_t st);
+cudaError_t launch_jacobi_L(const DevPattern &P, const double *vals, const double *y,
+                            const double *zold, double *znew, int64_t r0, int64_t r1,
+                            double omega, int G, cudaStream_t st);
+cudaError_t launch_jacobi_U(const DevPattern &P, const double *vals, const double *udiag,
+                            const double *z, const double *wold, double *wnew, double *x,
+                            const double *s, int64_t r0, int64_t r1, int64_t Gh, double omega,
+                            bool final, int G, cudaStream_t st);
+
+int sm_count(int device);
+
+}  // namespace fastilu

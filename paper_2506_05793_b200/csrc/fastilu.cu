@@ -1,0 +1,625 @@
+// C ABI of libfastilu_b200 (include/fastilu.h): handle, host setup orchestration, device
+// layouts, and the stream-ordered compute / apply sequences.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <thread>
+#include <vector>
+
+#include "../../include/fastilu.h"
+#include "comm.h"
+#include "device.h"
+#include "host.h"
+
+using namespace fastilu;
+
+struct fastilu_handle_s {
+  int64_t err_index = -1;
+  fastilu_options opt{};
+  int K = 0;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  // partition (global indices)
+  int64_t n = 0, global_n = 0, row_begin = 0, n_lead = 0;
+  int64_t G = 0, H = 0, lbase = 0, nloc = 0, E = 0;
+  int64_t nnz_loc = 0, nnz_own = 0, own_off = 0;  // S entries (local rows), owned rows, offset
+  int64_t nnzA_loc = 0, nnzA_own = 0;
+  int64_t a_in_off = 0, a_in_nnz = 0;  // local A rows inside the caller's value array
+  // host copies (owned rows) for introspection
+  std::vector<int64_t> h_rp;
+  std::vector<int32_t> h_ci;
+  std::vector<int8_t> h_lev;
+  // device structure
+  int64_t *d_rp = nullptr;
+  int32_t *d_ci = nullptr, *d_dloc = nullptr;
+  int64_t *d_arp = nullptr;
+  int32_t *d_aci = nullptr, *d_apos = nullptr, *d_adiag = nullptr;
+  double *d_aval = nullptr;
+  // device values
+  double *d_vals[2] = {nullptr, nullptr}, *d_ud[2] = {nullptr, nullptr}, *d_ahat = nullptr;
+  double *d_s = nullptr, *d_ad = nullptr;
+  double *d_y = nullptr, *d_z[2] = {nullptr, nullptr}, *d_w[2] = {nullptr, nullptr};
+  double *d_bx = nullptr;  // apply_host staging (2 n)
+  double *d_partials = nullptr, *d_r2 = nullptr;
+  int hist_cap = 0;
+  ErrFlags *d_err = nullptr;
+  ErrFlags *h_err = nullptr;  // pinned
+  double *h_r2 = nullptr;     // pinned, hist_cap
+  // launch configuration
+  SweepCfg scfg{};
+  int G_init = 32, G_tri = 32;
+  // state
+  bool have_values = false, computed = false;
+  int cur = 0;
+  std::vector<double> resid;
+  cudaEvent_t ev[5] = {};
+  float t_init = 0.f, t_sweeps = 0.f, t_apply = 0.f;
+  Comm *comm = nullptr;
+};
+
+static const char *kStatus[] = {"FASTILU_OK",          "FASTILU_ERR_INVALID_ARG",
+                                "FASTILU_ERR_BAD_MATRIX", "FASTILU_ERR_MISSING_DIAG",
+                                "FASTILU_ERR_ZERO_DIAG", "FASTILU_ERR_ZERO_PIVOT",
+                                "FASTILU_ERR_STATE",   "FASTILU_ERR_CUDA",
+                                "FASTILU_ERR_NCCL",    "FASTILU_ERR_OOM",
+                                "FASTILU_ERR_UNSUPPORTED"};
+
+extern "C" const char *fastilu_status_string(fastilu_status s) {
+  int i = (int)s;
+  return (i >= 0 && i <= 10) ? kStatus[i] : "FASTILU_UNKNOWN";
+}
+
+extern "C" int64_t fastilu_error_index(fastilu_handle h) { return h ? h->err_index : -1; }
+
+extern "C" void fastilu_default_options(fastilu_options *o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof(*o));
+  o->omega = 1.0;
+  o->omega_tri = 1.0;
+  o->device = -1;
+  o->stream = nullptr;
+  o->num_threads = 0;
+  o->rank = 0;
+  o->nranks = 1;
+  o->comm_kind = FASTILU_COMM_NONE;
+  o->global_n = -1;
+  o->row_begin = 0;
+  o->n_lead = 0;
+}
+
+extern "C" int64_t fastilu_required_lead_rows(int64_t bandwidth, int level_k) {
+  return 2 * (int64_t)(level_k + 1) * std::max<int64_t>(bandwidth, 1);
+}
+
+#define CU(x)                                  \
+  do {                                         \
+    cudaError_t e_ = (x);                      \
+    if (e_ != cudaSuccess) {                   \
+      return e_ == cudaErrorMemoryAllocation   \
+                 ? FASTILU_ERR_OOM             \
+                 : FASTILU_ERR_CUDA;           \
+    }                                          \
+  } while (0)
+
+template <class T>
+static cudaError_t dalloc(T **p, int64_t count) {
+  *p = nullptr;
+  if (count <= 0) count = 1;
+  return cudaMalloc((void **)p, sizeof(T) * (size_t)count);
+}
+
+// --------------------------------------------------------------------------- symbolic (host)
+extern "C" fastilu_status fastilu_symbolic(int64_t n, const int64_t *row_ptr,
+                                           const int32_t *col_idx, int level_k, int num_threads,
+                                           int64_t *nnz_out, int64_t *row_ptr_out,
+                                           int32_t *col_idx_out, int8_t *level_out,
+                                           int64_t *bad_row) {
+  if (bad_row) *bad_row = -1;
+  if (n < 0 || !row_ptr || (n > 0 && !col_idx) || level_k < 0 || level_k > 127)
+    return FASTILU_ERR_INVALID_ARG;
+  int64_t bad = -1;
+  int nt = hw_threads(num_threads);
+  int st = validate_csr(n, row_ptr, col_idx, 0, n, nt, &bad);
+  if (st) {
+    if (bad_row) *bad_row = bad;
+    return (fastilu_status)st;
+  }
+  Pattern pat;
+  st = symbolic_iluk(n, row_ptr, col_idx, 0, 0, n, level_k, nt, pat, &bad);
+  if (st) {
+    if (bad_row) *bad_row = bad;
+    return (fastilu_status)st;
+  }
+  if (nnz_out) *nnz_out = pat.rp[n];
+  if (col_idx_out) {
+    if (row_ptr_out) std::memcpy(row_ptr_out, pat.rp.data(), sizeof(int64_t) * (n + 1));
+    std::memcpy(col_idx_out, pat.ci.data(), sizeof(int32_t) * pat.ci.size());
+    if (level_out) std::memcpy(level_out, pat.lev.data(), pat.lev.size());
+  }
+  return FASTILU_OK;
+}
+
+// --------------------------------------------------------------------------- create
+static fastilu_status setup_configs(fastilu_handle h, int64_t m_max, int64_t maxU, double m_avg,
+                                    double nl_avg) {
+  // sweep: lanes per row from the average row length, pivots staged per chunk from smem
+  int G = m_avg <= 10 ? 8 : (m_avg <= 24 ? 16 : 32);
+  SweepCfg c{};
+  c.G = G;
+  c.cap_m = (int)((m_max + 3) / 4 * 4);
+  if (c.cap_m < 4) c.cap_m = 4;
+  int64_t mU = std::max<int64_t>(maxU, 1);
+  const size_t budget = 16 * 1024;  // staging bytes per group
+  int Pv = (int)std::min<int64_t>(G, std::max<int64_t>(1, (int64_t)(budget / (12 * mU))));
+  c.P = Pv;
+  c.cap_st = (int)(Pv * mU);
+  size_t gbytes = (size_t)c.cap_m * 12 + (size_t)c.cap_st * 12 + (size_t)Pv * 16 + (Pv + 1) * 4;
+  gbytes = (gbytes + 15) & ~(size_t)15;
+  int warps = 4;
+  while (warps > 1 && (size_t)(warps * 32 / G) * gbytes > 200 * 1024) warps /= 2;
+  if ((size_t)(warps * 32 / G) * gbytes > 220 * 1024) return FASTILU_ERR_UNSUPPORTED;
+  c.warps = warps;
+  c.smem = (size_t)(warps * 32 / G) * gbytes;
+  int per_sm = std::max<int>(1, (int)((220 * 1024) / std::max<size_t>(c.smem, 1)));
+  per_sm = std::min(per_sm, 64 / warps);
+  int sms = sm_count(h->device);
+  int64_t gpb = warps * 32 / G;
+  int64_t need = (h->n + gpb - 1) / gpb;
+  c.grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)sms * per_sm));
+  h->scfg = c;
+  h->G_init = G;
+  int gt = 1;
+  while (gt < nl_avg && gt < 32) gt *= 2;
+  h->G_tri = gt;
+  return FASTILU_OK;
+}
+
+static fastilu_status upload_values(fastilu_handle h, const double *values, bool device) {
+  cudaMemcpyKind kind = device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  CU(cudaMemcpyAsync(h->d_aval, values + h->a_in_off, sizeof(double) * h->nnzA_loc, kind,
+                     h->stream));
+  if (!device) CU(cudaStreamSynchronize(h->stream));
+  h->have_values = true;
+  h->computed = false;
+  return FASTILU_OK;
+}
+
+static fastilu_status create_impl(fastilu_handle h, int64_t n, const int64_t *row_ptr,
+                                  const int32_t *col_idx, const double *values, int K) {
+  const fastilu_options &o = h->opt;
+  const bool multi = o.nranks > 1;
+  h->n = n;
+  h->K = K;
+  h->row_begin = multi ? o.row_begin : 0;
+  h->global_n = multi ? o.global_n : n;
+  h->n_lead = multi ? o.n_lead : 0;
+  if (multi) {
+    if (o.global_n <= 0 || o.row_begin < 0 || o.row_begin + n > o.global_n || o.n_lead < 0 ||
+        o.n_lead > o.row_begin || o.rank < 0 || o.rank >= o.nranks)
+      return FASTILU_ERR_INVALID_ARG;
+  }
+  const int nt = hw_threads(o.num_threads);
+  const int64_t g0 = h->row_begin - h->n_lead;
+  const int64_t nrows = h->n_lead + n;
+  const int64_t row_end = h->row_begin + n;
+  int64_t bad = -1;
+  int st = validate_csr(nrows, row_ptr, col_idx, g0, h->global_n, nt, &bad);
+  if (st) {
+    h->err_index = bad;
+    return (fastilu_status)st;
+  }
+  const int64_t bw = half_bandwidth(nrows, row_ptr, col_idx, g0, nt);
+  const int64_t o0 = multi ? std::max(g0, h->row_begin - (int64_t)(K + 1) * std::max<int64_t>(bw, 1))
+                           : 0;
+  Pattern pat;
+  st = symbolic_iluk(nrows, row_ptr, col_idx, g0, o0, row_end, K, nt, pat, &bad);
+  if (st) {
+    h->err_index = bad;
+    return (fastilu_status)st;
+  }
+  // ghost extents
+  const int64_t own_r0 = h->row_begin - o0;  // pattern row index of the first owned row
+  int64_t mincol = h->row_begin, maxcol = row_end - 1;
+  for (int64_t r = own_r0; r < own_r0 + n; r++) {
+    int64_t s = pat.rp[r], e = pat.rp[r + 1];
+    if (e > s) {
+      mincol = std::min<int64_t>(mincol, pat.ci[s]);
+      maxcol = std::max<int64_t>(maxcol, pat.ci[e - 1]);
+    }
+  }
+  h->G = h->row_begin - mincol;
+  h->H = maxcol - (row_end - 1);
+  if (!multi && (h->G != 0 || h->H != 0)) return FASTILU_ERR_BAD_MATRIX;
+  if (h->G > own_r0) return FASTILU_ERR_UNSUPPORTED;  // ghost rows beyond the supplied margin
+  h->lbase = h->row_begin - h->G;
+  h->nloc = h->G + n;
+  h->E = h->nloc + h->H;
+  if (h->E >= (int64_t)INT32_MAX) return FASTILU_ERR_UNSUPPORTED;
+  const int64_t lr0 = own_r0 - h->G;  // pattern row of local row 0
+  const int64_t s_base = pat.rp[lr0];
+  h->nnz_loc = pat.rp[own_r0 + n] - s_base;
+  h->own_off = pat.rp[own_r0] - s_base;
+  h->nnz_own = h->nnz_loc - h->own_off;
+  // local structure
+  std::vector<int64_t> rp(h->nloc + 1);
+  std::vector<int32_t> ci(h->nnz_loc), dloc(h->nloc);
+  int64_t m_max = 0, maxU = 0;
+  for (int64_t r = 0; r <= h->nloc; r++) rp[r] = pat.rp[lr0 + r] - s_base;
+  {
+    std::vector<std::thread> th;
+    int T = std::max(1, std::min<int>(nt, (int)(h->nloc / 4096 + 1)));
+    std::vector<int64_t> mm(T, 0), mu(T, 0);
+    for (int t = 0; t < T; t++)
+      th.emplace_back([&, t]() {
+        int64_t a = h->nloc * t / T, b = h->nloc * (t + 1) / T;
+        for (int64_t r = a; r < b; r++) {
+          const int64_t g = h->lbase + r;
+          int32_t d = -1;
+          for (int64_t p = rp[r]; p < rp[r + 1]; p++) {
+            const int64_t c = pat.ci[s_base + p];
+            ci[p] = (int32_t)(c - h->lbase);  // ghost rows may hold negative (unused) columns
+            if (c == g) d = (int32_t)(p - rp[r]);
+          }
+          dloc[r] = d;
+          mu[t] = std::max<int64_t>(mu[t], rp[r + 1] - rp[r] - d - 1);
+          if (r >= h->G) mm[t] = std::max<int64_t>(mm[t], rp[r + 1] - rp[r]);
+        }
+      });
+    for (auto &x : th) x.join();
+    for (int t = 0; t < T; t++) {
+      m_max = std::max(m_max, mm[t]);
+      maxU = std::max(maxU, mu[t]);
+    }
+  }
+  // host copies of the owned rows (introspection)
+  h->h_rp.resize(n + 1);
+  for (int64_t r = 0; r <= n; r++) h->h_rp[r] = pat.rp[own_r0 + r] - pat.rp[own_r0];
+  h->h_ci.assign(pat.ci.begin() + pat.rp[own_r0], pat.ci.begin() + pat.rp[own_r0 + n]);
+  h->h_lev.assign(pat.lev.begin() + pat.rp[own_r0], pat.lev.begin() + pat.rp[own_r0 + n]);
+  // A layout for local rows [lbase, row_end): arp, adiag; owned rows: aci (local), apos
+  const int64_t ar0 = h->lbase - g0;  // caller row index of local row 0
+  h->a_in_off = row_ptr[ar0];
+  h->a_in_nnz = row_ptr[nrows];
+  h->nnzA_loc = row_ptr[ar0 + h->nloc] - h->a_in_off;
+  std::vector<int64_t> arp(h->nloc + 1);
+  std::vector<int32_t> adiag(h->nloc), aci(h->nnzA_loc, 0), apos(h->nnzA_loc, 0);
+  for (int64_t r = 0; r <= h->nloc; r++) arp[r] = row_ptr[ar0 + r] - h->a_in_off;
+  {
+    std::vector<std::thread> th;
+    int T = std::max(1, std::min<int>(nt, (int)(h->nloc / 4096 + 1)));
+    std::vector<int> fail(T, 0);
+    for (int t = 0; t < T; t++)
+      th.emplace_back([&, t]() {
+        int64_t a = h->nloc * t / T, b = h->nloc * (t + 1) / T;
+        for (int64_t r = a; r < b; r++) {
+          const int64_t g = h->lbase + r;
+          const int64_t q0 = h->a_in_off + arp[r], q1 = h->a_in_off + arp[r + 1];
+          for (int64_t q = q0; q < q1; q++)
+            if (col_idx[q] == g) adiag[r] = (int32_t)(q - q0);
+          if (r < h->G) continue;
+          int64_t p = rp[r];
+          for (int64_t q = q0; q < q1; q++) {
+            const int64_t c = col_idx[q] - h->lbase;
+            while (p < rp[r + 1] && ci[p] < c) p++;
+            if (p == rp[r + 1] || ci[p] != c) {
+              fail[t] = 1;
+              break;
+            }
+            aci[q - h->a_in_off] = (int32_t)c;
+            apos[q - h->a_in_off] = (int32_t)(p - rp[r]);
+          }
+        }
+      });
+    for (auto &x : th) x.join();
+    for (int t = 0; t < T; t++)
+      if (fail[t]) return FASTILU_ERR_BAD_MATRIX;  // S must contain A (cannot happen)
+  }
+  int64_t nl_own = 0;
+  for (int64_t r = h->G; r < h->nloc; r++) nl_own += dloc[r];
+  const double m_avg = n ? (double)h->nnz_own / n : 1.0;
+  const double nl_avg = n ? (double)nl_own / n : 1.0;
+  fastilu_status fs = setup_configs(h, m_max, maxU, m_avg, nl_avg);
+  if (fs) return fs;
+  // device allocations
+  CU(dalloc(&h->d_rp, h->nloc + 1));
+  CU(dalloc(&h->d_ci, h->nnz_loc));
+  CU(dalloc(&h->d_dloc, h->nloc));
+  CU(dalloc(&h->d_arp, h->nloc + 1));
+  CU(dalloc(&h->d_aci, h->nnzA_loc));
+  CU(dalloc(&h->d_apos, h->nnzA_loc));
+  CU(dalloc(&h->d_adiag, h->nloc));
+  CU(dalloc(&h->d_aval, h->nnzA_loc));
+  for (int b = 0; b < 2; b++) {
+    CU(dalloc(&h->d_vals[b], h->nnz_loc));
+    CU(dalloc(&h->d_ud[b], h->E));
+    CU(dalloc(&h->d_z[b], h->E));
+    CU(dalloc(&h->d_w[b], h->E));
+  }
+  CU(dalloc(&h->d_ahat, h->nnz_loc));
+  CU(dalloc(&h->d_s, h->E));
+  CU(dalloc(&h->d_ad, h->E));
+  CU(dalloc(&h->d_y, h->E));
+  CU(dalloc(&h->d_partials, h->scfg.grid));
+  CU(dalloc(&h->d_err, 1));
+  CU(cudaMallocHost((void **)&h->h_err, sizeof(ErrFlags)));
+  CU(cudaMemcpy(h->d_rp, rp.data(), sizeof(int64_t) * rp.size(), cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(h->d_ci, ci.data(), sizeof(int32_t) * ci.size(), cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(h->d_dloc, dloc.data(), sizeof(int32_t) * dloc.size(), cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(h->d_arp, arp.data(), sizeof(int64_t) * arp.size(), cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(h->d_aci, aci.data(), sizeof(int32_t) * aci.size(), cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(h->d_apos, apos.data(), sizeof(int32_t) * apos.size(), cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(h->d_adiag, adiag.data(), sizeof(int32_t) * adiag.size(),
+                cudaMemcpyHostToDevice));
+  CU(cudaMemset(h->d_s, 0, sizeof(double) * h->E));
+  CU(cudaMemset(h->d_ad, 0, sizeof(double) * h->E));
+  for (int b = 0; b < 2; b++) {
+    CU(cudaMemset(h->d_ud[b], 0, sizeof(double) * h->E));
+    CU(cudaMemset(h->d_z[b], 0, sizeof(double) * h->E));
+    CU(cudaMemset(h->d_w[b], 0, sizeof(double) * h->E));
+  }
+  for (int i = 0; i < 5; i++) CU(cudaEventCreate(&h->ev[i]));
+  if (multi) {
+    fastilu_status cs = comm_setup(h->comm, h->opt, h->row_begin, h->n, h->G, h->H, h->stream);
+    if (cs) return cs;
+  }
+  if (values) return upload_values(h, values, false);
+  return FASTILU_OK;
+}
+
+extern "C" fastilu_status fastilu_create(fastilu_handle *out, int64_t n, const int64_t *row_ptr,
+                                         const int32_t *col_idx, const double *values,
+                                         int level_k, const fastilu_options *opts) {
+  if (!out) return FASTILU_ERR_INVALID_ARG;
+  *out = nullptr;
+  fastilu_handle h = new (std::nothrow) fastilu_handle_s();
+  if (!h) return FASTILU_ERR_OOM;
+  *out = h;
+  if (opts) h->opt = *opts; else fastilu_default_options(&h->opt);
+  if (n < 0 || !row_ptr || (n > 0 && !col_idx) || level_k < 0 || level_k > 127 ||
+      h->opt.nranks < 1 || !(h->opt.omega > 0.0 && h->opt.omega <= 1.0) ||
+      !(h->opt.omega_tri > 0.0 && h->opt.omega_tri <= 1.0))
+    return FASTILU_ERR_INVALID_ARG;
+  if (h->opt.device >= 0) {
+    if (cudaSetDevice(h->opt.device) != cudaSuccess) return FASTILU_ERR_CUDA;
+    h->device = h->opt.device;
+  } else {
+    if (cudaGetDevice(&h->device) != cudaSuccess) return FASTILU_ERR_CUDA;
+  }
+  if (h->opt.stream) {
+    h->stream = (cudaStream_t)h->opt.stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess)
+      return FASTILU_ERR_CUDA;
+    h->own_stream = true;
+  }
+  return create_impl(h, n, row_ptr, col_idx, values, level_k);
+}
+
+extern "C" fastilu_status fastilu_set_values(fastilu_handle h, const double *values) {
+  if (!h || !values || !h->d_aval) return FASTILU_ERR_INVALID_ARG;
+  cudaSetDevice(h->device);
+  return upload_values(h, values, false);
+}
+
+extern "C" fastilu_status fastilu_set_values_device(fastilu_handle h, const double *values) {
+  if (!h || !values || !h->d_aval) return FASTILU_ERR_INVALID_ARG;
+  cudaSetDevice(h->device);
+  return upload_values(h, values, true);
+}
+
+// --------------------------------------------------------------------------- compute
+extern "C" fastilu_status fastilu_compute(fastilu_handle h, int nsweeps) {
+  if (!h || nsweeps < 0) return FASTILU_ERR_INVALID_ARG;
+  if (!h->have_values || !h->d_aval) return FASTILU_ERR_STATE;
+  cudaSetDevice(h->device);
+  h->computed = false;
+  h->err_index = -1;
+  cudaStream_t st = h->stream;
+  if (nsweeps > h->hist_cap) {
+    if (h->d_r2) cudaFree(h->d_r2);
+    if (h->h_r2) cudaFreeHost(h->h_r2);
+    h->d_r2 = nullptr;
+    h->h_r2 = nullptr;
+    CU(dalloc(&h->d_r2, nsweeps));
+    CU(cudaMallocHost((void **)&h->h_r2, sizeof(double) * nsweeps));
+    h->hist_cap = nsweeps;
+  }
+  CU(cudaMemsetAsync(h->d_err, 0xff, sizeof(ErrFlags), st));
+  DevPattern P{h->d_rp, h->d_ci, h->d_dloc};
+  const int64_t r0 = h->G, r1 = h->G + h->n;
+  CU(cudaEventRecord(h->ev[0], st));
+  // a2: scaling for every local row (lower ghosts included), then the upper ghosts' s / ad
+  CU(launch_scale(h->d_arp, h->d_adiag, h->d_aval, 0, h->nloc, h->d_s, h->d_ad, h->d_err, st));
+  if (h->comm) {
+    fastilu_status cs = comm_vector_halo(h->comm, h->d_s, st, true, true);
+    if (cs) return cs;
+    cs = comm_vector_halo(h->comm, h->d_ad, st, true, true);
+    if (cs) return cs;
+  }
+  // a3: ahat on S and the initial guess (iterate 0) for the owned rows
+  CU(launch_init(P, h->d_arp, h->d_aci, h->d_apos, h->d_aval, h->d_s, h->d_ad, r0, r1,
+                 h->d_ahat, h->d_vals[0], h->d_ud[0], h->d_err, h->G_init, st));
+  CU(cudaEventRecord(h->ev[1], st));
+  // a4/a5: nsweeps synchronous sweeps, ping-pong buffers
+  for (int sw = 1; sw <= nsweeps; sw++) {
+    const int ib = (sw - 1) & 1, ob = sw & 1;
+    if (h->comm) {
+      fastilu_status cs = comm_factor_halo(h->comm, h->d_vals[ib], h->d_rp, h->d_ud[ib], st);
+      if (cs) return cs;
+    }
+    CU(launch_sweep(P, h->d_ahat, h->d_vals[ib], h->d_vals[ob], h->d_ud[ib], h->d_ud[ob], r0, r1,
+                    h->opt.omega, h->d_partials, h->d_err, h->scfg, st));
+    CU(launch_reduce(h->d_partials, h->scfg.grid, h->d_r2 + (sw - 1), st));
+  }
+  CU(cudaEventRecord(h->ev[2], st));
+  CU(cudaMemcpyAsync(h->h_err, h->d_err, sizeof(ErrFlags), cudaMemcpyDeviceToHost, st));
+  if (nsweeps)
+    CU(cudaMemcpyAsync(h->h_r2, h->d_r2, sizeof(double) * nsweeps, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  CU(cudaEventElapsedTime(&h->t_init, h->ev[0], h->ev[1]));
+  CU(cudaEventElapsedTime(&h->t_sweeps, h->ev[1], h->ev[2]));
+  h->resid.assign(nsweeps, 0.0);
+  std::vector<double> r2(h->h_r2, h->h_r2 + nsweeps);
+  ErrFlags ef = *h->h_err;
+  if (h->comm) {
+    fastilu_status cs = comm_allreduce_host(h->comm, r2.data(), (int)r2.size(), ef);
+    if (cs) return cs;
+  }
+  for (int i = 0; i < nsweeps; i++) h->resid[i] = std::sqrt(r2[i]);
+  h->cur = nsweeps & 1;
+  if (ef.zero_diag != ~0ull) {
+    h->err_index = (int64_t)ef.zero_diag + h->lbase;
+    return FASTILU_ERR_ZERO_DIAG;
+  }
+  if (ef.zero_pivot != ~0ull) {
+    h->err_index = (int64_t)ef.zero_pivot + h->lbase;
+    return FASTILU_ERR_ZERO_PIVOT;
+  }
+  h->computed = true;
+  return FASTILU_OK;
+}
+
+// --------------------------------------------------------------------------- apply
+static fastilu_status apply_impl(fastilu_handle h, const double *b, double *x, int ntri) {
+  cudaStream_t st = h->stream;
+  DevPattern P{h->d_rp, h->d_ci, h->d_dloc};
+  const int64_t r0 = h->G, r1 = h->G + h->n;
+  const double om = h->opt.omega_tri;
+  const double *vals = h->d_vals[h->cur];
+  const double *ud = h->d_ud[h->cur];
+  // a8: L sweeps.  t = 1: z1 = w y with y = s o b (z0 = 0)
+  CU(launch_trisolve_first_L(b, h->d_s, h->d_y, h->d_z[0], r0, r1, h->G, om, st));
+  for (int t = 2; t <= ntri; t++) {
+    const double *zo = h->d_z[(t - 2) & 1];
+    if (h->comm) {
+      fastilu_status cs = comm_vector_halo(h->comm, h->d_z[(t - 2) & 1], st, true, false);
+      if (cs) return cs;
+    }
+    CU(launch_jacobi_L(P, vals, h->d_y, zo, h->d_z[(t - 1) & 1], r0, r1, om, h->G_tri, st));
+  }
+  const double *zf = h->d_z[(ntri - 1) & 1];
+  // a9: U sweeps.  t = 1: w1 = w z / u_ii; the last sweep writes x = s o w
+  CU(launch_trisolve_first_U(zf, ud, h->d_s, h->d_w[0], x, r0, r1, h->G, om, ntri == 1, st));
+  for (int t = 2; t <= ntri; t++) {
+    if (h->comm) {
+      fastilu_status cs = comm_vector_halo(h->comm, h->d_w[(t - 2) & 1], st, false, true);
+      if (cs) return cs;
+    }
+    CU(launch_jacobi_U(P, vals, ud, zf, h->d_w[(t - 2) & 1], h->d_w[(t - 1) & 1], x, h->d_s, r0,
+                       r1, h->G, om, t == ntri, h->G_tri, st));
+  }
+  return FASTILU_OK;
+}
+
+extern "C" fastilu_status fastilu_apply(fastilu_handle h, const double *b, double *x,
+                                        int ntrisweeps) {
+  if (!h || ntrisweeps < 1 || (h->n > 0 && (!b || !x))) return FASTILU_ERR_INVALID_ARG;
+  if (!h->computed) return FASTILU_ERR_STATE;
+  cudaSetDevice(h->device);
+  CU(cudaEventRecord(h->ev[3], h->stream));
+  fastilu_status s = apply_impl(h, b, x, ntrisweeps);
+  if (s) return s;
+  CU(cudaEventRecord(h->ev[4], h->stream));
+  return FASTILU_OK;
+}
+
+extern "C" fastilu_status fastilu_apply_host(fastilu_handle h, const double *b, double *x,
+                                             int ntrisweeps) {
+  if (!h || ntrisweeps < 1 || (h->n > 0 && (!b || !x))) return FASTILU_ERR_INVALID_ARG;
+  if (!h->computed) return FASTILU_ERR_STATE;
+  cudaSetDevice(h->device);
+  if (!h->d_bx) CU(dalloc(&h->d_bx, 2 * h->n));
+  CU(cudaMemcpyAsync(h->d_bx, b, sizeof(double) * h->n, cudaMemcpyHostToDevice, h->stream));
+  CU(cudaEventRecord(h->ev[3], h->stream));
+  fastilu_status s = apply_impl(h, h->d_bx, h->d_bx + h->n, ntrisweeps);
+  if (s) return s;
+  CU(cudaEventRecord(h->ev[4], h->stream));
+  CU(cudaMemcpyAsync(x, h->d_bx + h->n, sizeof(double) * h->n, cudaMemcpyDeviceToHost,
+                     h->stream));
+  CU(cudaStreamSynchronize(h->stream));
+  return FASTILU_OK;
+}
+
+// --------------------------------------------------------------------------- introspection
+extern "C" fastilu_status fastilu_get_sizes(fastilu_handle h, int64_t *n, int64_t *nnz_S,
+                                            int64_t *nnz_A) {
+  if (!h) return FASTILU_ERR_INVALID_ARG;
+  if (n) *n = h->n;
+  if (nnz_S) *nnz_S = (int64_t)h->h_ci.size();
+  if (nnz_A) {
+    // A entries of the owned rows
+    *nnz_A = h->nnzA_loc;
+    if (h->G && h->d_arp) {
+      int64_t g = 0;
+      cudaMemcpy(&g, h->d_arp + h->G, sizeof(int64_t), cudaMemcpyDeviceToHost);
+      *nnz_A -= g;
+    }
+  }
+  return FASTILU_OK;
+}
+
+extern "C" fastilu_status fastilu_get_pattern(fastilu_handle h, int64_t *row_ptr,
+                                              int32_t *col_idx, int8_t *level) {
+  if (!h) return FASTILU_ERR_INVALID_ARG;
+  if (row_ptr) std::memcpy(row_ptr, h->h_rp.data(), sizeof(int64_t) * h->h_rp.size());
+  if (col_idx) std::memcpy(col_idx, h->h_ci.data(), sizeof(int32_t) * h->h_ci.size());
+  if (level) std::memcpy(level, h->h_lev.data(), h->h_lev.size());
+  return FASTILU_OK;
+}
+
+extern "C" fastilu_status fastilu_get_factors(fastilu_handle h, double *vals, double *s) {
+  if (!h) return FASTILU_ERR_INVALID_ARG;
+  if (!h->computed) return FASTILU_ERR_STATE;
+  cudaSetDevice(h->device);
+  CU(cudaStreamSynchronize(h->stream));
+  if (vals)
+    CU(cudaMemcpy(vals, h->d_vals[h->cur] + h->own_off, sizeof(double) * h->nnz_own,
+                  cudaMemcpyDeviceToHost));
+  if (s) CU(cudaMemcpy(s, h->d_s + h->G, sizeof(double) * h->n, cudaMemcpyDeviceToHost));
+  return FASTILU_OK;
+}
+
+extern "C" fastilu_status fastilu_get_residual_history(fastilu_handle h, double *hist, int cap,
+                                                       int *count) {
+  if (!h) return FASTILU_ERR_INVALID_ARG;
+  int c = std::min<int>(cap, (int)h->resid.size());
+  for (int i = 0; i < c; i++) hist[i] = h->resid[i];
+  if (count) *count = c;
+  return FASTILU_OK;
+}
+
+extern "C" fastilu_status fastilu_get_timings(fastilu_handle h, double *t3) {
+  if (!h || !t3) return FASTILU_ERR_INVALID_ARG;
+  cudaSetDevice(h->device);
+  float ta = 0.f;
+  if (cudaEventQuery(h->ev[4]) == cudaSuccess) cudaEventElapsedTime(&ta, h->ev[3], h->ev[4]);
+  t3[0] = h->t_init;
+  t3[1] = h->t_sweeps;
+  t3[2] = ta;
+  return FASTILU_OK;
+}
+
+extern "C" fastilu_status fastilu_destroy(fastilu_handle h) {
+  if (!h) return FASTILU_OK;
+  cudaSetDevice(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  if (h->comm) comm_destroy(h->comm);
+  void *ptrs[] = {h->d_rp,    h->d_ci,    h->d_dloc,     h->d_arp,  h->d_aci,     h->d_apos,
+                  h->d_adiag, h->d_aval,  h->d_vals[0],  h->d_vals[1], h->d_ud[0], h->d_ud[1],
+                  h->d_ahat,  h->d_s,     h->d_ad,       h->d_y,    h->d_z[0],    h->d_z[1],
+                  h->d_w[0],  h->d_w[1],  h->d_bx,       h->d_partials, h->d_r2,  h->d_err};
+  for (void *p : ptrs)
+    if (p) cudaFree(p);
+  if (h->h_err) cudaFreeHost(h->h_err);
+  if (h->h_r2) cudaFreeHost(h->h_r2);
+  for (int i = 0; i < 5; i++)
+    if (h->ev[i]) cudaEventDestroy(h->ev[i]);
+  if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+  return FASTILU_OK;
+}

@@ -1,0 +1,91 @@
+"""CPU-only checks of the C-ABI library: it loads, exports every symbol include/fastilu.h declares,
+and its host-side setup (validation + the product's own symbolic ILU(k), an independent
+implementation: sorted linked lists, chunk-parallel windows) matches the oracle bit-exactly.
+No compute call needs a GPU here."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2506_05793_b200 as F
+import problems as P
+
+
+def test_library_exports_every_header_symbol():
+    L = F.lib()
+    names = F.header_functions()
+    assert len(names) >= 20
+    for name in names:
+        assert hasattr(L, name), name
+    assert set(F._SIGS) == set(names)
+
+
+def test_status_strings_and_defaults():
+    assert F.fastilu_status_string(0) == "FASTILU_OK"
+    assert F.fastilu_status_string(5) == "FASTILU_ERR_ZERO_PIVOT"
+    o = F.fastilu_default_options()
+    assert (o.omega, o.omega_tri, o.device, o.nranks) == (1.0, 1.0, -1, 1)
+    assert F.fastilu_required_lead_rows(10, 1) == 40
+
+
+def _same_pattern(a, k, threads=0):
+    rp, ci, lev = F.fastilu_symbolic(a.row_ptr, a.col_idx, k, threads)
+    pat = oracle.symbolic(a.row_ptr, a.col_idx, k)
+    assert np.array_equal(rp, pat.row_ptr)
+    assert np.array_equal(ci, pat.col_idx)
+    assert np.array_equal(lev.astype(np.int32), pat.level)
+
+
+@pytest.mark.parametrize("kind,g,k", [("7pt", 10, 0), ("7pt", 9, 2), ("27pt", 7, 1),
+                                       ("27pt", 6, 2), ("27pt", 5, 3), ("aniso7pt", 8, 1),
+                                       ("3dof", 5, 2)])
+def test_symbolic_matches_oracle(kind, g, k):
+    _same_pattern(P.make(kind, g), k)
+
+
+@pytest.mark.parametrize("seed,k", [(1, 0), (2, 1), (3, 2), (4, 4)])
+def test_symbolic_matches_oracle_random(seed, k):
+    _same_pattern(P.random_sparse(300, 0.01, seed=seed), k)
+
+
+@pytest.mark.parametrize("threads", [1, 3, 8])
+def test_symbolic_chunk_parallel_exact(threads):
+    # n = 110,592 > 65,536: the chunked windows are used; their rows must be exact
+    _same_pattern(P.laplace3d_27pt(48), 1, threads)
+
+
+def test_symbolic_chunk_parallel_exact_ilu2_ragged():
+    # 40 x 40 x 45 grid (ragged in z), ILU(2): several chunks with 6 (K+1) bandwidth margins
+    _same_pattern(P.laplace3d_27pt(40, gz=45), 2, 5)
+
+
+def test_symbolic_errors():
+    a = P.laplace3d_7pt(4)
+    rp, ci = a.row_ptr.copy(), a.col_idx.copy()
+    s, e = rp[7], rp[8]
+    d = s + int(np.searchsorted(ci[s:e], 7))
+    ci2 = np.delete(ci, d)
+    rp2 = rp.copy()
+    rp2[8:] -= 1
+    with pytest.raises(F.FastILUError) as ei:
+        F.fastilu_symbolic(rp2, ci2, 1)
+    assert ei.value.status == "MISSING_DIAG" and ei.value.index == 7
+    ci3 = ci.copy()
+    ci3[rp[3]], ci3[rp[3] + 1] = ci3[rp[3] + 1], ci3[rp[3]]
+    with pytest.raises(F.FastILUError) as ei:
+        F.fastilu_symbolic(rp, ci3, 0)
+    assert ei.value.status == "BAD_MATRIX" and ei.value.index == 3
+    with pytest.raises(F.FastILUError) as ei:
+        F.fastilu_symbolic(rp, ci, -1)
+    assert ei.value.status == "INVALID_ARG"
+
+
+def test_create_without_gpu_fails_loudly():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    a = P.laplace3d_7pt(3)
+    with pytest.raises(F.FastILUError) as ei:
+        F.FastILU(a.row_ptr, a.col_idx, a.values, 0)
+    assert ei.value.status == "CUDA"

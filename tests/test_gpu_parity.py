@@ -1,0 +1,184 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle, element by element.
+
+Tolerance (north_star): factors per entry |g - o| <= 1e-12 |o| (and g == o
+where o == 0); x per entry <= 1e-12 |o| with b > 0; pattern bit-exact.  The factor kernels use
+the oracle's operation order, so factors are in fact expected bitwise equal (asserted
+separately).  Inputs: seeded generators in problems/ only.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2506_05793_b200 as F
+import problems as P
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-12
+
+
+def gpu_run(a, k, ns, nt=0, b=None, omega=1.0, omega_tri=1.0, alias=False):
+    f = F.FastILU(a.row_ptr, a.col_idx, a.values, k, omega=omega, omega_tri=omega_tri)
+    f.compute(ns)
+    vals, s = f.factors()
+    x = None
+    if b is not None:
+        tb = torch.tensor(b, dtype=torch.float64, device="cuda")
+        tx = tb if alias else torch.empty_like(tb)
+        f.apply(tb, tx, nt)
+        torch.cuda.synchronize()
+        x = tx.cpu().numpy()
+    return f, vals, s, x
+
+
+def assert_rel(g, o, rtol=RTOL, what=""):
+    g, o = np.asarray(g), np.asarray(o)
+    assert g.shape == o.shape, what
+    zero = o == 0
+    assert np.array_equal(g[zero], o[zero]), f"{what}: entries that are exactly 0 in the oracle"
+    err = np.abs(g - o) / np.where(zero, 1.0, np.abs(o))
+    i = int(np.argmax(err)) if err.size else 0
+    assert err.size == 0 or err.max() <= rtol, f"{what}: max rel err {err.max():.3e} at {i}"
+
+
+def full_check(a, k, ns, nt, omega=1.0, omega_tri=1.0, bitwise=True):
+    b = P.rhs_positive(a.n)
+    f, vals, s, x = gpu_run(a, k, ns, nt, b, omega, omega_tri)
+    fo = oracle.compute(a, k, ns, omega)
+    rp, ci, lev = f.pattern()
+    assert np.array_equal(rp, fo.pattern.row_ptr)
+    assert np.array_equal(ci, fo.pattern.col_idx)
+    assert np.array_equal(lev.astype(np.int32), fo.pattern.level)
+    assert np.array_equal(s, fo.s)
+    assert_rel(vals, fo.vals, what="factors")
+    if bitwise:
+        assert np.array_equal(vals, fo.vals), "factors not bitwise equal to the oracle"
+    np.testing.assert_allclose(f.residual_history(), fo.resid, rtol=1e-12)
+    xo = oracle.apply(fo, b, nt, omega_tri)
+    assert_rel(x, xo, what="x")
+    return f
+
+
+# ------------------------------------------------------------------ BASELINE configs[0]
+def test_config1_7pt_10_ilu0():
+    full_check(P.laplace3d_7pt(10), 0, 3, 5)
+
+
+@pytest.mark.parametrize("kind,g,gz,k,ns,nt", [
+    ("27pt", 12, None, 1, 3, 5),
+    ("27pt", 10, None, 2, 3, 5),
+    ("27pt", 9, 13, 1, 4, 3),       # ragged grid
+    ("aniso7pt", 16, None, 0, 2, 5),
+    ("7pt", 17, None, 1, 3, 5),
+    ("7pt", 11, None, 2, 2, 4),
+    ("27pt", 8, None, 3, 2, 2),
+])
+def test_stencils(kind, g, gz, k, ns, nt):
+    full_check(P.make(kind, g, gz), k, ns, nt)
+
+
+def test_3dof_pattern():
+    full_check(P.elasticity_pattern_3dof(5), 1, 3, 3)
+
+
+@pytest.mark.parametrize("seed,k", [(11, 0), (12, 2)])
+def test_random_sparse(seed, k):
+    full_check(P.random_sparse(700, 0.006, seed=seed), k, 3, 4)
+
+
+def test_damping():
+    full_check(P.laplace3d_27pt(9), 1, 4, 5, omega=0.7, omega_tri=0.8)
+
+
+@pytest.mark.parametrize("nt", [1, 2])
+def test_few_trisweeps(nt):
+    full_check(P.laplace3d_7pt(12), 0, 2, nt)
+
+
+def test_zero_and_many_sweeps():
+    full_check(P.laplace3d_27pt(6), 1, 0, 3)
+    full_check(P.laplace3d_27pt(6), 1, 40, 30)  # converged to the exact ILU
+
+
+def test_sweeps_reach_exact_ilu_on_gpu():
+    a = P.laplace3d_7pt(6)
+    f, vals, s, _ = gpu_run(a, 0, 60)
+    pat = oracle.symbolic(a.row_ptr, a.col_idx, 0)
+    _, ahat, _ = oracle.scale_init(a, pat)
+    assert np.array_equal(vals, oracle.exact_ilu(pat, ahat))
+
+
+def test_alias_and_host_apply():
+    a = P.laplace3d_27pt(8)
+    b = P.rhs_positive(a.n)
+    f, _, _, x1 = gpu_run(a, 1, 3, 5, b)
+    _, _, _, x2 = gpu_run(a, 1, 3, 5, b, alias=True)
+    assert np.array_equal(x1, x2)
+    assert np.array_equal(f.apply_host(b, 5), x1)
+
+
+def test_signed_rhs_componentwise():
+    a = P.laplace3d_27pt(9)
+    b = P.rhs_signed(a.n)
+    f, vals, s, x = gpu_run(a, 1, 3, 5, b)
+    fo = oracle.compute(a, 1, 3)
+    xo = oracle.apply(fo, b, 5)
+    # componentwise bound for signed data
+    assert np.abs(x - xo).max() <= 1e-12 * np.abs(xo).max()
+
+
+def test_determinism_and_set_values():
+    a = P.laplace3d_27pt(10)
+    f = F.FastILU(a.row_ptr, a.col_idx, a.values, 1)
+    f.compute(3)
+    v1, _ = f.factors()
+    f.compute(3)
+    v2, _ = f.factors()
+    assert np.array_equal(v1, v2)
+    a2v = a.values * np.linspace(1.0, 2.0, a.nnz)
+    a2 = P.Csr(a.row_ptr, a.col_idx, a2v)
+    f.set_values(a2v)
+    f.compute(3)
+    v3, _ = f.factors()
+    assert_rel(v3, oracle.compute(a2, 1, 3).vals)
+    tv = torch.tensor(a.values, device="cuda")
+    f.set_values_device(tv)
+    f.compute(3)
+    assert np.array_equal(f.factors()[0], v1)
+
+
+def test_tiny_and_diagonal():
+    full_check(P.Csr([0, 1], [0], [4.0]), 0, 2, 2)
+    n = 37
+    full_check(P.Csr(np.arange(n + 1), np.arange(n), np.linspace(-3, 5, n) + 0.5), 0, 1, 1)
+    full_check(P.tridiagonal(300), 1, 5, 5)
+
+
+def test_errors():
+    a = P.laplace3d_7pt(4)
+    v = a.values.copy()
+    s, e = a.row_ptr[9], a.row_ptr[10]
+    v[s + int(np.searchsorted(a.col_idx[s:e], 9))] = 0.0
+    f = F.FastILU(a.row_ptr, a.col_idx, v, 0)
+    with pytest.raises(F.FastILUError) as ei:
+        f.compute(1)
+    assert ei.value.status == "ZERO_DIAG" and ei.value.index == 9
+    tb = torch.ones(a.n, dtype=torch.float64, device="cuda")
+    with pytest.raises(F.FastILUError) as ei:
+        f.apply(tb, tb, 1)
+    assert ei.value.status == "STATE"
+    z = P.Csr([0, 2, 4], [0, 1, 0, 1], [1.0, 1.0, 1.0, 1.0])
+    g = F.FastILU(z.row_ptr, z.col_idx, z.values, 0)
+    g.compute(0)
+    with pytest.raises(F.FastILUError) as ei:
+        g.compute(1)
+    assert ei.value.status == "ZERO_PIVOT" and ei.value.index == 1
+    with pytest.raises(oracle.OracleError) as eo:
+        oracle.compute(z, 0, 1)
+    assert eo.value.index == 1
+
+
+def test_config2_full_size_7pt_128_ilu0():
+    """BASELINE configs[1] at full size (n = 2,097,152), element by element."""
+    full_check(P.laplace3d_7pt(128), 0, 3, 5)
