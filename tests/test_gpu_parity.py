@@ -54,7 +54,11 @@ def full_check(a, k, ns, nt, omega=1.0, omega_tri=1.0, bitwise=True):
     assert_rel(vals, fo.vals, what="factors")
     if bitwise:
         assert np.array_equal(vals, fo.vals), "factors not bitwise equal to the oracle"
-    np.testing.assert_allclose(f.residual_history(), fo.resid, rtol=1e-12)
+    # r(s-1) is ONE scalar reduced over nnz(S) squares: the oracle's left-to-right sum is itself
+    # only accurate to gamma_N = N eps (Higham, recursive summation of non-negative terms), the
+    # GPU's tree sum to ~log2(N) eps; DESIGN.md "Tolerance".
+    rtol_r = max(1e-12, (fo.pattern.nnz + 64) * np.finfo(float).eps)
+    np.testing.assert_allclose(f.residual_history(), fo.resid, rtol=rtol_r)
     xo = oracle.apply(fo, b, nt, omega_tri)
     assert_rel(x, xo, what="x")
     return f
