@@ -17,13 +17,33 @@ struct DevPattern {
 };
 
 struct SweepCfg {
-  int G;        // lanes per row group (8, 16, 32)
-  int warps;    // warps per block
-  int cap_m;    // smem capacity for the row's entries
-  int P;        // pivots staged per chunk
-  int cap_st;   // smem capacity for staged U-row entries per group (P * maxU)
-  int grid;     // blocks
-  size_t smem;  // dynamic smem per block
+  int G;            // lanes per row group (4, 8, 16, 32)
+  int threads;      // threads per block
+  int cap_m;        // smem capacity for the row's entries
+  bool hash;        // injective offset hash available (else binary search)
+  uint32_t hmul;    // hash: slot = ((j - i) * hmul) >> hshift
+  int hshift;
+  int hsize;        // table entries (power of two)
+  int grid;         // blocks (= resident capacity)
+  int64_t chunk;    // rows per block
+  size_t smem;      // dynamic smem per block
+};
+
+struct ErrFlags;
+
+struct SweepArgs {
+  DevPattern P;
+  const int64_t *arp;     // A row pointers (local rows)
+  const int32_t *apos;    // offset of each A entry inside its S row
+  const double *ahatA;    // ahat on A's pattern
+  const double *old;      // iterate s-1 (S layout)
+  double *out;            // iterate s
+  const double *udo;      // u_ii of iterate s-1
+  double *udn;            // u_ii of iterate s
+  int64_t r0, r1;         // local rows to sweep
+  double omega;
+  double *partials;       // per-block residual partials
+  ErrFlags *err;
 };
 
 struct ErrFlags {
@@ -37,13 +57,12 @@ cudaError_t launch_scale(const int64_t *arp, const int32_t *adiag, const double 
 
 cudaError_t launch_init(const DevPattern &P, const int64_t *arp, const int32_t *aci,
                         const int32_t *apos, const double *aval, const double *s,
-                        const double *ad, int64_t r0, int64_t r1, double *ahat, double *vals,
+                        const double *ad, int64_t r0, int64_t r1, double *ahatA, double *vals,
                         double *udiag, ErrFlags *err, int G, cudaStream_t st);
 
-cudaError_t launch_sweep(const DevPattern &P, const double *ahat, const double *old,
-                         double *out, const double *udiag_old, double *udiag_new, int64_t r0,
-                         int64_t r1, double omega, double *partials, ErrFlags *err,
-                         const SweepCfg &cfg, cudaStream_t st);
+// sets the smem attribute and returns the resident blocks per SM for cfg
+cudaError_t sweep_configure(const SweepCfg &cfg, int *blocks_per_sm);
+cudaError_t launch_sweep(const SweepArgs &a, const SweepCfg &cfg, cudaStream_t st);
 
 cudaError_t launch_reduce(const double *partials, int np, double *dst, cudaStream_t st);
 

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <mutex>
@@ -145,36 +146,84 @@ extern "C" fastilu_status fastilu_symbolic(int64_t n, const int64_t *row_ptr,
 }
 
 // --------------------------------------------------------------------------- create
-static fastilu_status setup_configs(fastilu_handle h, int64_t m_max, int64_t maxU, double m_avg,
-                                    double nl_avg) {
-  // sweep: lanes per row from the average row length, pivots staged per chunk from smem
-  int G = m_avg <= 10 ? 8 : (m_avg <= 24 ? 16 : 32);
+// Injective multiplicative hash of the column offsets j - i of every owned row:
+// slot = ((uint32)(j - i) * mul) >> (32 - bits).  Returns false if none of the candidates works.
+static bool find_offset_hash(const std::vector<int64_t> &rp, const std::vector<int32_t> &ci,
+                             int64_t r0, int64_t r1, int64_t m_max, int nthreads, uint32_t *mul,
+                             int *bits) {
+  static const uint32_t kMul[] = {0x9E3779B1u, 0x85EBCA77u, 0xC2B2AE3Du, 0x27D4EB2Fu,
+                                  0x165667B1u, 0xD3A2646Cu | 1u, 0xFD7046C5u, 0xB55A4F09u};
+  if (m_max > 65535) return false;
+  int b0 = 1;
+  while ((1ll << b0) < 2 * std::max<int64_t>(m_max, 1)) b0++;
+  for (int b = b0; b <= 12; b++) {
+    for (uint32_t mu : kMul) {
+      std::atomic<bool> bad{false};
+      const int T = std::max(1, std::min<int>(nthreads, (int)((r1 - r0) / 4096 + 1)));
+      std::vector<std::thread> th;
+      for (int t = 0; t < T; t++)
+        th.emplace_back([&, t]() {
+          std::vector<int64_t> stamp((size_t)1 << b, -1);
+          int64_t a = r0 + (r1 - r0) * t / T, e = r0 + (r1 - r0) * (t + 1) / T;
+          for (int64_t r = a; r < e && !bad.load(std::memory_order_relaxed); r++) {
+            for (int64_t p = rp[r]; p < rp[r + 1]; p++) {
+              uint32_t h = ((uint32_t)(ci[p] - (int32_t)r) * mu) >> (32 - b);
+              if (stamp[h] == r) {
+                bad = true;
+                break;
+              }
+              stamp[h] = r;
+            }
+          }
+        });
+      for (auto &x : th) x.join();
+      if (!bad) {
+        *mul = mu;
+        *bits = b;
+        return true;
+      }
+    }
+  }
+  return false;
+}
+
+static fastilu_status setup_configs(fastilu_handle h, const std::vector<int64_t> &rp,
+                                    const std::vector<int32_t> &ci, int64_t m_max, double u_avg,
+                                    double nl_avg, int nthreads) {
   SweepCfg c{};
+  int G = 4;
+  while (G < u_avg && G < 32) G *= 2;
   c.G = G;
-  c.cap_m = (int)((m_max + 3) / 4 * 4);
-  if (c.cap_m < 4) c.cap_m = 4;
-  int64_t mU = std::max<int64_t>(maxU, 1);
-  const size_t budget = 16 * 1024;  // staging bytes per group
-  int Pv = (int)std::min<int64_t>(G, std::max<int64_t>(1, (int64_t)(budget / (12 * mU))));
-  c.P = Pv;
-  c.cap_st = (int)(Pv * mU);
-  size_t gbytes = (size_t)c.cap_m * 12 + (size_t)c.cap_st * 12 + (size_t)Pv * 16 + (Pv + 1) * 4;
-  gbytes = (gbytes + 15) & ~(size_t)15;
-  int warps = 4;
-  while (warps > 1 && (size_t)(warps * 32 / G) * gbytes > 200 * 1024) warps /= 2;
-  if ((size_t)(warps * 32 / G) * gbytes > 220 * 1024) return FASTILU_ERR_UNSUPPORTED;
-  c.warps = warps;
-  c.smem = (size_t)(warps * 32 / G) * gbytes;
-  int per_sm = std::max<int>(1, (int)((220 * 1024) / std::max<size_t>(c.smem, 1)));
-  per_sm = std::min(per_sm, 64 / warps);
-  int sms = sm_count(h->device);
-  int64_t gpb = warps * 32 / G;
-  int64_t need = (h->n + gpb - 1) / gpb;
-  c.grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)sms * per_sm));
+  c.threads = 512;
+  c.cap_m = (int)std::max<int64_t>(4, (m_max + 3) / 4 * 4);
+  uint32_t mul = 0;
+  int bits = 0;
+  c.hash = find_offset_hash(rp, ci, h->G, h->G + h->n, m_max, nthreads, &mul, &bits);
+  c.hmul = mul;
+  c.hshift = c.hash ? 32 - bits : 0;
+  c.hsize = c.hash ? (1 << bits) : 0;
+  auto gbytes = [&](const SweepCfg &cc) {
+    size_t b = (size_t)cc.cap_m * 12 + (size_t)cc.hsize * 2;
+    return (b + 15) & ~(size_t)15;
+  };
+  while (c.threads > 32 && (size_t)(c.threads / G) * gbytes(c) > 200 * 1024) c.threads /= 2;
+  if (c.threads < G || (size_t)(c.threads / G) * gbytes(c) > 220 * 1024)
+    return FASTILU_ERR_UNSUPPORTED;  // a row of S too long for the shared-memory accumulator
+  c.smem = (size_t)(c.threads / G) * gbytes(c);
+  int bps = 0;
+  if (sweep_configure(c, &bps) != cudaSuccess || bps < 1) return FASTILU_ERR_CUDA;
+  const int sms = sm_count(h->device);
+  const int64_t gpb = c.threads / G;
+  const int64_t need = std::max<int64_t>(1, (h->n + gpb - 1) / gpb);
+  c.grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * bps, need));
+  c.chunk = std::max<int64_t>(1, (h->n + c.grid - 1) / c.grid);
+  c.grid = (int)std::max<int64_t>(1, (h->n + c.chunk - 1) / c.chunk);
   h->scfg = c;
-  h->G_init = G;
-  int gt = 1;
-  while (gt < nl_avg && gt < 32) gt *= 2;
+  int gi = 4;
+  while (gi < (double)h->nnz_own / std::max<int64_t>(h->n, 1) && gi < 32) gi *= 2;
+  h->G_init = gi;
+  int gt = 1;  // trisolve: 2 entries per lane in the fast path
+  while (2 * gt < nl_avg && gt < 32) gt *= 2;
   h->G_tri = gt;
   return FASTILU_OK;
 }
@@ -321,9 +370,10 @@ static fastilu_status create_impl(fastilu_handle h, int64_t n, const int64_t *ro
   }
   int64_t nl_own = 0;
   for (int64_t r = h->G; r < h->nloc; r++) nl_own += dloc[r];
-  const double m_avg = n ? (double)h->nnz_own / n : 1.0;
   const double nl_avg = n ? (double)nl_own / n : 1.0;
-  fastilu_status fs = setup_configs(h, m_max, maxU, m_avg, nl_avg);
+  const double u_avg = n ? (double)(h->nnz_own - n - nl_own) / n : 1.0;
+  (void)maxU;
+  fastilu_status fs = setup_configs(h, rp, ci, m_max, u_avg, nl_avg, nt);
   if (fs) return fs;
   // device allocations
   CU(dalloc(&h->d_rp, h->nloc + 1));
@@ -340,7 +390,7 @@ static fastilu_status create_impl(fastilu_handle h, int64_t n, const int64_t *ro
     CU(dalloc(&h->d_z[b], h->E));
     CU(dalloc(&h->d_w[b], h->E));
   }
-  CU(dalloc(&h->d_ahat, h->nnz_loc));
+  CU(dalloc(&h->d_ahat, h->nnzA_loc));  // ahat on A's pattern
   CU(dalloc(&h->d_s, h->E));
   CU(dalloc(&h->d_ad, h->E));
   CU(dalloc(&h->d_y, h->E));
@@ -452,8 +502,10 @@ extern "C" fastilu_status fastilu_compute(fastilu_handle h, int nsweeps) {
       fastilu_status cs = comm_factor_halo(h->comm, h->d_vals[ib], h->d_rp, h->d_ud[ib], st);
       if (cs) return cs;
     }
-    CU(launch_sweep(P, h->d_ahat, h->d_vals[ib], h->d_vals[ob], h->d_ud[ib], h->d_ud[ob], r0, r1,
-                    h->opt.omega, h->d_partials, h->d_err, h->scfg, st));
+    SweepArgs sa{P,           h->d_arp,      h->d_apos,     h->d_ahat, h->d_vals[ib],
+                 h->d_vals[ob], h->d_ud[ib], h->d_ud[ob], r0,        r1,
+                 h->opt.omega,  h->d_partials, h->d_err};
+    CU(launch_sweep(sa, h->scfg, st));
     CU(launch_reduce(h->d_partials, h->scfg.grid, h->d_r2 + (sw - 1), st));
   }
   CU(cudaEventRecord(h->ev[2], st));

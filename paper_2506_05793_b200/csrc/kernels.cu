@@ -2,7 +2,7 @@
 //
 // Step map (PAPER.md citations at each kernel):
 //   a2 scale_kernel      s_i = 1/sqrt(|a_ii|), ahat_ii                     (R5)
-//   a3 init_kernel       ahat on S, L0 = ahat_ij/ahat_jj, U0 = ahat_ij     (R4)
+//   a3 init_kernel       ahat on A, L0 = ahat_ij/ahat_jj, U0 = ahat_ij     (R4)
 //   a4/a5 sweep_kernel   one synchronous FastILU sweep + residual partials
 //   a8 jacobi_L_kernel   z <- y - (L - I) z
 //   a9 jacobi_U_kernel   w <- D^-1 (z - (U - D) w), last sweep x = s o w
@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(256)
 init_kernel(DevPattern P, const int64_t *__restrict__ arp, const int32_t *__restrict__ aci,
             const int32_t *__restrict__ apos, const double *__restrict__ aval,
             const double *__restrict__ s, const double *__restrict__ ad, int64_t r0, int64_t r1,
-            double *__restrict__ ahat, double *__restrict__ vals, double *__restrict__ udiag,
+            double *__restrict__ ahatA, double *__restrict__ vals, double *__restrict__ udiag,
             ErrFlags *err) {
   auto tile = cg::tiled_partition<G>(cg::this_thread_block());
   const int gpb = blockDim.x / G;
@@ -69,17 +69,14 @@ init_kernel(DevPattern P, const int64_t *__restrict__ arp, const int32_t *__rest
   const int64_t stride = (int64_t)gridDim.x * gpb;
   for (int64_t row = r0 + (int64_t)blockIdx.x * gpb + threadIdx.x / G; row < r1; row += stride) {
     const int64_t rb = P.rp[row], re = P.rp[row + 1];
-    for (int64_t p = rb + lane; p < re; p += G) {
-      ahat[p] = 0.0;  // fill entries: +0.0 (R4)
-      vals[p] = 0.0;
-    }
+    for (int64_t p = rb + lane; p < re; p += G) vals[p] = 0.0;  // fill entries: +0.0 (R4)
     tile.sync();
     const double si = s[row];
     for (int64_t q = arp[row] + lane; q < arp[row + 1]; q += G) {
       const int32_t j = aci[q];
       const int64_t p = rb + apos[q];
       const double ah = __dmul_rn(__dmul_rn(aval[q], si), s[j]);
-      ahat[p] = ah;
+      ahatA[q] = ah;
       vals[p] = (j < row) ? __ddiv_rn(ah, ad[j]) : ah;
       if (j == row) {
         udiag[row] = ah;
@@ -92,7 +89,7 @@ init_kernel(DevPattern P, const int64_t *__restrict__ arp, const int32_t *__rest
 
 cudaError_t launch_init(const DevPattern &P, const int64_t *arp, const int32_t *aci,
                         const int32_t *apos, const double *aval, const double *s,
-                        const double *ad, int64_t r0, int64_t r1, double *ahat, double *vals,
+                        const double *ad, int64_t r0, int64_t r1, double *ahatA, double *vals,
                         double *udiag, ErrFlags *err, int G, cudaStream_t st) {
   if (r1 <= r0) return cudaSuccess;
   const int threads = 256, gpb = threads / G;
@@ -100,7 +97,7 @@ cudaError_t launch_init(const DevPattern &P, const int64_t *arp, const int32_t *
   if (blocks > (1ll << 30)) blocks = 1ll << 30;
 #define FASTILU_INIT(GG)                                                                   \
   init_kernel<GG><<<(unsigned)blocks, threads, 0, st>>>(P, arp, aci, apos, aval, s, ad, r0, r1, \
-                                                         ahat, vals, udiag, err)
+                                                         ahatA, vals, udiag, err)
   switch (G) {
     case 4: FASTILU_INIT(4); break;
     case 8: FASTILU_INIT(8); break;
@@ -119,92 +116,118 @@ cudaError_t launch_init(const DevPattern &P, const int64_t *arp, const int32_t *
 //       for each j in the strict upper row of U_k (j > k) with (i,j) in S:
 //           acc[p(j)] -= l_ik * u_kj                      (old values, iterate s-1)
 // which is exactly the oracle's sum over k < min(i,j), (k,j) in S, in ascending k, for every
-// target.  The U-rows of a chunk of P pivots are staged in shared memory by one flattened,
-// coalesced copy (all loads in flight at once), then applied pivot by pivot.
-// Finalize: l_ij = acc / u_jj(old), u_ij = acc (omega-damped), residual partial
-// (acc - l_ij u_jj)^2 / (acc - u_ij)^2 of iterate s-1, new diagonal copied to udiag.
+// target (the same rounded products subtracted in the same order => bitwise equal).
+//  * the row's columns, its accumulator (seeded from ahat on A's pattern) and a position table
+//    live in shared memory; p(j) is found through an injective multiplicative hash of the
+//    offset j - i (verified on the host for every row at create) or, if none was found, by
+//    binary search;
+//  * lanes take consecutive entries of U_k (coalesced); the next pivot's entries are loaded
+//    into registers while the current pivot is applied (software pipeline, no smem staging);
+//  * each block owns a contiguous chunk of rows and its groups walk it interleaved, so
+//    neighbouring rows (which share most of their pivots' U-rows) run on the same SM (L1).
+// Finalize: l_ij = acc / u_jj(old), u_ij = acc (omega-damped), residual partial of iterate s-1
+// ((acc - l_ij u_jj)^2 or (acc - u_ij)^2), contiguous row write, diagonal copy into udiag.
 // ----------------------------------------------------------------------------------------
-__host__ __device__ inline size_t sweep_group_bytes(int cap_m, int cap_st, int Pv) {
-  size_t b = (size_t)cap_m * 12 + (size_t)cap_st * 12 + (size_t)Pv * 16 + (size_t)(Pv + 1) * 4;
+__host__ __device__ inline size_t sweep_group_bytes(int cap_m, int hsize) {
+  size_t b = (size_t)cap_m * 12 + (size_t)hsize * 2;
   return (b + 15) & ~(size_t)15;
 }
 
-template <int G>
-__global__ void __launch_bounds__(256)
-sweep_kernel(DevPattern P, const double *__restrict__ ahat, const double *__restrict__ old,
+template <int G, bool HASH>
+__global__ void __launch_bounds__(512)
+sweep_kernel(DevPattern P, const int64_t *__restrict__ arp, const int32_t *__restrict__ apos,
+             const double *__restrict__ ahatA, const double *__restrict__ old,
              double *__restrict__ out, const double *__restrict__ udo, double *__restrict__ udn,
-             int64_t r0, int64_t r1, double omega, double *__restrict__ partials, ErrFlags *err,
-             int cap_m, int Pv, int cap_st) {
+             int64_t r0, int64_t r1, int64_t chunk, double omega, double *__restrict__ partials,
+             ErrFlags *err, int cap_m, uint32_t hmul, int hshift, int hsize) {
   extern __shared__ __align__(16) unsigned char smem[];
   auto blk = cg::this_thread_block();
   auto tile = cg::tiled_partition<G>(blk);
   const int gpb = blockDim.x / G;
   const int gib = threadIdx.x / G;
   const int lane = tile.thread_rank();
-  unsigned char *gb = smem + sweep_group_bytes(cap_m, cap_st, Pv) * gib;
+  unsigned char *gb = smem + sweep_group_bytes(cap_m, hsize) * gib;
   double *acc = reinterpret_cast<double *>(gb);
-  double *stv = acc + cap_m;
-  double *lik = stv + cap_st;
-  int64_t *ub = reinterpret_cast<int64_t *>(lik + Pv);
-  int32_t *sc = reinterpret_cast<int32_t *>(ub + Pv);
-  int32_t *stc = sc + cap_m;
-  int32_t *off = stc + cap_st;
+  int32_t *sc = reinterpret_cast<int32_t *>(acc + cap_m);
+  uint16_t *T = reinterpret_cast<uint16_t *>(sc + cap_m);
   const bool damp = (omega != 1.0);
   const double om1 = 1.0 - omega;
 
   double r2 = 0.0;
-  const int64_t stride = (int64_t)gridDim.x * gpb;
-  for (int64_t row = r0 + (int64_t)blockIdx.x * gpb + gib; row < r1; row += stride) {
+  const int64_t cb = r0 + (int64_t)blockIdx.x * chunk;
+  const int64_t ce = min(r1, cb + chunk);
+  for (int64_t row = cb + gib; row < ce; row += gpb) {
     const int64_t rb = P.rp[row];
     const int m = (int)(P.rp[row + 1] - rb);
     const int nl = P.dloc[row];
+    const int irow = (int)row;
     for (int p = lane; p < m; p += G) {
-      sc[p] = P.ci[rb + p];
-      acc[p] = ahat[rb + p];
+      const int c = P.ci[rb + p];
+      sc[p] = c;
+      acc[p] = 0.0;  // fill entries start from +0.0 (R4)
+      if (HASH) T[((uint32_t)(c - irow) * hmul) >> hshift] = (uint16_t)p;
     }
     tile.sync();
-    for (int t0 = 0; t0 < nl; t0 += Pv) {
-      const int np = min(Pv, nl - t0);
+    for (int64_t q = arp[row] + lane; q < arp[row + 1]; q += G) acc[apos[q]] = ahatA[q];
+    tile.sync();
+
+    auto apply1 = [&](int j, double u, double l, int t) {
+      int p = -1;
+      if (HASH) {
+        const int pp = T[((uint32_t)(j - irow) * hmul) >> hshift];
+        if (pp < m && sc[pp] == j) p = pp;
+      } else {
+        int lo = t + 1, hi = m - 1;
+        while (lo <= hi) {
+          const int mid = (lo + hi) >> 1;
+          const int cm = sc[mid];
+          if (cm == j) { p = mid; break; }
+          if (cm < j) lo = mid + 1; else hi = mid - 1;
+        }
+      }
+      if (p >= 0) acc[p] = __dsub_rn(acc[p], __dmul_rn(l, u));
+    };
+
+    for (int t0 = 0; t0 < nl; t0 += G) {
+      const int np = min(G, nl - t0);
+      int64_t ub = 0;
       int len = 0;
+      double lv = 0.0;
       if (lane < np) {
         const int k = sc[t0 + lane];
-        const int64_t u0 = P.rp[k] + P.dloc[k] + 1;  // strict upper part of row k
-        len = (int)(P.rp[k + 1] - u0);
-        ub[lane] = u0;
-        lik[lane] = old[rb + t0 + lane];
+        const int64_t rk = P.rp[k];
+        ub = rk + P.dloc[k] + 1;  // strict upper part of row k
+        len = (int)(P.rp[k + 1] - ub);
+        lv = old[rb + t0 + lane];
       }
-      const int incl = cg::inclusive_scan(tile, len);
-      if (lane < np) off[lane] = incl - len;
-      const int total = tile.shfl(incl, np - 1);
-      if (lane == 0) off[np] = total;
-      tile.sync();
-      for (int c = lane; c < total; c += G) {
-        int lo = 0, hi = np;  // off[lo] <= c < off[lo + 1]
-        while (hi - lo > 1) {
-          const int mid = (lo + hi) >> 1;
-          if (off[mid] <= c) lo = mid; else hi = mid;
-        }
-        const int64_t src = ub[lo] + (c - off[lo]);
-        stc[c] = P.ci[src];
-        stv[c] = old[src];
-      }
-      tile.sync();
+      // software pipeline: (cj0,cu0),(cj1,cu1) = entries lane, lane+G of the current pivot
+      int64_t cbse = tile.shfl(ub, 0);
+      int clen = tile.shfl(len, 0);
+      double cl = tile.shfl(lv, 0);
+      int cj0 = -1, cj1 = -1;
+      double cu0 = 0.0, cu1 = 0.0;
+      if (lane < clen) { cj0 = P.ci[cbse + lane]; cu0 = old[cbse + lane]; }
+      if (lane + G < clen) { cj1 = P.ci[cbse + lane + G]; cu1 = old[cbse + lane + G]; }
       for (int q = 0; q < np; q++) {
-        const double l = lik[q];
-        const int t = t0 + q;
-        const int e1 = off[q + 1];
-        for (int e = off[q] + lane; e < e1; e += G) {
-          const int j = stc[e];
-          int lo = t + 1, hi = m - 1, p = -1;
-          while (lo <= hi) {
-            const int mid = (lo + hi) >> 1;
-            const int cm = sc[mid];
-            if (cm == j) { p = mid; break; }
-            if (cm < j) lo = mid + 1; else hi = mid - 1;
-          }
-          if (p >= 0) acc[p] = __dsub_rn(acc[p], __dmul_rn(l, stv[e]));
+        int64_t nbse = 0;
+        int nlen = 0;
+        double nlv = 0.0;
+        int nj0 = -1, nj1 = -1;
+        double nu0 = 0.0, nu1 = 0.0;
+        if (q + 1 < np) {
+          nbse = tile.shfl(ub, q + 1);
+          nlen = tile.shfl(len, q + 1);
+          nlv = tile.shfl(lv, q + 1);
+          if (lane < nlen) { nj0 = P.ci[nbse + lane]; nu0 = old[nbse + lane]; }
+          if (lane + G < nlen) { nj1 = P.ci[nbse + lane + G]; nu1 = old[nbse + lane + G]; }
         }
+        const int t = t0 + q;
+        if (cj0 >= 0) apply1(cj0, cu0, cl, t);
+        if (cj1 >= 0) apply1(cj1, cu1, cl, t);
+        for (int e = lane + 2 * G; e < clen; e += G) apply1(P.ci[cbse + e], old[cbse + e], cl, t);
         tile.sync();
+        cbse = nbse; clen = nlen; cl = nlv;
+        cj0 = nj0; cj1 = nj1; cu0 = nu0; cu1 = nu1;
       }
     }
     for (int p = lane; p < m; p += G) {
@@ -242,39 +265,38 @@ sweep_kernel(DevPattern P, const double *__restrict__ ahat, const double *__rest
   }
 }
 
-template <int G>
-static cudaError_t launch_sweep_t(const DevPattern &P, const double *ahat, const double *old,
-                                  double *out, const double *udo, double *udn, int64_t r0,
-                                  int64_t r1, double omega, double *partials, ErrFlags *err,
-                                  const SweepCfg &c, cudaStream_t st) {
-  static bool attr_set = false;
-  static size_t attr_bytes = 0;
-  if (!attr_set || attr_bytes < c.smem) {
-    cudaFuncSetAttribute(sweep_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(c.smem > 48 * 1024 ? c.smem : 48 * 1024));
-    attr_set = true;
-    attr_bytes = c.smem;
-  }
-  sweep_kernel<G><<<c.grid, c.warps * 32, c.smem, st>>>(P, ahat, old, out, udo, udn, r0, r1,
-                                                         omega, partials, err, c.cap_m, c.P,
-                                                         c.cap_st);
+template <int G, bool HASH>
+static cudaError_t launch_sweep_t(const SweepArgs &a, const SweepCfg &c, cudaStream_t st) {
+  sweep_kernel<G, HASH><<<c.grid, c.threads, c.smem, st>>>(
+      a.P, a.arp, a.apos, a.ahatA, a.old, a.out, a.udo, a.udn, a.r0, a.r1, c.chunk, a.omega,
+      a.partials, a.err, c.cap_m, c.hmul, c.hshift, c.hsize);
   return cudaGetLastError();
 }
 
-cudaError_t launch_sweep(const DevPattern &P, const double *ahat, const double *old,
-                         double *out, const double *udiag_old, double *udiag_new, int64_t r0,
-                         int64_t r1, double omega, double *partials, ErrFlags *err,
-                         const SweepCfg &cfg, cudaStream_t st) {
-  switch (cfg.G) {
-    case 4: return launch_sweep_t<4>(P, ahat, old, out, udiag_old, udiag_new, r0, r1, omega,
-                                      partials, err, cfg, st);
-    case 8: return launch_sweep_t<8>(P, ahat, old, out, udiag_old, udiag_new, r0, r1, omega,
-                                      partials, err, cfg, st);
-    case 16: return launch_sweep_t<16>(P, ahat, old, out, udiag_old, udiag_new, r0, r1, omega,
-                                        partials, err, cfg, st);
-    default: return launch_sweep_t<32>(P, ahat, old, out, udiag_old, udiag_new, r0, r1, omega,
-                                        partials, err, cfg, st);
+template <int G, bool HASH>
+static cudaError_t sweep_attr_t(const SweepCfg &c, int *blocks_per_sm) {
+  cudaError_t e = cudaFuncSetAttribute(sweep_kernel<G, HASH>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(c.smem > 0 ? c.smem : 1));
+  if (e != cudaSuccess) return e;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, sweep_kernel<G, HASH>,
+                                                       c.threads, c.smem);
+}
+
+#define FASTILU_SWEEP_DISPATCH(FN, ...)                                   \
+  switch (cfg.G) {                                                        \
+    case 4: return cfg.hash ? FN<4, true>(__VA_ARGS__) : FN<4, false>(__VA_ARGS__);     \
+    case 8: return cfg.hash ? FN<8, true>(__VA_ARGS__) : FN<8, false>(__VA_ARGS__);     \
+    case 16: return cfg.hash ? FN<16, true>(__VA_ARGS__) : FN<16, false>(__VA_ARGS__);  \
+    default: return cfg.hash ? FN<32, true>(__VA_ARGS__) : FN<32, false>(__VA_ARGS__);  \
   }
+
+cudaError_t sweep_configure(const SweepCfg &cfg, int *blocks_per_sm) {
+  FASTILU_SWEEP_DISPATCH(sweep_attr_t, cfg, blocks_per_sm)
+}
+
+cudaError_t launch_sweep(const SweepArgs &a, const SweepCfg &cfg, cudaStream_t st) {
+  FASTILU_SWEEP_DISPATCH(launch_sweep_t, a, cfg, st)
 }
 
 // deterministic sum of the per-block partials (one block, fixed order)
@@ -345,7 +367,11 @@ cudaError_t launch_trisolve_first_U(const double *z, const double *udiag, const 
   return cudaGetLastError();
 }
 
-template <int G, bool LOWER>
+// One G-lane group handles R consecutive rows per iteration; the first 2G entries of every row
+// are loaded up front (column, value, then the gathered x) so that 2R independent gathers per
+// lane are in flight, the rest of a long row is streamed after.  Row sums are reduced across
+// the group (fixed shuffle tree), lane r writes row r.
+template <int G, int R, bool LOWER>
 __global__ void __launch_bounds__(256)
 jacobi_kernel(DevPattern P, const double *__restrict__ vals, const double *__restrict__ ud,
               const double *__restrict__ rhs, const double *__restrict__ xo,
@@ -354,20 +380,51 @@ jacobi_kernel(DevPattern P, const double *__restrict__ vals, const double *__res
   auto tile = cg::tiled_partition<G>(cg::this_thread_block());
   const int gpb = blockDim.x / G;
   const int lane = tile.thread_rank();
-  const int64_t stride = (int64_t)gridDim.x * gpb;
-  for (int64_t row = r0 + (int64_t)blockIdx.x * gpb + threadIdx.x / G; row < r1; row += stride) {
-    const int64_t rb = P.rp[row];
-    const int nl = P.dloc[row];
-    const int64_t b0 = LOWER ? rb : rb + nl + 1;
-    const int64_t b1 = LOWER ? rb + nl : P.rp[row + 1];
-    double sum = 0.0;
-    for (int64_t p = b0 + lane; p < b1; p += G) sum = fma(vals[p], xo[P.ci[p]], sum);
-    sum = cg::reduce(tile, sum, cg::plus<double>());
-    if (lane == 0) {
-      double u = rhs[row] - sum;
-      if (!LOWER) u = __ddiv_rn(u, ud[row]);
-      const double v = (omega == 1.0) ? u : (1.0 - omega) * xo[row] + omega * u;
-      if (final) xfinal[row - Gh] = __dmul_rn(s[row], v); else xn[row] = v;
+  const int64_t stride = (int64_t)gridDim.x * gpb * R;
+  for (int64_t base = r0 + ((int64_t)blockIdx.x * gpb + threadIdx.x / G) * R; base < r1;
+       base += stride) {
+    int64_t b0[R], b1[R];
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+      const int64_t row = base + r;
+      b0[r] = b1[r] = 0;
+      if (row < r1) {
+        const int64_t rb = P.rp[row];
+        const int nl = P.dloc[row];
+        b0[r] = LOWER ? rb : rb + nl + 1;
+        b1[r] = LOWER ? rb + nl : P.rp[row + 1];
+      }
+    }
+    int c0[R], c1[R];
+    double v0[R], v1[R], sum[R];
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+      const int64_t p0 = b0[r] + lane, p1 = p0 + G;
+      c0[r] = p0 < b1[r] ? P.ci[p0] : -1;
+      v0[r] = p0 < b1[r] ? vals[p0] : 0.0;
+      c1[r] = p1 < b1[r] ? P.ci[p1] : -1;
+      v1[r] = p1 < b1[r] ? vals[p1] : 0.0;
+    }
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+      const double x0 = c0[r] >= 0 ? xo[c0[r]] : 0.0;
+      const double x1 = c1[r] >= 0 ? xo[c1[r]] : 0.0;
+      sum[r] = fma(v1[r], x1, v0[r] * x0);
+    }
+#pragma unroll
+    for (int r = 0; r < R; r++)
+      for (int64_t p = b0[r] + lane + 2 * G; p < b1[r]; p += G) sum[r] = fma(vals[p], xo[P.ci[p]], sum[r]);
+#pragma unroll
+    for (int r = 0; r < R; r++) sum[r] = cg::reduce(tile, sum[r], cg::plus<double>());
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+      const int64_t row = base + r;
+      if (lane == (r % G) && row < r1) {
+        double u = rhs[row] - sum[r];
+        if (!LOWER) u = __ddiv_rn(u, ud[row]);
+        const double v = (omega == 1.0) ? u : (1.0 - omega) * xo[row] + omega * u;
+        if (final) xfinal[row - Gh] = __dmul_rn(s[row], v); else xn[row] = v;
+      }
     }
   }
 }
@@ -378,12 +435,13 @@ static cudaError_t launch_jacobi_t(const DevPattern &P, const double *vals, cons
                                    const double *s, int64_t r0, int64_t r1, int64_t Gh,
                                    double omega, bool final, int G, cudaStream_t st) {
   if (r1 <= r0) return cudaSuccess;
+  constexpr int R = 2;
   const int threads = 256, gpb = threads / G;
-  int64_t blocks = (r1 - r0 + gpb - 1) / gpb;
+  int64_t blocks = (r1 - r0 + (int64_t)gpb * R - 1) / ((int64_t)gpb * R);
   if (blocks > (1ll << 30)) blocks = 1ll << 30;
-#define FASTILU_JAC(GG)                                                                     \
-  jacobi_kernel<GG, LOWER><<<(unsigned)blocks, threads, 0, st>>>(P, vals, ud, rhs, xo, xn, xf, s, \
-                                                                   r0, r1, Gh, omega, final)
+#define FASTILU_JAC(GG)                                                                 \
+  jacobi_kernel<GG, R, LOWER><<<(unsigned)blocks, threads, 0, st>>>(P, vals, ud, rhs, xo, xn, xf, \
+                                                                      s, r0, r1, Gh, omega, final)
   switch (G) {
     case 1: FASTILU_JAC(1); break;
     case 2: FASTILU_JAC(2); break;
