@@ -158,6 +158,18 @@ fastilu_status fastilu_symbolic(int64_t n, const int64_t *row_ptr, const int32_t
                                 int64_t *row_ptr_out, int32_t *col_idx_out, int8_t *level_out,
                                 int64_t *bad_row);
 
+/* Host-only symbolic ILU(k) of a ROW WINDOW (the multi-GPU setup's building block): the caller
+ * supplies rows [row0, row0 + nrows) of a global matrix (global column indices; entries with a
+ * column < row0 are ignored) and receives the exact pattern of global rows [out_begin,
+ * out_end), which is exact when out_begin - row0 >= fastilu_required_lead_rows(bandwidth, k)
+ * or row0 == 0.  Two-phase like fastilu_symbolic; row_ptr_out has out_end - out_begin + 1
+ * entries (rebased to 0). */
+fastilu_status fastilu_symbolic_window(int64_t nrows, const int64_t *row_ptr,
+                                       const int32_t *col_idx, int64_t row0, int64_t ncols,
+                                       int64_t out_begin, int64_t out_end, int level_k,
+                                       int num_threads, int64_t *nnz_out, int64_t *row_ptr_out,
+                                       int32_t *col_idx_out, int8_t *level_out, int64_t *bad_row);
+
 /* In-process rank group for FASTILU_COMM_LOCAL (ranks = threads of one process, halos by
  * device-to-device copies).  Destroy after all member handles are destroyed. */
 fastilu_status fastilu_group_create(fastilu_group *out, int nranks);

@@ -68,6 +68,9 @@ _SIGS = {
     "fastilu_error_index": (C.c_int64, [H]),
     "fastilu_symbolic": (C.c_int, [C.c_int64, I64P, I32P, C.c_int, C.c_int, I64P, I64P, I32P,
                                    I8P, I64P]),
+    "fastilu_symbolic_window": (C.c_int, [C.c_int64, I64P, I32P, C.c_int64, C.c_int64, C.c_int64,
+                                          C.c_int64, C.c_int, C.c_int, I64P, I64P, I32P, I8P,
+                                          I64P]),
     "fastilu_group_create": (C.c_int, [C.POINTER(H), C.c_int]),
     "fastilu_group_destroy": (C.c_int, [H]),
     "fastilu_nccl_unique_id": (C.c_int, [C.c_void_p]),
@@ -144,6 +147,51 @@ def fastilu_symbolic(row_ptr, col_idx, level_k: int, num_threads: int = 0):
     if st:
         raise FastILUError(st, bad.value, "fastilu_symbolic")
     return orp, oci[:nnz.value], olev[:nnz.value]
+
+
+def fastilu_symbolic_window(row_ptr, col_idx, row0: int, ncols: int, out_begin: int,
+                            out_end: int, level_k: int, num_threads: int = 0):
+    """Host-only symbolic ILU(k) of global rows [out_begin, out_end) from the supplied rows
+    [row0, row0 + nrows) -> (row_ptr, col_idx (global), level)."""
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    ci = np.ascontiguousarray(col_idx, dtype=np.int32)
+    nrows = rp.shape[0] - 1
+    nnz = C.c_int64(0)
+    bad = C.c_int64(-1)
+    args = (nrows, _p(rp, I64P), _p(ci, I32P), int(row0), int(ncols), int(out_begin),
+            int(out_end), int(level_k), int(num_threads), C.byref(nnz))
+    st = lib().fastilu_symbolic_window(*args, None, None, None, C.byref(bad))
+    if st:
+        raise FastILUError(st, bad.value, "fastilu_symbolic_window")
+    no = out_end - out_begin
+    orp = np.empty(no + 1, dtype=np.int64)
+    oci = np.empty(max(nnz.value, 1), dtype=np.int32)
+    olev = np.empty(max(nnz.value, 1), dtype=np.int8)
+    st = lib().fastilu_symbolic_window(*args, _p(orp, I64P), _p(oci, I32P), _p(olev, I8P),
+                                       C.byref(bad))
+    if st:
+        raise FastILUError(st, bad.value, "fastilu_symbolic_window")
+    return orp, oci[:nnz.value], olev[:nnz.value]
+
+
+def fastilu_group_create(nranks: int):
+    g = H()
+    st = lib().fastilu_group_create(C.byref(g), int(nranks))
+    if st:
+        raise FastILUError(st, -1, "fastilu_group_create")
+    return g
+
+
+def fastilu_group_destroy(g) -> None:
+    lib().fastilu_group_destroy(g)
+
+
+def fastilu_nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    st = lib().fastilu_nccl_unique_id(buf)
+    if st:
+        raise FastILUError(st, -1, "fastilu_nccl_unique_id")
+    return buf.raw
 
 
 def fastilu_status_string(code: int) -> str:

@@ -12,8 +12,12 @@ struct Comm;
 
 // Collective over the ranks of opts: exchanges the partition (row_begin, n, G, H) of every rank
 // and validates that ghost rows come only from the immediate neighbours.
+// Also sums `stat` (e.g. the number of strict-lower entries) over ranks into *stat_global so
+// that launch shapes that affect rounding (the trisolve's lanes per row) are chosen from global
+// statistics and results stay bitwise independent of the partition.
 fastilu_status comm_setup(Comm *&out, const fastilu_options &opts, int64_t row_begin, int64_t n,
-                          int64_t G, int64_t H, cudaStream_t st);
+                          int64_t G, int64_t H, const int64_t *h_rp_local, int64_t stat,
+                          int64_t *stat_global, cudaStream_t st);
 // Vector halo on an extended vector [G | n | H]: lower ghosts from rank-1's last G owned
 // entries, upper ghosts from rank+1's first H owned entries.
 fastilu_status comm_vector_halo(Comm *c, double *x, cudaStream_t st, bool lower, bool upper);
@@ -21,7 +25,7 @@ fastilu_status comm_vector_halo(Comm *c, double *x, cudaStream_t st, bool lower,
 // diagonal copies from rank-1.
 fastilu_status comm_factor_halo(Comm *c, double *vals, const int64_t *d_rp, double *udiag,
                                 cudaStream_t st);
-// Host-side sum of the residual history and min of the error flags over ranks.
+// Host-side sum of the residual history and min of the (GLOBAL-index) error flags over ranks.
 fastilu_status comm_allreduce_host(Comm *c, double *r2, int count, ErrFlags &ef);
 void comm_destroy(Comm *c);
 

@@ -145,6 +145,41 @@ extern "C" fastilu_status fastilu_symbolic(int64_t n, const int64_t *row_ptr,
   return FASTILU_OK;
 }
 
+extern "C" fastilu_status fastilu_symbolic_window(int64_t nrows, const int64_t *row_ptr,
+                                                  const int32_t *col_idx, int64_t row0,
+                                                  int64_t ncols, int64_t out_begin,
+                                                  int64_t out_end, int level_k, int num_threads,
+                                                  int64_t *nnz_out, int64_t *row_ptr_out,
+                                                  int32_t *col_idx_out, int8_t *level_out,
+                                                  int64_t *bad_row) {
+  if (bad_row) *bad_row = -1;
+  if (nrows < 0 || !row_ptr || (nrows > 0 && !col_idx) || level_k < 0 || level_k > 127 ||
+      row0 < 0 || out_begin < row0 || out_end < out_begin || out_end > row0 + nrows ||
+      ncols < row0 + nrows)
+    return FASTILU_ERR_INVALID_ARG;
+  int64_t bad = -1;
+  int nt = hw_threads(num_threads);
+  int st = validate_csr(nrows, row_ptr, col_idx, row0, ncols, nt, &bad);
+  if (st) {
+    if (bad_row) *bad_row = bad;
+    return (fastilu_status)st;
+  }
+  Pattern pat;
+  st = symbolic_iluk(nrows, row_ptr, col_idx, row0, out_begin, out_end, level_k, nt, pat, &bad);
+  if (st) {
+    if (bad_row) *bad_row = bad;
+    return (fastilu_status)st;
+  }
+  const int64_t no = out_end - out_begin;
+  if (nnz_out) *nnz_out = pat.rp[no];
+  if (col_idx_out) {
+    if (row_ptr_out) std::memcpy(row_ptr_out, pat.rp.data(), sizeof(int64_t) * (no + 1));
+    std::memcpy(col_idx_out, pat.ci.data(), sizeof(int32_t) * pat.ci.size());
+    if (level_out) std::memcpy(level_out, pat.lev.data(), pat.lev.size());
+  }
+  return FASTILU_OK;
+}
+
 // --------------------------------------------------------------------------- create
 // Injective multiplicative hash of the column offsets j - i of every owned row:
 // slot = ((uint32)(j - i) * mul) >> (32 - bits).  Returns false if none of the candidates works.
@@ -414,8 +449,14 @@ static fastilu_status create_impl(fastilu_handle h, int64_t n, const int64_t *ro
   }
   for (int i = 0; i < 5; i++) CU(cudaEventCreate(&h->ev[i]));
   if (multi) {
-    fastilu_status cs = comm_setup(h->comm, h->opt, h->row_begin, h->n, h->G, h->H, h->stream);
+    int64_t nl_global = 0;
+    fastilu_status cs = comm_setup(h->comm, h->opt, h->row_begin, h->n, h->G, h->H, rp.data(),
+                                   nl_own, &nl_global, h->stream);
     if (cs) return cs;
+    const double nlg = (double)nl_global / (double)std::max<int64_t>(h->global_n, 1);
+    int gt = 1;  // same rule as setup_configs, from the GLOBAL average (partition-independent)
+    while (2 * gt < nlg && gt < 32) gt *= 2;
+    h->G_tri = gt;
   }
   if (values) return upload_values(h, values, false);
   return FASTILU_OK;
@@ -485,10 +526,8 @@ extern "C" fastilu_status fastilu_compute(fastilu_handle h, int nsweeps) {
   CU(cudaEventRecord(h->ev[0], st));
   // a2: scaling for every local row (lower ghosts included), then the upper ghosts' s / ad
   CU(launch_scale(h->d_arp, h->d_adiag, h->d_aval, 0, h->nloc, h->d_s, h->d_ad, h->d_err, st));
-  if (h->comm) {
-    fastilu_status cs = comm_vector_halo(h->comm, h->d_s, st, true, true);
-    if (cs) return cs;
-    cs = comm_vector_halo(h->comm, h->d_ad, st, true, true);
+  if (h->comm) {  // lower ghosts' s / ahat_ii are computed locally from the lead rows of A
+    fastilu_status cs = comm_vector_halo(h->comm, h->d_s, st, false, true);
     if (cs) return cs;
   }
   // a3: ahat on S and the initial guess (iterate 0) for the owned rows
@@ -517,7 +556,9 @@ extern "C" fastilu_status fastilu_compute(fastilu_handle h, int nsweeps) {
   CU(cudaEventElapsedTime(&h->t_sweeps, h->ev[1], h->ev[2]));
   h->resid.assign(nsweeps, 0.0);
   std::vector<double> r2(h->h_r2, h->h_r2 + nsweeps);
-  ErrFlags ef = *h->h_err;
+  ErrFlags ef = *h->h_err;  // local rows -> global rows
+  if (ef.zero_diag != ~0ull) ef.zero_diag += (unsigned long long)h->lbase;
+  if (ef.zero_pivot != ~0ull) ef.zero_pivot += (unsigned long long)h->lbase;
   if (h->comm) {
     fastilu_status cs = comm_allreduce_host(h->comm, r2.data(), (int)r2.size(), ef);
     if (cs) return cs;
@@ -525,11 +566,11 @@ extern "C" fastilu_status fastilu_compute(fastilu_handle h, int nsweeps) {
   for (int i = 0; i < nsweeps; i++) h->resid[i] = std::sqrt(r2[i]);
   h->cur = nsweeps & 1;
   if (ef.zero_diag != ~0ull) {
-    h->err_index = (int64_t)ef.zero_diag + h->lbase;
+    h->err_index = (int64_t)ef.zero_diag;
     return FASTILU_ERR_ZERO_DIAG;
   }
   if (ef.zero_pivot != ~0ull) {
-    h->err_index = (int64_t)ef.zero_pivot + h->lbase;
+    h->err_index = (int64_t)ef.zero_pivot;
     return FASTILU_ERR_ZERO_PIVOT;
   }
   h->computed = true;

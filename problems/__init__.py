@@ -47,18 +47,22 @@ class Csr:
         return d
 
 
-def _stencil(g: int, offsets, weights, diag: float, gz: int | None = None) -> Csr:
+def _stencil(g: int, offsets, weights, diag: float, gz: int | None = None,
+             planes: tuple[int, int] | None = None) -> Csr:
     """Assemble a 3D stencil operator on a g x g x gz grid (x fastest).
 
     offsets: list of (dx, dy, dz); weights: value of each off-diagonal entry.
     Out-of-grid neighbours are dropped (Dirichlet truncation).
+    planes=(z0, z1): only the rows of planes z0..z1-1, with GLOBAL column indices (a row block
+    of the global matrix, used by the multi-GPU row partition).
     """
     gz = g if gz is None else gz
-    n = g * g * gz
+    z0, z1 = (0, gz) if planes is None else planes
+    n = g * g * (z1 - z0)
     ents = [((0, 0, 0), diag)] + list(zip(offsets, weights))
     # increasing column order == increasing linear offset dz*g^2 + dy*g + dx
     ents.sort(key=lambda e: e[0][2] * g * g + e[0][1] * g + e[0][0])
-    rows = np.arange(n, dtype=np.int64)
+    rows = np.arange(n, dtype=np.int64) + z0 * g * g
     x = rows % g
     y = (rows // g) % g
     z = rows // (g * g)
@@ -96,21 +100,21 @@ CUBE26 = [(dx, dy, dz) for dz in (-1, 0, 1) for dy in (-1, 0, 1) for dx in (-1, 
           if (dx, dy, dz) != (0, 0, 0)]
 
 
-def laplace3d_7pt(g: int, coeffs=(1.0, 1.0, 1.0), gz: int | None = None) -> Csr:
+def laplace3d_7pt(g: int, coeffs=(1.0, 1.0, 1.0), gz: int | None = None, planes=None) -> Csr:
     cx, cy, cz = coeffs
     w = [-cx, -cx, -cy, -cy, -cz, -cz]
-    return _stencil(g, AXIS6, w, 2.0 * (cx + cy + cz), gz)
+    return _stencil(g, AXIS6, w, 2.0 * (cx + cy + cz), gz, planes)
 
 
-def laplace3d_27pt(g: int, gz: int | None = None) -> Csr:
-    return _stencil(g, CUBE26, [-1.0] * 26, 26.0, gz)
+def laplace3d_27pt(g: int, gz: int | None = None, planes=None) -> Csr:
+    return _stencil(g, CUBE26, [-1.0] * 26, 26.0, gz, planes)
 
 
 ANISO_COEFFS = (1.0, 0.01, 0.01)
 
 
-def aniso3d_7pt(g: int, gz: int | None = None) -> Csr:
-    return laplace3d_7pt(g, ANISO_COEFFS, gz)
+def aniso3d_7pt(g: int, gz: int | None = None, planes=None) -> Csr:
+    return laplace3d_7pt(g, ANISO_COEFFS, gz, planes)
 
 
 def elasticity_pattern_3dof(g: int) -> Csr:
@@ -187,6 +191,17 @@ def submatrix(a: Csr, lo: int, hi: int) -> Csr:
     return Csr(nrp, (ci[keep] - lo).astype(np.int32), vals[keep])
 
 
+def bandwidth(kind: str, g: int) -> int:
+    """Half bandwidth max |i - j| of the stencil matrices in natural order."""
+    return g * g + (g + 1 if kind == "27pt" else 0)
+
+
+def row_block(a: Csr, r0: int, r1: int) -> Csr:
+    """Rows [r0, r1) of `a` with their global column indices (plain CSR slicing)."""
+    s, e = int(a.row_ptr[r0]), int(a.row_ptr[r1])
+    return Csr(a.row_ptr[r0:r1 + 1] - s, a.col_idx[s:e], a.values[s:e])
+
+
 def rhs_positive(n: int, seed: int = SEED) -> np.ndarray:
     """b ~ U[0.5, 1.5) (positive b keeps Jacobi terms one-signed)."""
     return np.random.default_rng(seed).uniform(0.5, 1.5, size=n)
@@ -212,13 +227,13 @@ WORKLOADS = {
 }
 
 
-def make(kind: str, g: int, gz: int | None = None) -> Csr:
+def make(kind: str, g: int, gz: int | None = None, planes=None) -> Csr:
     if kind == "7pt":
-        return laplace3d_7pt(g, gz=gz)
+        return laplace3d_7pt(g, gz=gz, planes=planes)
     if kind == "27pt":
-        return laplace3d_27pt(g, gz=gz)
+        return laplace3d_27pt(g, gz=gz, planes=planes)
     if kind == "aniso7pt":
-        return aniso3d_7pt(g, gz=gz)
+        return aniso3d_7pt(g, gz=gz, planes=planes)
     if kind == "3dof":
         return elasticity_pattern_3dof(g)
     raise ValueError(kind)
