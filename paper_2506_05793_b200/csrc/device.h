@@ -27,6 +27,15 @@ struct SweepCfg {
   int grid;         // blocks (= resident capacity)
   int64_t chunk;    // rows per block
   size_t smem;      // dynamic smem per block
+  bool prog;        // class-program kernel (else hash / binary-search kernel)
+  int E;            // prog kernel: U-row entries per lane per pivot (1, 2, 4)
+};
+
+struct ProgView {
+  const int32_t *row_class;  // per owned row
+  const int64_t *class_off;  // program byte offset per class
+  const int32_t *class_aoff; // A-position part offset per class
+  const uint8_t *prog;
 };
 
 struct ErrFlags;
@@ -63,6 +72,9 @@ cudaError_t launch_init(const DevPattern &P, const int64_t *arp, const int32_t *
 // sets the smem attribute and returns the resident blocks per SM for cfg
 cudaError_t sweep_configure(const SweepCfg &cfg, int *blocks_per_sm);
 cudaError_t launch_sweep(const SweepArgs &a, const SweepCfg &cfg, cudaStream_t st);
+cudaError_t sweep_prog_configure(const SweepCfg &cfg, int *blocks_per_sm);
+cudaError_t launch_sweep_prog(const SweepArgs &a, const ProgView &pv, const SweepCfg &cfg,
+                              cudaStream_t st);
 
 cudaError_t launch_reduce(const double *partials, int np, double *dst, cudaStream_t st);
 

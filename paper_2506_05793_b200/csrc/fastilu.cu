@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -48,6 +49,10 @@ struct fastilu_handle_s {
   double *d_bx = nullptr;  // apply_host staging (2 n)
   double *d_partials = nullptr, *d_r2 = nullptr;
   int hist_cap = 0;
+  int32_t *d_rclass = nullptr, *d_caoff = nullptr;  // class-program sweep
+  int64_t *d_coff = nullptr;
+  uint8_t *d_prog = nullptr;
+  int64_t nclasses = 0;
   ErrFlags *d_err = nullptr;
   ErrFlags *h_err = nullptr;  // pinned
   double *h_r2 = nullptr;     // pinned, hist_cap
@@ -224,13 +229,41 @@ static bool find_offset_hash(const std::vector<int64_t> &rp, const std::vector<i
 
 static fastilu_status setup_configs(fastilu_handle h, const std::vector<int64_t> &rp,
                                     const std::vector<int32_t> &ci, int64_t m_max, double u_avg,
-                                    double nl_avg, int nthreads) {
+                                    double nl_avg, int64_t maxU, bool have_prog, int nthreads) {
   SweepCfg c{};
   int G = 4;
   while (G < u_avg && G < 32) G *= 2;
   c.G = G;
   c.threads = 512;
   c.cap_m = (int)std::max<int64_t>(4, (m_max + 3) / 4 * 4);
+  c.E = (int)((std::max<int64_t>(maxU, 1) + G - 1) / G);
+  if (c.E == 3) c.E = 4;
+  c.prog = have_prog && c.E <= (G == 32 ? 4 : 2);
+  if (c.prog) {
+    const size_t gb = (((size_t)c.cap_m * 8 + (size_t)G * 24) + 15) & ~(size_t)15;
+    while (c.threads > 64 && (size_t)(c.threads / G) * gb > 200 * 1024) c.threads /= 2;
+    if ((size_t)(c.threads / G) * gb <= 220 * 1024) {
+      c.smem = (size_t)(c.threads / G) * gb;
+      int bps = 0;
+      if (sweep_prog_configure(c, &bps) != cudaSuccess || bps < 1) return FASTILU_ERR_CUDA;
+      const int sms = sm_count(h->device);
+      const int64_t gpb = c.threads / G;
+      const int64_t need = std::max<int64_t>(1, (h->n + gpb - 1) / gpb);
+      c.grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * bps, need));
+      c.chunk = std::max<int64_t>(1, (h->n + c.grid - 1) / c.grid);
+      c.grid = (int)std::max<int64_t>(1, (h->n + c.chunk - 1) / c.chunk);
+      h->scfg = c;
+      int gi = 4;
+      while (gi < (double)h->nnz_own / std::max<int64_t>(h->n, 1) && gi < 32) gi *= 2;
+      h->G_init = gi;
+      int gt = 1;  // trisolve: 2 entries per lane in the fast path
+      while (2 * gt < nl_avg && gt < 32) gt *= 2;
+      h->G_tri = gt;
+      return FASTILU_OK;
+    }
+    c.prog = false;
+    c.threads = 512;
+  }
   uint32_t mul = 0;
   int bits = 0;
   c.hash = find_offset_hash(rp, ci, h->G, h->G + h->n, m_max, nthreads, &mul, &bits);
@@ -407,9 +440,27 @@ static fastilu_status create_impl(fastilu_handle h, int64_t n, const int64_t *ro
   for (int64_t r = h->G; r < h->nloc; r++) nl_own += dloc[r];
   const double nl_avg = n ? (double)nl_own / n : 1.0;
   const double u_avg = n ? (double)(h->nnz_own - n - nl_own) / n : 1.0;
-  (void)maxU;
-  fastilu_status fs = setup_configs(h, rp, ci, m_max, u_avg, nl_avg, nt);
+  // structure classes for the class-program sweep (falls back to the hash kernel if absent)
+  ClassProgram cp;
+  const bool have_prog =
+      !std::getenv("FASTILU_NO_CLASSES") &&
+      build_classes(rp, ci, dloc, h->nloc, h->G, h->G + n, arp, apos, nt, (size_t)256 << 20,
+                    1 << 16, cp);
+  fastilu_status fs = setup_configs(h, rp, ci, m_max, u_avg, nl_avg, maxU, have_prog, nt);
   if (fs) return fs;
+  if (h->scfg.prog) {
+    h->nclasses = cp.nclasses;
+    CU(dalloc(&h->d_rclass, (int64_t)cp.row_class.size()));
+    CU(dalloc(&h->d_coff, (int64_t)cp.class_off.size()));
+    CU(dalloc(&h->d_caoff, (int64_t)cp.class_aoff.size()));
+    CU(dalloc(&h->d_prog, (int64_t)cp.prog.size()));
+    CU(cudaMemcpy(h->d_rclass, cp.row_class.data(), 4 * cp.row_class.size(),
+                  cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(h->d_coff, cp.class_off.data(), 8 * cp.class_off.size(), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(h->d_caoff, cp.class_aoff.data(), 4 * cp.class_aoff.size(),
+                  cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(h->d_prog, cp.prog.data(), cp.prog.size(), cudaMemcpyHostToDevice));
+  }
   // device allocations
   CU(dalloc(&h->d_rp, h->nloc + 1));
   CU(dalloc(&h->d_ci, h->nnz_loc));
@@ -544,7 +595,12 @@ extern "C" fastilu_status fastilu_compute(fastilu_handle h, int nsweeps) {
     SweepArgs sa{P,           h->d_arp,      h->d_apos,     h->d_ahat, h->d_vals[ib],
                  h->d_vals[ob], h->d_ud[ib], h->d_ud[ob], r0,        r1,
                  h->opt.omega,  h->d_partials, h->d_err};
-    CU(launch_sweep(sa, h->scfg, st));
+    if (h->scfg.prog) {
+      ProgView pv{h->d_rclass, h->d_coff, h->d_caoff, h->d_prog};
+      CU(launch_sweep_prog(sa, pv, h->scfg, st));
+    } else {
+      CU(launch_sweep(sa, h->scfg, st));
+    }
     CU(launch_reduce(h->d_partials, h->scfg.grid, h->d_r2 + (sw - 1), st));
   }
   CU(cudaEventRecord(h->ev[2], st));
@@ -705,7 +761,8 @@ extern "C" fastilu_status fastilu_destroy(fastilu_handle h) {
   void *ptrs[] = {h->d_rp,    h->d_ci,    h->d_dloc,     h->d_arp,  h->d_aci,     h->d_apos,
                   h->d_adiag, h->d_aval,  h->d_vals[0],  h->d_vals[1], h->d_ud[0], h->d_ud[1],
                   h->d_ahat,  h->d_s,     h->d_ad,       h->d_y,    h->d_z[0],    h->d_z[1],
-                  h->d_w[0],  h->d_w[1],  h->d_bx,       h->d_partials, h->d_r2,  h->d_err};
+                  h->d_w[0],  h->d_w[1],  h->d_bx,       h->d_partials, h->d_r2,  h->d_err,
+                  h->d_rclass, h->d_coff, h->d_caoff, h->d_prog};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   if (h->h_err) cudaFreeHost(h->h_err);

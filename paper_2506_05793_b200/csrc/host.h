@@ -1,6 +1,7 @@
 // Private host-side declarations of libfastilu_b200 (not part of the ABI).
 #pragma once
 #include <cstdint>
+#include <algorithm>
 #include <vector>
 
 namespace fastilu {
@@ -34,5 +35,22 @@ int symbolic_iluk(int64_t nrows, const int64_t *rp, const int32_t *ci, int64_t g
                   int64_t o1, int K, int nthreads, Pattern &out, int64_t *bad);
 
 int hw_threads(int requested);
+
+// Structure classes of the owned rows and their position programs (classes.cpp).
+struct ClassProgram {
+  std::vector<int32_t> row_class;   // per owned row
+  std::vector<int64_t> class_off;   // nclasses + 1: byte offset of each class's program
+  std::vector<int32_t> class_aoff;  // per class: offset of the A-position part
+  std::vector<uint8_t> prog;        // positions in S_i (255 = absent)
+  int64_t nclasses = 0, nuclasses = 0;
+};
+
+// rp/ci/dloc: local S structure (nloc rows, local columns); owned rows [r0, r1); arp/apos:
+// A's row pointers (local rows) and the offset of each A entry inside its S row.  Returns
+// false (no classes) if a row is longer than 254 entries or the caps are exceeded.
+bool build_classes(const std::vector<int64_t> &rp, const std::vector<int32_t> &ci,
+                   const std::vector<int32_t> &dloc, int64_t nloc, int64_t r0, int64_t r1,
+                   const std::vector<int64_t> &arp, const std::vector<int32_t> &apos,
+                   int nthreads, size_t max_bytes, int32_t max_classes, ClassProgram &out);
 
 }  // namespace fastilu

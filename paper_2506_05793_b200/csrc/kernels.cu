@@ -299,6 +299,189 @@ cudaError_t launch_sweep(const SweepArgs &a, const SweepCfg &cfg, cudaStream_t s
   FASTILU_SWEEP_DISPATCH(launch_sweep_t, a, cfg, st)
 }
 
+// ----------------------------------------------------------------------------------------
+// a4 + a5, class-program variant (classes.cpp): the same recurrence in the same order, with
+// the index matching precomputed per structure class.  Per pivot t of row i, lane e loads
+// u_k,e (coalesced, L1/L2) and the byte prog[class][t][e] = position of (i, j_e) in S_i
+// (255 = not in S), then acc[p] -= l_ik u_kj.  No column loads, hashing or searching.
+// ----------------------------------------------------------------------------------------
+__host__ __device__ inline size_t prog_group_bytes(int cap_m, int G) {
+  size_t b = (size_t)cap_m * 8 + (size_t)G * 24;
+  return (b + 15) & ~(size_t)15;
+}
+
+template <int G, int E>
+__global__ void __launch_bounds__(512)
+sweep_prog_kernel(DevPattern P, ProgView pv, const int64_t *__restrict__ arp,
+                  const double *__restrict__ ahatA, const double *__restrict__ old,
+                  double *__restrict__ out, const double *__restrict__ udo,
+                  double *__restrict__ udn, int64_t r0, int64_t r1, int64_t chunk, double omega,
+                  double *__restrict__ partials, ErrFlags *err, int cap_m) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  auto blk = cg::this_thread_block();
+  auto tile = cg::tiled_partition<G>(blk);
+  const int gpb = blockDim.x / G;
+  const int gib = threadIdx.x / G;
+  const int lane = tile.thread_rank();
+  unsigned char *gb = smem + prog_group_bytes(cap_m, G) * gib;
+  double *acc = reinterpret_cast<double *>(gb);
+  int64_t *pub = reinterpret_cast<int64_t *>(acc + cap_m);  // pivot U-row starts
+  double *plv = reinterpret_cast<double *>(pub + G);        // l_ik
+  int32_t *plen = reinterpret_cast<int32_t *>(plv + G);     // U-row lengths
+  int32_t *poff = plen + G;                                 // program offsets
+  const bool damp = (omega != 1.0);
+  const double om1 = 1.0 - omega;
+  const uint8_t *__restrict__ prog = pv.prog;
+
+  double r2 = 0.0;
+  const int64_t cb = r0 + (int64_t)blockIdx.x * chunk;
+  const int64_t ce = min(r1, cb + chunk);
+  for (int64_t row = cb + gib; row < ce; row += gpb) {
+    const int64_t rb = P.rp[row];
+    const int m = (int)(P.rp[row + 1] - rb);
+    const int nl = P.dloc[row];
+    const int cls = pv.row_class[row - r0];
+    const int64_t pbase = pv.class_off[cls];
+    const int aoff = pv.class_aoff[cls];
+    const int64_t a0 = arp[row];
+    const int na = (int)(arp[row + 1] - a0);
+    for (int p = lane; p < m; p += G) acc[p] = 0.0;  // fill entries start from +0.0 (R4)
+    tile.sync();
+    for (int q = lane; q < na; q += G) acc[prog[pbase + aoff + q]] = ahatA[a0 + q];
+    int carry = 0;
+    for (int t0 = 0; t0 < nl; t0 += G) {
+      const int np = min(G, nl - t0);
+      int len = 0;
+      if (lane < np) {
+        const int k = P.ci[rb + t0 + lane];
+        const int64_t u0 = P.rp[k] + P.dloc[k] + 1;  // strict upper part of row k
+        len = (int)(P.rp[k + 1] - u0);
+        pub[lane] = u0;
+        plv[lane] = old[rb + t0 + lane];
+      }
+      const int excl = cg::exclusive_scan(tile, len);
+      if (lane < np) {
+        plen[lane] = len;
+        poff[lane] = carry + excl;
+      }
+      carry += tile.shfl(excl + len, G - 1);
+      tile.sync();
+      // software pipeline over the pivots: next pivot's (u, position) loaded ahead
+      double cu[E];
+      int cp[E];
+      {
+        const int64_t u0 = pub[0];
+        const int L = plen[0], po = poff[0];
+#pragma unroll
+        for (int e = 0; e < E; e++) {
+          const int idx = lane + e * G;
+          cu[e] = idx < L ? old[u0 + idx] : 0.0;
+          cp[e] = idx < L ? prog[pbase + po + idx] : 255;
+        }
+      }
+      for (int q = 0; q < np; q++) {
+        double nu[E];
+        int npp[E];
+#pragma unroll
+        for (int e = 0; e < E; e++) { nu[e] = 0.0; npp[e] = 255; }
+        if (q + 1 < np) {
+          const int64_t u0 = pub[q + 1];
+          const int L = plen[q + 1], po = poff[q + 1];
+#pragma unroll
+          for (int e = 0; e < E; e++) {
+            const int idx = lane + e * G;
+            if (idx < L) {
+              nu[e] = old[u0 + idx];
+              npp[e] = prog[pbase + po + idx];
+            }
+          }
+        }
+        const double l = plv[q];
+#pragma unroll
+        for (int e = 0; e < E; e++)
+          if (cp[e] != 255) acc[cp[e]] = __dsub_rn(acc[cp[e]], __dmul_rn(l, cu[e]));
+        tile.sync();
+#pragma unroll
+        for (int e = 0; e < E; e++) { cu[e] = nu[e]; cp[e] = npp[e]; }
+      }
+    }
+    tile.sync();
+    for (int p = lane; p < m; p += G) {
+      const double a = acc[p];
+      const double o = old[rb + p];
+      double nv, e;
+      if (p < nl) {
+        const double ujj = udo[P.ci[rb + p]];
+        e = __dsub_rn(a, __dmul_rn(o, ujj));
+        const double l = __ddiv_rn(a, ujj);
+        nv = damp ? __dadd_rn(__dmul_rn(om1, o), __dmul_rn(omega, l)) : l;
+      } else {
+        e = __dsub_rn(a, o);
+        nv = damp ? __dadd_rn(__dmul_rn(om1, o), __dmul_rn(omega, a)) : a;
+      }
+      r2 = fma(e, e, r2);
+      out[rb + p] = nv;
+      if (p == nl) {
+        udn[row] = nv;
+        if (bad_pivot(nv)) atomicMin(&err->zero_pivot, (unsigned long long)row);
+      }
+    }
+    tile.sync();
+  }
+  __shared__ double wsum[32];
+  double v = r2;
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); w++) t += wsum[w];
+    partials[blockIdx.x] = t;
+  }
+}
+
+template <int G, int E>
+static cudaError_t launch_prog_t(const SweepArgs &a, const ProgView &pv, const SweepCfg &c,
+                                 cudaStream_t st) {
+  sweep_prog_kernel<G, E><<<c.grid, c.threads, c.smem, st>>>(
+      a.P, pv, a.arp, a.ahatA, a.old, a.out, a.udo, a.udn, a.r0, a.r1, c.chunk, a.omega,
+      a.partials, a.err, c.cap_m);
+  return cudaGetLastError();
+}
+
+template <int G, int E>
+static cudaError_t prog_attr_t(const SweepCfg &c, int *bps) {
+  cudaError_t e = cudaFuncSetAttribute(sweep_prog_kernel<G, E>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(c.smem > 0 ? c.smem : 1));
+  if (e != cudaSuccess) return e;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, sweep_prog_kernel<G, E>, c.threads,
+                                                       c.smem);
+}
+
+#define FASTILU_PROG_DISPATCH(FN, ...)                                           \
+  switch (cfg.G * 8 + cfg.E) {                                                   \
+    case 4 * 8 + 1: return FN<4, 1>(__VA_ARGS__);                                \
+    case 4 * 8 + 2: return FN<4, 2>(__VA_ARGS__);                                \
+    case 8 * 8 + 1: return FN<8, 1>(__VA_ARGS__);                                \
+    case 8 * 8 + 2: return FN<8, 2>(__VA_ARGS__);                                \
+    case 16 * 8 + 1: return FN<16, 1>(__VA_ARGS__);                              \
+    case 16 * 8 + 2: return FN<16, 2>(__VA_ARGS__);                              \
+    case 32 * 8 + 1: return FN<32, 1>(__VA_ARGS__);                              \
+    case 32 * 8 + 2: return FN<32, 2>(__VA_ARGS__);                              \
+    case 32 * 8 + 4: return FN<32, 4>(__VA_ARGS__);                              \
+    default: return cudaErrorInvalidConfiguration;                               \
+  }
+
+cudaError_t sweep_prog_configure(const SweepCfg &cfg, int *blocks_per_sm) {
+  FASTILU_PROG_DISPATCH(prog_attr_t, cfg, blocks_per_sm)
+}
+
+cudaError_t launch_sweep_prog(const SweepArgs &a, const ProgView &pv, const SweepCfg &cfg,
+                              cudaStream_t st) {
+  FASTILU_PROG_DISPATCH(launch_prog_t, a, pv, cfg, st)
+}
+
 // deterministic sum of the per-block partials (one block, fixed order)
 __global__ void reduce_kernel(const double *__restrict__ partials, int np, double *dst) {
   __shared__ double sh[1024];

@@ -1,0 +1,106 @@
+"""Multi-rank CUDA path on ONE B200: P ranks as threads of this process (FASTILU_COMM_LOCAL), each
+with its own handle, stream and z-slab of rows, halos exchanged by the library (factor rows of
+the lower neighbour per sweep; z / w vector halos per trisolve sweep; s once).  Synchronous
+sweeps make every result independent of the partition: factors and x must be BITWISE equal to
+the single-GPU run (and therefore to the oracle's factors)."""
+import threading
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2506_05793_b200 as F
+import problems as P
+
+pytestmark = pytest.mark.gpu
+
+
+def split_planes(gz, world):
+    return [(gz * r // world, gz * (r + 1) // world) for r in range(world)]
+
+
+def run_partitioned(kind, g, gz, k, ns, nt, world, omega=1.0, omega_tri=1.0):
+    plane = g * g
+    global_n = plane * gz
+    b = P.rhs_positive(global_n)
+    grp = F.fastilu_group_create(world)
+    out = [None] * world
+    errs = [None] * world
+
+    def worker(r):
+        try:
+            torch.cuda.set_device(0)
+            z0, z1 = split_planes(gz, world)[r]
+            need = F.fastilu_required_lead_rows(P.bandwidth(kind, g), k)
+            lp = min(z0, -(-need // plane))
+            blk = P.make(kind, g, gz, planes=(z0 - lp, z1))
+            f = F.FastILU(blk.row_ptr, blk.col_idx, blk.values, k, omega=omega,
+                          omega_tri=omega_tri, rank=r, nranks=world, comm_kind=F.COMM_LOCAL,
+                          group=grp, global_n=global_n, row_begin=z0 * plane,
+                          n_lead=lp * plane, n=(z1 - z0) * plane)
+            f.compute(ns)
+            vals, s = f.factors()
+            tb = torch.tensor(b[z0 * plane:z1 * plane], device="cuda")
+            tx = torch.empty_like(tb)
+            f.apply(tb, tx, nt)
+            torch.cuda.synchronize()
+            out[r] = (vals, s, tx.cpu().numpy(), f.residual_history(), f.pattern())
+            f.close()
+        except Exception as e:  # surfaced below
+            errs[r] = e
+
+    th = [threading.Thread(target=worker, args=(r,), daemon=True) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    assert not any(t.is_alive() for t in th), "rank threads hung"
+    F.fastilu_group_destroy(grp)
+    for e in errs:
+        if e is not None:
+            raise e
+    return out, b
+
+
+@pytest.mark.parametrize("kind,g,gz,k,ns,nt,world", [
+    ("27pt", 10, 16, 1, 3, 5, 2),
+    ("27pt", 8, 24, 2, 3, 4, 3),
+    ("7pt", 16, 20, 0, 3, 5, 4),
+    ("27pt", 12, 30, 1, 2, 3, 4),
+])
+def test_partition_bitwise_equal_single_gpu(kind, g, gz, k, ns, nt, world):
+    a = P.make(kind, g, gz)
+    b = P.rhs_positive(a.n)
+    f1 = F.FastILU(a.row_ptr, a.col_idx, a.values, k)
+    f1.compute(ns)
+    v1, s1 = f1.factors()
+    tb = torch.tensor(b, device="cuda")
+    tx = torch.empty_like(tb)
+    f1.apply(tb, tx, nt)
+    torch.cuda.synchronize()
+    x1 = tx.cpu().numpy()
+    out, _ = run_partitioned(kind, g, gz, k, ns, nt, world)
+    vP = np.concatenate([o[0] for o in out])
+    sP = np.concatenate([o[1] for o in out])
+    xP = np.concatenate([o[2] for o in out])
+    assert np.array_equal(np.concatenate([o[4][1] for o in out]), f1.pattern()[1])
+    assert np.array_equal(sP, s1)
+    assert np.array_equal(vP, v1), "partitioned factors differ from the single-GPU run"
+    assert np.array_equal(xP, x1), "partitioned x differs from the single-GPU run"
+    for o in out:  # residual: rank-ordered sum of the same per-row terms
+        np.testing.assert_allclose(o[3], f1.residual_history(), rtol=1e-12)
+    fo = oracle.compute(a, k, ns)
+    assert np.array_equal(vP, fo.vals)
+
+
+def test_partition_damped():
+    kind, g, gz, k, ns, nt = "27pt", 8, 18, 1, 3, 3
+    a = P.make(kind, g, gz)
+    b = P.rhs_positive(a.n)
+    out, _ = run_partitioned(kind, g, gz, k, ns, nt, 3, omega=0.8, omega_tri=0.9)
+    fo = oracle.compute(a, k, ns, 0.8)
+    assert np.array_equal(np.concatenate([o[0] for o in out]), fo.vals)
+    xo = oracle.apply(fo, b, nt, 0.9)
+    xP = np.concatenate([o[2] for o in out])
+    assert np.all(np.abs(xP - xo) <= 1e-12 * np.abs(xo))

@@ -82,6 +82,17 @@ def test_stencils(kind, g, gz, k, ns, nt):
     full_check(P.make(kind, g, gz), k, ns, nt)
 
 
+@pytest.mark.parametrize("kind,g,gz,k,ns,nt", [
+    ("27pt", 12, None, 1, 3, 5),
+    ("27pt", 9, 11, 2, 3, 3),
+    ("7pt", 17, None, 0, 3, 5),
+])
+def test_hash_kernel_fallback(kind, g, gz, k, ns, nt, monkeypatch):
+    """The general (hash / binary-search) sweep kernel, forced by FASTILU_NO_CLASSES."""
+    monkeypatch.setenv("FASTILU_NO_CLASSES", "1")
+    full_check(P.make(kind, g, gz), k, ns, nt)
+
+
 def test_3dof_pattern():
     full_check(P.elasticity_pattern_3dof(5), 1, 3, 3)
 
