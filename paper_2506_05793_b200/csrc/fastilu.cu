@@ -250,8 +250,7 @@ static fastilu_status setup_configs(fastilu_handle h, const std::vector<int64_t>
       const int64_t gpb = c.threads / G;
       const int64_t need = std::max<int64_t>(1, (h->n + gpb - 1) / gpb);
       c.grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * bps, need));
-      c.chunk = std::max<int64_t>(1, (h->n + c.grid - 1) / c.grid);
-      c.grid = (int)std::max<int64_t>(1, (h->n + c.chunk - 1) / c.chunk);
+      c.chunk = gpb * 4;  // rows per block tile (4 rows per group)
       h->scfg = c;
       int gi = 4;
       while (gi < (double)h->nnz_own / std::max<int64_t>(h->n, 1) && gi < 32) gi *= 2;
@@ -284,8 +283,7 @@ static fastilu_status setup_configs(fastilu_handle h, const std::vector<int64_t>
   const int64_t gpb = c.threads / G;
   const int64_t need = std::max<int64_t>(1, (h->n + gpb - 1) / gpb);
   c.grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * bps, need));
-  c.chunk = std::max<int64_t>(1, (h->n + c.grid - 1) / c.grid);
-  c.grid = (int)std::max<int64_t>(1, (h->n + c.chunk - 1) / c.chunk);
+  c.chunk = gpb * 4;  // rows per block tile (4 rows per group)
   h->scfg = c;
   int gi = 4;
   while (gi < (double)h->nnz_own / std::max<int64_t>(h->n, 1) && gi < 32) gi *= 2;

@@ -154,9 +154,12 @@ sweep_kernel(DevPattern P, const int64_t *__restrict__ arp, const int32_t *__res
   const double om1 = 1.0 - omega;
 
   double r2 = 0.0;
-  const int64_t cb = r0 + (int64_t)blockIdx.x * chunk;
-  const int64_t ce = min(r1, cb + chunk);
-  for (int64_t row = cb + gib; row < ce; row += gpb) {
+  // tile-strided rows: block b takes tiles of `chunk` consecutive rows, tiles strided by the
+  // grid, so all SMs work inside one window of grid*chunk rows (the pivots' U-rows stay in
+  // L2) while each block walks consecutive rows (neighbours share U-rows in L1).
+  for (int64_t row = r0 + (int64_t)blockIdx.x * chunk + gib; row < r1;
+       row += ((row - r0) % chunk + gpb < chunk) ? gpb
+                                                 : (int64_t)(gridDim.x - 1) * chunk + gpb) {
     const int64_t rb = P.rp[row];
     const int m = (int)(P.rp[row + 1] - rb);
     const int nl = P.dloc[row];
@@ -334,9 +337,12 @@ sweep_prog_kernel(DevPattern P, ProgView pv, const int64_t *__restrict__ arp,
   const uint8_t *__restrict__ prog = pv.prog;
 
   double r2 = 0.0;
-  const int64_t cb = r0 + (int64_t)blockIdx.x * chunk;
-  const int64_t ce = min(r1, cb + chunk);
-  for (int64_t row = cb + gib; row < ce; row += gpb) {
+  // tile-strided rows: block b takes tiles of `chunk` consecutive rows, tiles strided by the
+  // grid, so all SMs work inside one window of grid*chunk rows (the pivots' U-rows stay in
+  // L2) while each block walks consecutive rows (neighbours share U-rows in L1).
+  for (int64_t row = r0 + (int64_t)blockIdx.x * chunk + gib; row < r1;
+       row += ((row - r0) % chunk + gpb < chunk) ? gpb
+                                                 : (int64_t)(gridDim.x - 1) * chunk + gpb) {
     const int64_t rb = P.rp[row];
     const int m = (int)(P.rp[row + 1] - rb);
     const int nl = P.dloc[row];
