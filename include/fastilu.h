@@ -146,6 +146,10 @@ fastilu_status fastilu_get_residual_history(fastilu_handle h, double *hist, int 
 /* Device-time breakdown of the last compute/apply in milliseconds (CUDA events):
  * t[0] = scale+init, t[1] = all sweeps, t[2] = apply (last call).  */
 fastilu_status fastilu_get_timings(fastilu_handle h, double *t3);
+/* One-line description of the handle's kernel configuration (path "tsell" = template-SELL
+ * with the JIT-specialised sweep, "csr-classes" / "csr-hash" / "csr-bsearch" = CSR kernels),
+ * written NUL-terminated into buf (at most cap bytes). */
+fastilu_status fastilu_get_info(fastilu_handle h, char *buf, int cap);
 const char *fastilu_status_string(fastilu_status s);
 int64_t fastilu_error_index(fastilu_handle h);
 

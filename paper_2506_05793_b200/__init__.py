@@ -64,6 +64,7 @@ _SIGS = {
     "fastilu_get_factors": (C.c_int, [H, F64P, F64P]),
     "fastilu_get_residual_history": (C.c_int, [H, F64P, C.c_int, C.POINTER(C.c_int)]),
     "fastilu_get_timings": (C.c_int, [H, F64P]),
+    "fastilu_get_info": (C.c_int, [H, C.c_char_p, C.c_int]),
     "fastilu_status_string": (C.c_char_p, [C.c_int]),
     "fastilu_error_index": (C.c_int64, [H]),
     "fastilu_symbolic": (C.c_int, [C.c_int64, I64P, I32P, C.c_int, C.c_int, I64P, I64P, I32P,
@@ -285,6 +286,12 @@ class FastILU:
         t = np.zeros(3)
         _check(lib().fastilu_get_timings(self._h, _p(t, F64P)), "fastilu_get_timings", self._h)
         return {"init_ms": t[0], "sweeps_ms": t[1], "apply_ms": t[2]}
+
+    def info(self) -> str:
+        """Kernel configuration of this handle (fastilu_get_info)."""
+        buf = C.create_string_buffer(512)
+        _check(lib().fastilu_get_info(self._h, buf, 512), "fastilu_get_info", self._h)
+        return buf.value.decode()
 
     def close(self):
         if getattr(self, "_h", None):

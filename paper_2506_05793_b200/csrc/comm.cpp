@@ -163,7 +163,8 @@ static fastilu_status allgather_i64(Comm *c, const std::vector<int64_t> &mine,
 
 fastilu_status comm_setup(Comm *&out, const fastilu_options &o, int64_t row_begin, int64_t n,
                           int64_t G, int64_t H, const int64_t *h_rp, int64_t stat,
-                          int64_t *stat_global, cudaStream_t st) {
+                          int64_t *stat_global, int tsell_W, uint64_t layout_hash,
+                          cudaStream_t st) {
   out = nullptr;
   Comm *c = new (std::nothrow) Comm();
   if (!c) return FASTILU_ERR_OOM;
@@ -215,15 +216,23 @@ fastilu_status comm_setup(Comm *&out, const fastilu_options &o, int64_t row_begi
   }
   // factor halo: I send my last G_{p+1} owned rows (local rows [G + n - G_{p+1}, G + n))
   const int64_t gn = (p + 1 < P) ? c->GG[p + 1] : 0;
-  c->send_off = h_rp[G + n - gn];
-  c->send_cnt = h_rp[G + n] - c->send_off;
-  c->recv_cnt = h_rp[G];
-  s = allgather_i64(c, {c->send_cnt, c->recv_cnt, stat}, all, st);
+  if (tsell_W > 0) {  // whole 32-row slices of the template layout (G, n multiples of 32)
+    c->send_off = (G + n - gn) * (int64_t)tsell_W;
+    c->send_cnt = gn * (int64_t)tsell_W;
+    c->recv_cnt = G * (int64_t)tsell_W;
+  } else {
+    c->send_off = h_rp[G + n - gn];
+    c->send_cnt = h_rp[G + n] - c->send_off;
+    c->recv_cnt = h_rp[G];
+  }
+  s = allgather_i64(c, {c->send_cnt, c->recv_cnt, stat, (int64_t)layout_hash}, all, st);
   if (s) return s;
   for (int r = 0; r + 1 < P; r++)
-    if (all[3 * r] != all[3 * (r + 1) + 1]) return FASTILU_ERR_BAD_MATRIX;  // patterns disagree
+    if (all[4 * r] != all[4 * (r + 1) + 1]) return FASTILU_ERR_BAD_MATRIX;  // patterns disagree
+  for (int r = 0; r < P; r++)
+    if (all[4 * r + 3] != all[3]) return FASTILU_ERR_UNSUPPORTED;  // layouts differ
   *stat_global = 0;
-  for (int r = 0; r < P; r++) *stat_global += all[3 * r + 2];
+  for (int r = 0; r < P; r++) *stat_global += all[4 * r + 2];
   return FASTILU_OK;
 }
 

@@ -17,11 +17,13 @@ struct Comm;
 // statistics and results stay bitwise independent of the partition.
 fastilu_status comm_setup(Comm *&out, const fastilu_options &opts, int64_t row_begin, int64_t n,
                           int64_t G, int64_t H, const int64_t *h_rp_local, int64_t stat,
-                          int64_t *stat_global, cudaStream_t st);
+                          int64_t *stat_global, int tsell_W, uint64_t layout_hash,
+                          cudaStream_t st);
 // Vector halo on an extended vector [G | n | H]: lower ghosts from rank-1's last G owned
 // entries, upper ghosts from rank+1's first H owned entries.
 fastilu_status comm_vector_halo(Comm *c, double *x, cudaStream_t st, bool lower, bool upper);
-// Factor halo before a sweep: the G ghost rows' values (whole rows, S order) and their
+// Factor halo before a sweep: the G ghost rows' values (whole rows: CSR S order, or whole
+// 32-row template slices when tsell_W > 0) and their
 // diagonal copies from rank-1.
 fastilu_status comm_factor_halo(Comm *c, double *vals, const int64_t *d_rp, double *udiag,
                                 cudaStream_t st);

@@ -94,6 +94,28 @@ cudaError_t launch_jacobi_U(const DevPattern &P, const double *vals, const doubl
                             const double *s, int64_t r0, int64_t r1, int64_t Gh, double omega,
                             bool final, int G, cudaStream_t st);
 
+// ---- template-SELL layout (tsell.h): one lane per row, slot(i, w) = ((i>>5) W + w) 32 + (i&31)
+struct TDev {
+  int W, c0, WA, words;
+  const int32_t *off;     // W template offsets
+  const int32_t *offA;    // WA offsets of A's sub-template
+  const int8_t *w2a;      // W -> A index or -1
+  const unsigned long long *mask;  // presence bits, [slice][word][lane]
+  const int32_t *asrc;    // [slice][a][lane]: index of A's entry in the local A arrays, or -1
+};
+
+cudaError_t launch_tsell_init(const TDev &t, const double *aval, const double *s,
+                              const double *ad, int64_t r0, int64_t r1, double *ahatT,
+                              double *vals, double *udiag, ErrFlags *err, cudaStream_t st);
+cudaError_t launch_tsell_jacobi(const TDev &t, bool lower, const double *vals,
+                                const double *udiag, const double *rhs, const double *xo,
+                                double *xn, double *xfinal, const double *s, int64_t r0,
+                                int64_t r1, int64_t Gh, double omega, bool final,
+                                cudaStream_t st);
+// deterministic sum of partials into *dst; also resets the tile counter (if non-null) to 0
+cudaError_t launch_reduce_reset(const double *partials, int np, double *dst,
+                                unsigned int *counter, cudaStream_t st);
+
 int sm_count(int device);
 
 }  // namespace fastilu

@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -16,6 +17,8 @@
 #include "comm.h"
 #include "device.h"
 #include "host.h"
+#include "jit.h"
+#include "tsell.h"
 
 using namespace fastilu;
 
@@ -53,6 +56,17 @@ struct fastilu_handle_s {
   int64_t *d_coff = nullptr;
   uint8_t *d_prog = nullptr;
   int64_t nclasses = 0;
+  // template-SELL fast path (tsell.h)
+  bool tsell = false;
+  Template T;
+  int64_t nsl = 0;  // slices of 32 local rows
+  int32_t *d_toff = nullptr, *d_toffA = nullptr, *d_tasrc = nullptr;
+  int8_t *d_tw2a = nullptr;
+  unsigned long long *d_tmask = nullptr;
+  unsigned int *d_counter = nullptr;
+  void *jit_sweep = nullptr;
+  int t_threads = 128, t_grid = 1, t_regs = 0, t_spill = 0;
+  int64_t t_ntiles = 0;
   ErrFlags *d_err = nullptr;
   ErrFlags *h_err = nullptr;  // pinned
   double *h_r2 = nullptr;     // pinned, hist_cap
@@ -304,6 +318,62 @@ static fastilu_status upload_values(fastilu_handle h, const double *values, bool
   return FASTILU_OK;
 }
 
+// Template-SELL: compile the template-specialised sweep, allocate and upload the layout.
+static fastilu_status setup_tsell(fastilu_handle h, const std::vector<unsigned long long> &mask,
+                                  const std::vector<int32_t> &asrc) {
+  const Template &T = h->T;
+  h->nsl = (h->nloc + 31) / 32;
+  const char *ev_th = std::getenv("FASTILU_TSELL_THREADS");
+  const char *ev_ch = std::getenv("FASTILU_TSELL_CHUNK");
+  const int threads = ev_th ? std::max(32, atoi(ev_th) / 32 * 32) : 128;
+  // accumulators per pass: all targets when they fit the register budget
+  int chunk = T.W <= 72 ? T.W : (T.W + 1) / 2 <= 72 ? (T.W + 1) / 2 : 64;
+  if (ev_ch) chunk = std::max(1, atoi(ev_ch));
+  std::string log;
+  const std::string src = sweep_source(T, threads, chunk);
+  if (jit_get(src, "fastilu_tsell_sweep", h->device, &h->jit_sweep, &log)) {
+    if (std::getenv("FASTILU_DEBUG")) fprintf(stderr, "fastilu: JIT failed: %s\n", log.c_str());
+    return FASTILU_ERR_UNSUPPORTED;
+  }
+  int bps = 0;
+  jit_func_info(h->jit_sweep, &h->t_regs, &h->t_spill, threads, &bps);
+  if (std::getenv("FASTILU_DEBUG"))
+    fprintf(stderr, "fastilu: tsell W=%d c0=%d WA=%d terms=%zu regs=%d local=%d bps=%d\n", T.W,
+            T.c0, T.WA, T.terms.size(), h->t_regs, h->t_spill, bps);
+  if (bps < 1) return FASTILU_ERR_UNSUPPORTED;
+  h->t_threads = threads;
+  h->t_ntiles = std::max<int64_t>(1, (h->n + threads - 1) / threads);
+  h->t_grid = (int)std::min<int64_t>((int64_t)sm_count(h->device) * bps, h->t_ntiles);
+  const int64_t nv = h->nsl * T.W * 32;
+  for (int b = 0; b < 2; b++) {
+    CU(dalloc(&h->d_vals[b], nv));
+    CU(cudaMemset(h->d_vals[b], 0, sizeof(double) * nv));  // absent slots stay +0.0
+  }
+  CU(dalloc(&h->d_ahat, h->nsl * T.WA * 32));
+  CU(cudaMemset(h->d_ahat, 0, sizeof(double) * h->nsl * T.WA * 32));
+  CU(dalloc(&h->d_tmask, (int64_t)mask.size()));
+  CU(dalloc(&h->d_tasrc, (int64_t)asrc.size()));
+  CU(dalloc(&h->d_toff, T.W));
+  CU(dalloc(&h->d_toffA, T.WA));
+  CU(dalloc(&h->d_tw2a, T.W));
+  CU(dalloc(&h->d_counter, 1));
+  CU(dalloc(&h->d_partials, h->t_ntiles));
+  CU(cudaMemset(h->d_counter, 0, sizeof(unsigned int)));
+  CU(cudaMemcpy(h->d_tmask, mask.data(), 8 * mask.size(), cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(h->d_tasrc, asrc.data(), 4 * asrc.size(), cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(h->d_toff, T.off.data(), 4 * T.W, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(h->d_toffA, T.offA.data(), 4 * T.WA, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(h->d_tw2a, T.w2a.data(), T.W, cudaMemcpyHostToDevice));
+  int gt = 1;  // (unused by the template trisolve; kept for introspection)
+  h->G_tri = gt;
+  return FASTILU_OK;
+}
+
+static TDev tdev(fastilu_handle h) {
+  return TDev{h->T.W,   h->T.c0,    h->T.WA,  h->T.words, h->d_toff,
+              h->d_toffA, h->d_tw2a, h->d_tmask, h->d_tasrc};
+}
+
 static fastilu_status create_impl(fastilu_handle h, int64_t n, const int64_t *row_ptr,
                                   const int32_t *col_idx, const double *values, int K) {
   const fastilu_options &o = h->opt;
@@ -350,6 +420,8 @@ static fastilu_status create_impl(fastilu_handle h, int64_t n, const int64_t *ro
   h->G = h->row_begin - mincol;
   h->H = maxcol - (row_end - 1);
   if (!multi && (h->G != 0 || h->H != 0)) return FASTILU_ERR_BAD_MATRIX;
+  // multi-GPU: whole 32-row slices of ghost rows (template-SELL layout), if the margin allows
+  if (multi && h->G % 32 && (h->G + 31) / 32 * 32 <= own_r0) h->G = (h->G + 31) / 32 * 32;
   if (h->G > own_r0) return FASTILU_ERR_UNSUPPORTED;  // ghost rows beyond the supplied margin
   h->lbase = h->row_begin - h->G;
   h->nloc = h->G + n;
@@ -416,7 +488,6 @@ static fastilu_status create_impl(fastilu_handle h, int64_t n, const int64_t *ro
           const int64_t q0 = h->a_in_off + arp[r], q1 = h->a_in_off + arp[r + 1];
           for (int64_t q = q0; q < q1; q++)
             if (col_idx[q] == g) adiag[r] = (int32_t)(q - q0);
-          if (r < h->G) continue;
           int64_t p = rp[r];
           for (int64_t q = q0; q < q1; q++) {
             const int64_t c = col_idx[q] - h->lbase;
@@ -438,13 +509,25 @@ static fastilu_status create_impl(fastilu_handle h, int64_t n, const int64_t *ro
   for (int64_t r = h->G; r < h->nloc; r++) nl_own += dloc[r];
   const double nl_avg = n ? (double)nl_own / n : 1.0;
   const double u_avg = n ? (double)(h->nnz_own - n - nl_own) / n : 1.0;
+  // template-SELL fast path for structured patterns (else the CSR kernels below)
+  if (!std::getenv("FASTILU_NO_TSELL") && (!multi || (n % 32 == 0 && h->G % 32 == 0)) &&
+      jit_available(nullptr)) {
+    std::vector<unsigned long long> tmask;
+    std::vector<int32_t> tasrc;
+    if (build_template(rp, ci, h->nloc, arp, aci, nt, h->T, tmask, tasrc)) {
+      fastilu_status ts = setup_tsell(h, tmask, tasrc);
+      if (ts == FASTILU_OK) h->tsell = true;
+      else if (ts != FASTILU_ERR_UNSUPPORTED) return ts;
+    }
+  }
   // structure classes for the class-program sweep (falls back to the hash kernel if absent)
   ClassProgram cp;
-  const bool have_prog =
+  const bool have_prog = !h->tsell &&
       !std::getenv("FASTILU_NO_CLASSES") &&
       build_classes(rp, ci, dloc, h->nloc, h->G, h->G + n, arp, apos, nt, (size_t)256 << 20,
                     1 << 16, cp);
-  fastilu_status fs = setup_configs(h, rp, ci, m_max, u_avg, nl_avg, maxU, have_prog, nt);
+  fastilu_status fs = h->tsell ? FASTILU_OK
+                              : setup_configs(h, rp, ci, m_max, u_avg, nl_avg, maxU, have_prog, nt);
   if (fs) return fs;
   if (h->scfg.prog) {
     h->nclasses = cp.nclasses;
@@ -460,33 +543,39 @@ static fastilu_status create_impl(fastilu_handle h, int64_t n, const int64_t *ro
     CU(cudaMemcpy(h->d_prog, cp.prog.data(), cp.prog.size(), cudaMemcpyHostToDevice));
   }
   // device allocations
-  CU(dalloc(&h->d_rp, h->nloc + 1));
-  CU(dalloc(&h->d_ci, h->nnz_loc));
-  CU(dalloc(&h->d_dloc, h->nloc));
+  if (!h->tsell) {  // CSR structure of S (the template path needs none)
+    CU(dalloc(&h->d_rp, h->nloc + 1));
+    CU(dalloc(&h->d_ci, h->nnz_loc));
+    CU(dalloc(&h->d_dloc, h->nloc));
+    CU(dalloc(&h->d_aci, h->nnzA_loc));
+    CU(dalloc(&h->d_apos, h->nnzA_loc));
+    CU(dalloc(&h->d_ahat, h->nnzA_loc));  // ahat on A's pattern
+    CU(dalloc(&h->d_partials, h->scfg.grid));
+    for (int b = 0; b < 2; b++) CU(dalloc(&h->d_vals[b], h->nnz_loc));
+  }
   CU(dalloc(&h->d_arp, h->nloc + 1));
-  CU(dalloc(&h->d_aci, h->nnzA_loc));
-  CU(dalloc(&h->d_apos, h->nnzA_loc));
   CU(dalloc(&h->d_adiag, h->nloc));
   CU(dalloc(&h->d_aval, h->nnzA_loc));
   for (int b = 0; b < 2; b++) {
-    CU(dalloc(&h->d_vals[b], h->nnz_loc));
     CU(dalloc(&h->d_ud[b], h->E));
     CU(dalloc(&h->d_z[b], h->E));
     CU(dalloc(&h->d_w[b], h->E));
   }
-  CU(dalloc(&h->d_ahat, h->nnzA_loc));  // ahat on A's pattern
   CU(dalloc(&h->d_s, h->E));
   CU(dalloc(&h->d_ad, h->E));
   CU(dalloc(&h->d_y, h->E));
-  CU(dalloc(&h->d_partials, h->scfg.grid));
   CU(dalloc(&h->d_err, 1));
   CU(cudaMallocHost((void **)&h->h_err, sizeof(ErrFlags)));
-  CU(cudaMemcpy(h->d_rp, rp.data(), sizeof(int64_t) * rp.size(), cudaMemcpyHostToDevice));
-  CU(cudaMemcpy(h->d_ci, ci.data(), sizeof(int32_t) * ci.size(), cudaMemcpyHostToDevice));
-  CU(cudaMemcpy(h->d_dloc, dloc.data(), sizeof(int32_t) * dloc.size(), cudaMemcpyHostToDevice));
+  if (!h->tsell) {
+    CU(cudaMemcpy(h->d_rp, rp.data(), sizeof(int64_t) * rp.size(), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(h->d_ci, ci.data(), sizeof(int32_t) * ci.size(), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(h->d_dloc, dloc.data(), sizeof(int32_t) * dloc.size(),
+                  cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(h->d_aci, aci.data(), sizeof(int32_t) * aci.size(), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(h->d_apos, apos.data(), sizeof(int32_t) * apos.size(),
+                  cudaMemcpyHostToDevice));
+  }
   CU(cudaMemcpy(h->d_arp, arp.data(), sizeof(int64_t) * arp.size(), cudaMemcpyHostToDevice));
-  CU(cudaMemcpy(h->d_aci, aci.data(), sizeof(int32_t) * aci.size(), cudaMemcpyHostToDevice));
-  CU(cudaMemcpy(h->d_apos, apos.data(), sizeof(int32_t) * apos.size(), cudaMemcpyHostToDevice));
   CU(cudaMemcpy(h->d_adiag, adiag.data(), sizeof(int32_t) * adiag.size(),
                 cudaMemcpyHostToDevice));
   CU(cudaMemset(h->d_s, 0, sizeof(double) * h->E));
@@ -500,7 +589,8 @@ static fastilu_status create_impl(fastilu_handle h, int64_t n, const int64_t *ro
   if (multi) {
     int64_t nl_global = 0;
     fastilu_status cs = comm_setup(h->comm, h->opt, h->row_begin, h->n, h->G, h->H, rp.data(),
-                                   nl_own, &nl_global, h->stream);
+                                   nl_own, &nl_global, h->tsell ? h->T.W : 0,
+                                   h->tsell ? h->T.hash : 0, h->stream);
     if (cs) return cs;
     const double nlg = (double)nl_global / (double)std::max<int64_t>(h->global_n, 1);
     int gt = 1;  // same rule as setup_configs, from the GLOBAL average (partition-independent)
@@ -579,9 +669,13 @@ extern "C" fastilu_status fastilu_compute(fastilu_handle h, int nsweeps) {
     fastilu_status cs = comm_vector_halo(h->comm, h->d_s, st, false, true);
     if (cs) return cs;
   }
-  // a3: ahat on S and the initial guess (iterate 0) for the owned rows
-  CU(launch_init(P, h->d_arp, h->d_aci, h->d_apos, h->d_aval, h->d_s, h->d_ad, r0, r1,
-                 h->d_ahat, h->d_vals[0], h->d_ud[0], h->d_err, h->G_init, st));
+  // a3: ahat and the initial guess (iterate 0) for the owned rows
+  if (h->tsell)
+    CU(launch_tsell_init(tdev(h), h->d_aval, h->d_s, h->d_ad, r0, r1, h->d_ahat, h->d_vals[0],
+                         h->d_ud[0], h->d_err, st));
+  else
+    CU(launch_init(P, h->d_arp, h->d_aci, h->d_apos, h->d_aval, h->d_s, h->d_ad, r0, r1,
+                   h->d_ahat, h->d_vals[0], h->d_ud[0], h->d_err, h->G_init, st));
   CU(cudaEventRecord(h->ev[1], st));
   // a4/a5: nsweeps synchronous sweeps, ping-pong buffers
   for (int sw = 1; sw <= nsweeps; sw++) {
@@ -593,6 +687,20 @@ extern "C" fastilu_status fastilu_compute(fastilu_handle h, int nsweeps) {
     SweepArgs sa{P,           h->d_arp,      h->d_apos,     h->d_ahat, h->d_vals[ib],
                  h->d_vals[ob], h->d_ud[ib], h->d_ud[ob], r0,        r1,
                  h->opt.omega,  h->d_partials, h->d_err};
+    if (h->tsell) {
+      const double *old = h->d_vals[ib], *ahat = h->d_ahat, *udo = h->d_ud[ib];
+      double *outp = h->d_vals[ob], *udn = h->d_ud[ob], *part = h->d_partials;
+      const unsigned long long *mk = h->d_tmask;
+      long long a0 = r0, a1 = r1;
+      double om = h->opt.omega;
+      unsigned long long *zp = &h->d_err->zero_pivot;
+      unsigned int *ctr = h->d_counter;
+      void *args[] = {&old, &outp, &ahat, &mk, &udo, &udn, &a0, &a1, &om, &part, &zp, &ctr};
+      if (jit_launch(h->jit_sweep, h->t_grid, h->t_threads, st, args)) return FASTILU_ERR_CUDA;
+      CU(launch_reduce_reset(h->d_partials, (int)h->t_ntiles, h->d_r2 + (sw - 1), h->d_counter,
+                             st));
+      continue;
+    }
     if (h->scfg.prog) {
       ProgView pv{h->d_rclass, h->d_coff, h->d_caoff, h->d_prog};
       CU(launch_sweep_prog(sa, pv, h->scfg, st));
@@ -647,7 +755,11 @@ static fastilu_status apply_impl(fastilu_handle h, const double *b, double *x, i
       fastilu_status cs = comm_vector_halo(h->comm, h->d_z[(t - 2) & 1], st, true, false);
       if (cs) return cs;
     }
-    CU(launch_jacobi_L(P, vals, h->d_y, zo, h->d_z[(t - 1) & 1], r0, r1, om, h->G_tri, st));
+    if (h->tsell)
+      CU(launch_tsell_jacobi(tdev(h), true, vals, nullptr, h->d_y, zo, h->d_z[(t - 1) & 1],
+                             nullptr, nullptr, r0, r1, 0, om, false, st));
+    else
+      CU(launch_jacobi_L(P, vals, h->d_y, zo, h->d_z[(t - 1) & 1], r0, r1, om, h->G_tri, st));
   }
   const double *zf = h->d_z[(ntri - 1) & 1];
   // a9: U sweeps.  t = 1: w1 = w z / u_ii; the last sweep writes x = s o w
@@ -657,8 +769,12 @@ static fastilu_status apply_impl(fastilu_handle h, const double *b, double *x, i
       fastilu_status cs = comm_vector_halo(h->comm, h->d_w[(t - 2) & 1], st, false, true);
       if (cs) return cs;
     }
-    CU(launch_jacobi_U(P, vals, ud, zf, h->d_w[(t - 2) & 1], h->d_w[(t - 1) & 1], x, h->d_s, r0,
-                       r1, h->G, om, t == ntri, h->G_tri, st));
+    if (h->tsell)
+      CU(launch_tsell_jacobi(tdev(h), false, vals, ud, zf, h->d_w[(t - 2) & 1],
+                             h->d_w[(t - 1) & 1], x, h->d_s, r0, r1, h->G, om, t == ntri, st));
+    else
+      CU(launch_jacobi_U(P, vals, ud, zf, h->d_w[(t - 2) & 1], h->d_w[(t - 1) & 1], x, h->d_s,
+                         r0, r1, h->G, om, t == ntri, h->G_tri, st));
   }
   return FASTILU_OK;
 }
@@ -724,9 +840,23 @@ extern "C" fastilu_status fastilu_get_factors(fastilu_handle h, double *vals, do
   if (!h->computed) return FASTILU_ERR_STATE;
   cudaSetDevice(h->device);
   CU(cudaStreamSynchronize(h->stream));
-  if (vals)
+  if (vals && h->tsell) {  // gather the owned rows' S entries out of the template slots
+    const Template &T = h->T;
+    std::vector<double> tv((size_t)h->nsl * T.W * 32);
+    CU(cudaMemcpy(tv.data(), h->d_vals[h->cur], sizeof(double) * tv.size(),
+                  cudaMemcpyDeviceToHost));
+    for (int64_t r = 0; r < h->n; r++) {
+      const int64_t i = h->G + r, g = h->row_begin + r;
+      for (int64_t p = h->h_rp[r]; p < h->h_rp[r + 1]; p++) {
+        const int32_t o = (int32_t)(h->h_ci[p] - g);
+        const int w = (int)(std::lower_bound(T.off.begin(), T.off.end(), o) - T.off.begin());
+        vals[p] = tv[((i >> 5) * T.W + w) * 32 + (i & 31)];
+      }
+    }
+  } else if (vals) {
     CU(cudaMemcpy(vals, h->d_vals[h->cur] + h->own_off, sizeof(double) * h->nnz_own,
                   cudaMemcpyDeviceToHost));
+  }
   if (s) CU(cudaMemcpy(s, h->d_s + h->G, sizeof(double) * h->n, cudaMemcpyDeviceToHost));
   return FASTILU_OK;
 }
@@ -751,6 +881,25 @@ extern "C" fastilu_status fastilu_get_timings(fastilu_handle h, double *t3) {
   return FASTILU_OK;
 }
 
+extern "C" fastilu_status fastilu_get_info(fastilu_handle h, char *buf, int cap) {
+  if (!h || !buf || cap < 1) return FASTILU_ERR_INVALID_ARG;
+  char tmp[512];
+  if (h->tsell)
+    snprintf(tmp, sizeof(tmp),
+             "path=tsell W=%d c0=%d WA=%d terms=%zu threads=%d grid=%d regs=%d local=%d "
+             "tiles=%lld G=%lld H=%lld",
+             h->T.W, h->T.c0, h->T.WA, h->T.terms.size(), h->t_threads, h->t_grid, h->t_regs,
+             h->t_spill, (long long)h->t_ntiles, (long long)h->G, (long long)h->H);
+  else
+    snprintf(tmp, sizeof(tmp),
+             "path=%s G_lanes=%d E=%d threads=%d grid=%d classes=%lld tri_lanes=%d G=%lld H=%lld",
+             h->scfg.prog ? "csr-classes" : (h->scfg.hash ? "csr-hash" : "csr-bsearch"),
+             h->scfg.G, h->scfg.E, h->scfg.threads, h->scfg.grid, (long long)h->nclasses,
+             h->G_tri, (long long)h->G, (long long)h->H);
+  snprintf(buf, cap, "%s", tmp);
+  return FASTILU_OK;
+}
+
 extern "C" fastilu_status fastilu_destroy(fastilu_handle h) {
   if (!h) return FASTILU_OK;
   cudaSetDevice(h->device);
@@ -760,7 +909,8 @@ extern "C" fastilu_status fastilu_destroy(fastilu_handle h) {
                   h->d_adiag, h->d_aval,  h->d_vals[0],  h->d_vals[1], h->d_ud[0], h->d_ud[1],
                   h->d_ahat,  h->d_s,     h->d_ad,       h->d_y,    h->d_z[0],    h->d_z[1],
                   h->d_w[0],  h->d_w[1],  h->d_bx,       h->d_partials, h->d_r2,  h->d_err,
-                  h->d_rclass, h->d_coff, h->d_caoff, h->d_prog};
+                  h->d_rclass, h->d_coff, h->d_caoff, h->d_prog, h->d_toff, h->d_toffA,
+                  h->d_tasrc, h->d_tw2a, h->d_tmask, h->d_counter};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   if (h->h_err) cudaFreeHost(h->h_err);

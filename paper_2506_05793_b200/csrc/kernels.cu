@@ -658,4 +658,128 @@ cudaError_t launch_jacobi_U(const DevPattern &P, const double *vals, const doubl
                                 G, st);
 }
 
+// ----------------------------------------------------------------------------------------
+// Template-SELL kernels (one lane per row).  The template arrays are staged
+// in shared memory; every value access is a coalesced 32-row slot, no index arrays are read.
+// ----------------------------------------------------------------------------------------
+__device__ __forceinline__ bool tbit(const unsigned long long *m, int w) {
+  return (m[w >> 6] >> (w & 63)) & 1ull;
+}
+
+// a2/a3 on the template layout: ahat on A's sub-template and the initial guess (R4, R5).
+__global__ void __launch_bounds__(256)
+tsell_init_kernel(TDev t, const double *__restrict__ aval, const double *__restrict__ s,
+                  const double *__restrict__ ad, int64_t r0, int64_t r1,
+                  double *__restrict__ ahatT, double *__restrict__ vals,
+                  double *__restrict__ udiag, ErrFlags *err) {
+  __shared__ int32_t soff[128], soffA[128];
+  __shared__ int8_t sw2a[128];
+  for (int q = threadIdx.x; q < t.W; q += blockDim.x) {
+    soff[q] = t.off[q];
+    sw2a[q] = t.w2a[q];
+  }
+  for (int q = threadIdx.x; q < t.WA; q += blockDim.x) soffA[q] = t.offA[q];
+  __syncthreads();
+  const int64_t i = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= r1) return;
+  const int64_t sl = i >> 5, ln = i & 31;
+  unsigned long long m[2] = {0ull, 0ull};
+  for (int q = 0; q < t.words; q++) m[q] = t.mask[(sl * t.words + q) * 32 + ln];
+  const double si = s[i];
+  for (int a = 0; a < t.WA; a++) {
+    const int32_t q = t.asrc[(sl * t.WA + a) * 32 + ln];
+    const double ah = q >= 0 ? __dmul_rn(__dmul_rn(aval[q], si), s[i + soffA[a]]) : 0.0;
+    ahatT[(sl * t.WA + a) * 32 + ln] = ah;
+  }
+  for (int w = 0; w < t.W; w++) {
+    const int a = sw2a[w];
+    double v = 0.0;  // fill entries and slots outside S: +0.0
+    if (a >= 0 && tbit(m, w)) {
+      const double ah = ahatT[(sl * t.WA + a) * 32 + ln];
+      v = (w < t.c0) ? __ddiv_rn(ah, ad[i + soff[w]]) : ah;
+    }
+    vals[(sl * t.W + w) * 32 + ln] = v;
+    if (w == t.c0) {
+      udiag[i] = v;
+      if (bad_pivot(v)) atomicMin(&err->zero_pivot, (unsigned long long)i);
+    }
+  }
+}
+
+cudaError_t launch_tsell_init(const TDev &t, const double *aval, const double *s,
+                              const double *ad, int64_t r0, int64_t r1, double *ahatT,
+                              double *vals, double *udiag, ErrFlags *err, cudaStream_t st) {
+  if (r1 <= r0) return cudaSuccess;
+  tsell_init_kernel<<<(unsigned)((r1 - r0 + 255) / 256), 256, 0, st>>>(t, aval, s, ad, r0, r1,
+                                                                       ahatT, vals, udiag, err);
+  return cudaGetLastError();
+}
+
+// a8/a9 on the template layout: the oracle's row sums in the oracle's order (ascending
+// columns, rounded product then difference), absent slots skipped => bitwise equal.
+template <bool LOWER>
+__global__ void __launch_bounds__(256)
+tsell_jacobi_kernel(TDev t, const double *__restrict__ vals, const double *__restrict__ ud,
+                    const double *__restrict__ rhs, const double *__restrict__ xo,
+                    double *__restrict__ xn, double *__restrict__ xf,
+                    const double *__restrict__ s, int64_t r0, int64_t r1, int64_t Gh,
+                    double omega, bool final) {
+  __shared__ int32_t soff[128];
+  for (int q = threadIdx.x; q < t.W; q += blockDim.x) soff[q] = t.off[q];
+  __syncthreads();
+  const int64_t i = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= r1) return;
+  const int64_t sl = i >> 5, ln = i & 31;
+  unsigned long long m[2] = {0ull, 0ull};
+  for (int q = 0; q < t.words; q++) m[q] = t.mask[(sl * t.words + q) * 32 + ln];
+  const double *row = vals + sl * t.W * 32 + ln;
+  double acc = rhs[i];
+  const int w0 = LOWER ? 0 : t.c0 + 1, w1 = LOWER ? t.c0 : t.W;
+  for (int w = w0; w < w1; w++)
+    if (tbit(m, w)) acc = __dsub_rn(acc, __dmul_rn(row[w * 32], xo[i + soff[w]]));
+  if (!LOWER) acc = __ddiv_rn(acc, ud[i]);
+  const double v = (omega == 1.0) ? acc
+                                  : __dadd_rn(__dmul_rn(1.0 - omega, xo[i]), __dmul_rn(omega, acc));
+  if (final) xf[i - Gh] = __dmul_rn(s[i], v); else xn[i] = v;
+}
+
+cudaError_t launch_tsell_jacobi(const TDev &t, bool lower, const double *vals,
+                                const double *udiag, const double *rhs, const double *xo,
+                                double *xn, double *xfinal, const double *s, int64_t r0,
+                                int64_t r1, int64_t Gh, double omega, bool final,
+                                cudaStream_t st) {
+  if (r1 <= r0) return cudaSuccess;
+  const unsigned blocks = (unsigned)((r1 - r0 + 255) / 256);
+  if (lower)
+    tsell_jacobi_kernel<true><<<blocks, 256, 0, st>>>(t, vals, udiag, rhs, xo, xn, xfinal, s, r0,
+                                                       r1, Gh, omega, final);
+  else
+    tsell_jacobi_kernel<false><<<blocks, 256, 0, st>>>(t, vals, udiag, rhs, xo, xn, xfinal, s,
+                                                        r0, r1, Gh, omega, final);
+  return cudaGetLastError();
+}
+
+__global__ void reduce_reset_kernel(const double *__restrict__ partials, int np, double *dst,
+                                    unsigned int *counter) {
+  __shared__ double sh[1024];
+  double t = 0.0;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) t += partials[i];
+  sh[threadIdx.x] = t;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    *dst = sh[0];
+    if (counter) *counter = 0u;
+  }
+}
+
+cudaError_t launch_reduce_reset(const double *partials, int np, double *dst,
+                                unsigned int *counter, cudaStream_t st) {
+  reduce_reset_kernel<<<1, 1024, 0, st>>>(partials, np, dst, counter);
+  return cudaGetLastError();
+}
+
 }  // namespace fastilu

@@ -87,10 +87,22 @@ def test_stencils(kind, g, gz, k, ns, nt):
     ("27pt", 9, 11, 2, 3, 3),
     ("7pt", 17, None, 0, 3, 5),
 ])
-def test_hash_kernel_fallback(kind, g, gz, k, ns, nt, monkeypatch):
-    """The general (hash / binary-search) sweep kernel, forced by FASTILU_NO_CLASSES."""
-    monkeypatch.setenv("FASTILU_NO_CLASSES", "1")
-    full_check(P.make(kind, g, gz), k, ns, nt)
+@pytest.mark.parametrize("path", ["csr-classes", "csr-hash"])
+def test_csr_kernels(kind, g, gz, k, ns, nt, path, monkeypatch):
+    """The general CSR kernels (template path disabled): class-program and hash sweeps."""
+    monkeypatch.setenv("FASTILU_NO_TSELL", "1")
+    if path == "csr-hash":
+        monkeypatch.setenv("FASTILU_NO_CLASSES", "1")
+    f = full_check(P.make(kind, g, gz), k, ns, nt)
+    assert f.info().startswith(f"path={path}"), f.info()
+
+
+@pytest.mark.parametrize("kind,g,k", [("27pt", 12, 1), ("27pt", 10, 2), ("7pt", 20, 0),
+                                       ("aniso7pt", 16, 1)])
+def test_template_path_active(kind, g, k):
+    """Stencil patterns take the template-SELL path with the JIT-specialised sweep."""
+    f = full_check(P.make(kind, g), k, 3, 3)
+    assert f.info().startswith("path=tsell"), f.info()
 
 
 def test_3dof_pattern():
