@@ -118,6 +118,13 @@ fastilu_status fastilu_set_values_device(fastilu_handle h, const double *values_
  * Returns ZERO_DIAG / ZERO_PIVOT with the row in fastilu_error_index. */
 fastilu_status fastilu_compute(fastilu_handle h, int nsweeps);
 
+/* "Sweeps to convergence" (BASELINE config 3; reading G15): like fastilu_compute but
+ * stops after the first sweep s whose by-product residual of iterate s-1 satisfies
+ * r(s-1) = ||(Ahat - L U)|_S||_F <= rtol ||Ahat|_S||_F, or after max_sweeps.  The factors are
+ * iterate s; *sweeps_done = s.  One host synchronisation per sweep.  rtol > 0. */
+fastilu_status fastilu_compute_tol(fastilu_handle h, double rtol, int max_sweeps,
+                                   int *sweeps_done);
+
 /* x = s o U^-1 L^-1 (s o b) with ntrisweeps >= 1 Jacobi sweeps for each factor.
  * b, x: caller-owned DEVICE arrays of length n on the handle's device (x may alias b).
  * Enqueued on the handle's stream; does not synchronise. */

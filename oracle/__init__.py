@@ -199,6 +199,22 @@ def compute(a, k: int, nsweeps: int, omega: float = 1.0, pat: Pattern | None = N
     return Factors(pat, s, ahat, vals, hist[:nsweeps].copy())
 
 
+def compute_tol(a, k: int, rtol: float, max_sweeps: int = 100, omega: float = 1.0):
+    """Sweeps to convergence (reading G15): sweep s yields r(s-1); stop after the first
+    s with r(s-1) <= rtol * ||Ahat|_S||_F, or after max_sweeps.  Returns (Factors, s)."""
+    pat = symbolic(a.row_ptr, a.col_idx, k)
+    s, ahat, vals = scale_init(a, pat)
+    thr = rtol * float(np.sqrt(np.sum(ahat * ahat)))
+    hist = []
+    sw = 0
+    for sw in range(1, max_sweeps + 1):
+        vals, r = sweep(pat, ahat, vals, omega)
+        hist.append(r)
+        if r <= thr:
+            break
+    return Factors(pat, s, ahat, vals, np.array(hist)), sw
+
+
 def exact_ilu(pat: Pattern, ahat):
     ahat = _f64(ahat)
     vals = np.empty_like(ahat)

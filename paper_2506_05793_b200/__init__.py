@@ -56,6 +56,7 @@ _SIGS = {
     "fastilu_set_values": (C.c_int, [H, F64P]),
     "fastilu_set_values_device": (C.c_int, [H, C.c_void_p]),
     "fastilu_compute": (C.c_int, [H, C.c_int]),
+    "fastilu_compute_tol": (C.c_int, [H, C.c_double, C.c_int, C.POINTER(C.c_int)]),
     "fastilu_apply": (C.c_int, [H, C.c_void_p, C.c_void_p, C.c_int]),
     "fastilu_apply_host": (C.c_int, [H, F64P, F64P, C.c_int]),
     "fastilu_destroy": (C.c_int, [H]),
@@ -246,6 +247,13 @@ class FastILU:
 
     def compute(self, nsweeps: int):
         _check(lib().fastilu_compute(self._h, int(nsweeps)), "fastilu_compute", self._h)
+
+    def compute_tol(self, rtol: float, max_sweeps: int = 100) -> int:
+        """Sweeps until r(s-1) <= rtol ||Ahat|_S||_F (or max_sweeps); returns s."""
+        d = C.c_int(0)
+        _check(lib().fastilu_compute_tol(self._h, float(rtol), int(max_sweeps), C.byref(d)),
+               "fastilu_compute_tol", self._h)
+        return d.value
 
     def apply(self, b, x, ntrisweeps: int):
         """b, x: float64 CUDA tensors (or raw device pointers) of length n; x may alias b."""

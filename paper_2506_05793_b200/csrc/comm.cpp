@@ -13,11 +13,20 @@
 #include <nccl.h>
 
 #include <condition_variable>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
 
 #include "comm.h"
+
+#define FAIL(code)                                                                  \
+  do {                                                                              \
+    if (std::getenv("FASTILU_DEBUG"))                                               \
+      fprintf(stderr, "fastilu: %s at %s:%d\n", #code, __FILE__, __LINE__);         \
+    return code;                                                                    \
+  } while (0)
 
 struct fastilu_group_s {
   int nranks = 0;
@@ -45,7 +54,7 @@ struct fastilu_group_s {
 };
 
 extern "C" fastilu_status fastilu_group_create(fastilu_group *out, int nranks) {
-  if (!out || nranks < 1) return FASTILU_ERR_INVALID_ARG;
+  if (!out || nranks < 1) FAIL(FASTILU_ERR_INVALID_ARG);
   fastilu_group g = new (std::nothrow) fastilu_group_s();
   if (!g) return FASTILU_ERR_OOM;
   g->nranks = nranks;
@@ -126,7 +135,7 @@ struct Comm {
   } while (0)
 #define NCC(x)                                                    \
   do {                                                            \
-    if ((x) != ncclSuccess) return FASTILU_ERR_NCCL;              \
+    if ((x) != ncclSuccess) FAIL(FASTILU_ERR_NCCL);              \
   } while (0)
 
 static fastilu_status scratch(Comm *c, size_t elems) {
@@ -177,17 +186,17 @@ fastilu_status comm_setup(Comm *&out, const fastilu_options &o, int64_t row_begi
   c->n = n;
   CUC(cudaGetDevice(&c->dev));
   if (c->kind == FASTILU_COMM_LOCAL) {
-    if (!o.group || o.group->nranks != o.nranks) return FASTILU_ERR_INVALID_ARG;
+    if (!o.group || o.group->nranks != o.nranks) FAIL(FASTILU_ERR_INVALID_ARG);
     c->grp = o.group;
     c->grp->dev[c->rank] = c->dev;
   } else if (c->kind == FASTILU_COMM_NCCL) {
-    if (!o.nccl_unique_id) return FASTILU_ERR_INVALID_ARG;
-    if (!nccl().ok) return FASTILU_ERR_NCCL;
+    if (!o.nccl_unique_id) FAIL(FASTILU_ERR_INVALID_ARG);
+    if (!nccl().ok) FAIL(FASTILU_ERR_NCCL);
     ncclUniqueId id;
     std::memcpy(&id, o.nccl_unique_id, sizeof(id));
     NCC(nccl().CommInitRank(&c->nc, o.nranks, id, o.rank));
   } else {
-    return FASTILU_ERR_INVALID_ARG;
+    FAIL(FASTILU_ERR_INVALID_ARG);
   }
   CUC(cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming));
   CUC(cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming));
@@ -207,12 +216,12 @@ fastilu_status comm_setup(Comm *&out, const fastilu_options &o, int64_t row_begi
     c->HH[r] = all[4 * r + 3];
   }
   for (int r = 0; r < P; r++) {
-    if (r > 0 && c->rb[r] != c->rb[r - 1] + c->nn[r - 1]) return FASTILU_ERR_INVALID_ARG;
-    if (r == 0 && c->GG[r] != 0) return FASTILU_ERR_INVALID_ARG;
-    if (r == P - 1 && c->HH[r] != 0) return FASTILU_ERR_INVALID_ARG;
+    if (r > 0 && c->rb[r] != c->rb[r - 1] + c->nn[r - 1]) FAIL(FASTILU_ERR_INVALID_ARG);
+    if (r == 0 && c->GG[r] != 0) FAIL(FASTILU_ERR_INVALID_ARG);
+    if (r == P - 1 && c->HH[r] != 0) FAIL(FASTILU_ERR_INVALID_ARG);
     // ghosts must come from the immediate neighbours only
-    if (r > 0 && c->GG[r] > c->nn[r - 1]) return FASTILU_ERR_UNSUPPORTED;
-    if (r < P - 1 && c->HH[r] > c->nn[r + 1]) return FASTILU_ERR_UNSUPPORTED;
+    if (r > 0 && c->GG[r] > c->nn[r - 1]) FAIL(FASTILU_ERR_UNSUPPORTED);
+    if (r < P - 1 && c->HH[r] > c->nn[r + 1]) FAIL(FASTILU_ERR_UNSUPPORTED);
   }
   // factor halo: I send my last G_{p+1} owned rows (local rows [G + n - G_{p+1}, G + n))
   const int64_t gn = (p + 1 < P) ? c->GG[p + 1] : 0;
@@ -228,9 +237,9 @@ fastilu_status comm_setup(Comm *&out, const fastilu_options &o, int64_t row_begi
   s = allgather_i64(c, {c->send_cnt, c->recv_cnt, stat, (int64_t)layout_hash}, all, st);
   if (s) return s;
   for (int r = 0; r + 1 < P; r++)
-    if (all[4 * r] != all[4 * (r + 1) + 1]) return FASTILU_ERR_BAD_MATRIX;  // patterns disagree
+    if (all[4 * r] != all[4 * (r + 1) + 1]) FAIL(FASTILU_ERR_BAD_MATRIX);  // patterns disagree
   for (int r = 0; r < P; r++)
-    if (all[4 * r + 3] != all[3]) return FASTILU_ERR_UNSUPPORTED;  // layouts differ
+    if (all[4 * r + 3] != all[3]) FAIL(FASTILU_ERR_UNSUPPORTED);  // layouts differ
   *stat_global = 0;
   for (int r = 0; r < P; r++) *stat_global += all[4 * r + 2];
   return FASTILU_OK;
@@ -279,7 +288,7 @@ static fastilu_status exchange(Comm *c, const std::vector<Xfer> &sends,
         src = (const double *)(intptr_t)q[i + 1];
         cnt = q[i + 2];
       }
-    if (cnt != x.cnt) return FASTILU_ERR_STATE;
+    if (cnt != x.cnt) FAIL(FASTILU_ERR_STATE);
     if (cnt > 0) {
       CUC(cudaStreamWaitEvent(st, g->ev[x.peer], 0));
       if (g->dev[x.peer] == c->dev)
@@ -396,10 +405,10 @@ void comm_destroy(Comm *c) {
 }  // namespace fastilu
 
 extern "C" fastilu_status fastilu_nccl_unique_id(void *id128) {
-  if (!id128) return FASTILU_ERR_INVALID_ARG;
-  if (!fastilu::nccl().ok) return FASTILU_ERR_NCCL;
+  if (!id128) FAIL(FASTILU_ERR_INVALID_ARG);
+  if (!fastilu::nccl().ok) FAIL(FASTILU_ERR_NCCL);
   ncclUniqueId id;
-  if (fastilu::nccl().GetUniqueId(&id) != ncclSuccess) return FASTILU_ERR_NCCL;
+  if (fastilu::nccl().GetUniqueId(&id) != ncclSuccess) FAIL(FASTILU_ERR_NCCL);
   std::memcpy(id128, &id, sizeof(id));
   return FASTILU_OK;
 }

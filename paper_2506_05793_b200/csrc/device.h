@@ -116,6 +116,11 @@ cudaError_t launch_tsell_jacobi(const TDev &t, bool lower, const double *vals,
 cudaError_t launch_reduce_reset(const double *partials, int np, double *dst,
                                 unsigned int *counter, cudaStream_t st);
 
+// *dst = sum of x[i]^2 (deterministic; partials needs kSumsqBlocks entries)
+constexpr int kSumsqBlocks = 256;
+cudaError_t launch_sumsq(const double *x, int64_t n, double *partials, double *dst,
+                         cudaStream_t st);
+
 int sm_count(int device);
 
 }  // namespace fastilu

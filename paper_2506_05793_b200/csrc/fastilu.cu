@@ -20,6 +20,13 @@
 #include "jit.h"
 #include "tsell.h"
 
+#define FAIL(code)                                                                  \
+  do {                                                                              \
+    if (std::getenv("FASTILU_DEBUG"))                                               \
+      fprintf(stderr, "fastilu: %s at %s:%d\n", #code, __FILE__, __LINE__);         \
+    return code;                                                                    \
+  } while (0)
+
 using namespace fastilu;
 
 struct fastilu_handle_s {
@@ -141,7 +148,7 @@ extern "C" fastilu_status fastilu_symbolic(int64_t n, const int64_t *row_ptr,
                                            int64_t *bad_row) {
   if (bad_row) *bad_row = -1;
   if (n < 0 || !row_ptr || (n > 0 && !col_idx) || level_k < 0 || level_k > 127)
-    return FASTILU_ERR_INVALID_ARG;
+    FAIL(FASTILU_ERR_INVALID_ARG);
   int64_t bad = -1;
   int nt = hw_threads(num_threads);
   int st = validate_csr(n, row_ptr, col_idx, 0, n, nt, &bad);
@@ -175,7 +182,7 @@ extern "C" fastilu_status fastilu_symbolic_window(int64_t nrows, const int64_t *
   if (nrows < 0 || !row_ptr || (nrows > 0 && !col_idx) || level_k < 0 || level_k > 127 ||
       row0 < 0 || out_begin < row0 || out_end < out_begin || out_end > row0 + nrows ||
       ncols < row0 + nrows)
-    return FASTILU_ERR_INVALID_ARG;
+    FAIL(FASTILU_ERR_INVALID_ARG);
   int64_t bad = -1;
   int nt = hw_threads(num_threads);
   int st = validate_csr(nrows, row_ptr, col_idx, row0, ncols, nt, &bad);
@@ -289,7 +296,7 @@ static fastilu_status setup_configs(fastilu_handle h, const std::vector<int64_t>
   };
   while (c.threads > 32 && (size_t)(c.threads / G) * gbytes(c) > 200 * 1024) c.threads /= 2;
   if (c.threads < G || (size_t)(c.threads / G) * gbytes(c) > 220 * 1024)
-    return FASTILU_ERR_UNSUPPORTED;  // a row of S too long for the shared-memory accumulator
+    FAIL(FASTILU_ERR_UNSUPPORTED);  // a row of S too long for the shared-memory accumulator
   c.smem = (size_t)(c.threads / G) * gbytes(c);
   int bps = 0;
   if (sweep_configure(c, &bps) != cudaSuccess || bps < 1) return FASTILU_ERR_CUDA;
@@ -333,14 +340,14 @@ static fastilu_status setup_tsell(fastilu_handle h, const std::vector<unsigned l
   const std::string src = sweep_source(T, threads, chunk);
   if (jit_get(src, "fastilu_tsell_sweep", h->device, &h->jit_sweep, &log)) {
     if (std::getenv("FASTILU_DEBUG")) fprintf(stderr, "fastilu: JIT failed: %s\n", log.c_str());
-    return FASTILU_ERR_UNSUPPORTED;
+    FAIL(FASTILU_ERR_UNSUPPORTED);
   }
   int bps = 0;
   jit_func_info(h->jit_sweep, &h->t_regs, &h->t_spill, threads, &bps);
   if (std::getenv("FASTILU_DEBUG"))
     fprintf(stderr, "fastilu: tsell W=%d c0=%d WA=%d terms=%zu regs=%d local=%d bps=%d\n", T.W,
             T.c0, T.WA, T.terms.size(), h->t_regs, h->t_spill, bps);
-  if (bps < 1) return FASTILU_ERR_UNSUPPORTED;
+  if (bps < 1) FAIL(FASTILU_ERR_UNSUPPORTED);
   h->t_threads = threads;
   h->t_ntiles = std::max<int64_t>(1, (h->n + threads - 1) / threads);
   h->t_grid = (int)std::min<int64_t>((int64_t)sm_count(h->device) * bps, h->t_ntiles);
@@ -357,7 +364,7 @@ static fastilu_status setup_tsell(fastilu_handle h, const std::vector<unsigned l
   CU(dalloc(&h->d_toffA, T.WA));
   CU(dalloc(&h->d_tw2a, T.W));
   CU(dalloc(&h->d_counter, 1));
-  CU(dalloc(&h->d_partials, h->t_ntiles));
+  CU(dalloc(&h->d_partials, std::max<int64_t>(h->t_ntiles, kSumsqBlocks)));
   CU(cudaMemset(h->d_counter, 0, sizeof(unsigned int)));
   CU(cudaMemcpy(h->d_tmask, mask.data(), 8 * mask.size(), cudaMemcpyHostToDevice));
   CU(cudaMemcpy(h->d_tasrc, asrc.data(), 4 * asrc.size(), cudaMemcpyHostToDevice));
@@ -386,7 +393,7 @@ static fastilu_status create_impl(fastilu_handle h, int64_t n, const int64_t *ro
   if (multi) {
     if (o.global_n <= 0 || o.row_begin < 0 || o.row_begin + n > o.global_n || o.n_lead < 0 ||
         o.n_lead > o.row_begin || o.rank < 0 || o.rank >= o.nranks)
-      return FASTILU_ERR_INVALID_ARG;
+      FAIL(FASTILU_ERR_INVALID_ARG);
   }
   const int nt = hw_threads(o.num_threads);
   const int64_t g0 = h->row_begin - h->n_lead;
@@ -419,14 +426,14 @@ static fastilu_status create_impl(fastilu_handle h, int64_t n, const int64_t *ro
   }
   h->G = h->row_begin - mincol;
   h->H = maxcol - (row_end - 1);
-  if (!multi && (h->G != 0 || h->H != 0)) return FASTILU_ERR_BAD_MATRIX;
+  if (!multi && (h->G != 0 || h->H != 0)) FAIL(FASTILU_ERR_BAD_MATRIX);
   // multi-GPU: whole 32-row slices of ghost rows (template-SELL layout), if the margin allows
   if (multi && h->G % 32 && (h->G + 31) / 32 * 32 <= own_r0) h->G = (h->G + 31) / 32 * 32;
-  if (h->G > own_r0) return FASTILU_ERR_UNSUPPORTED;  // ghost rows beyond the supplied margin
+  if (h->G > own_r0) FAIL(FASTILU_ERR_UNSUPPORTED);  // ghost rows beyond the supplied margin
   h->lbase = h->row_begin - h->G;
   h->nloc = h->G + n;
   h->E = h->nloc + h->H;
-  if (h->E >= (int64_t)INT32_MAX) return FASTILU_ERR_UNSUPPORTED;
+  if (h->E >= (int64_t)INT32_MAX) FAIL(FASTILU_ERR_UNSUPPORTED);
   const int64_t lr0 = own_r0 - h->G;  // pattern row of local row 0
   const int64_t s_base = pat.rp[lr0];
   h->nnz_loc = pat.rp[own_r0 + n] - s_base;
@@ -503,7 +510,7 @@ static fastilu_status create_impl(fastilu_handle h, int64_t n, const int64_t *ro
       });
     for (auto &x : th) x.join();
     for (int t = 0; t < T; t++)
-      if (fail[t]) return FASTILU_ERR_BAD_MATRIX;  // S must contain A (cannot happen)
+      if (fail[t]) FAIL(FASTILU_ERR_BAD_MATRIX);  // S must contain A (cannot happen)
   }
   int64_t nl_own = 0;
   for (int64_t r = h->G; r < h->nloc; r++) nl_own += dloc[r];
@@ -549,8 +556,9 @@ static fastilu_status create_impl(fastilu_handle h, int64_t n, const int64_t *ro
     CU(dalloc(&h->d_dloc, h->nloc));
     CU(dalloc(&h->d_aci, h->nnzA_loc));
     CU(dalloc(&h->d_apos, h->nnzA_loc));
-    CU(dalloc(&h->d_ahat, h->nnzA_loc));  // ahat on A's pattern
-    CU(dalloc(&h->d_partials, h->scfg.grid));
+    CU(dalloc(&h->d_ahat, h->nnzA_loc));  // ahat on A's pattern (ghost rows' stay 0)
+    CU(cudaMemset(h->d_ahat, 0, sizeof(double) * h->nnzA_loc));
+    CU(dalloc(&h->d_partials, std::max<int64_t>(h->scfg.grid, kSumsqBlocks)));
     for (int b = 0; b < 2; b++) CU(dalloc(&h->d_vals[b], h->nnz_loc));
   }
   CU(dalloc(&h->d_arp, h->nloc + 1));
@@ -604,7 +612,7 @@ static fastilu_status create_impl(fastilu_handle h, int64_t n, const int64_t *ro
 extern "C" fastilu_status fastilu_create(fastilu_handle *out, int64_t n, const int64_t *row_ptr,
                                          const int32_t *col_idx, const double *values,
                                          int level_k, const fastilu_options *opts) {
-  if (!out) return FASTILU_ERR_INVALID_ARG;
+  if (!out) FAIL(FASTILU_ERR_INVALID_ARG);
   *out = nullptr;
   fastilu_handle h = new (std::nothrow) fastilu_handle_s();
   if (!h) return FASTILU_ERR_OOM;
@@ -613,7 +621,7 @@ extern "C" fastilu_status fastilu_create(fastilu_handle *out, int64_t n, const i
   if (n < 0 || !row_ptr || (n > 0 && !col_idx) || level_k < 0 || level_k > 127 ||
       h->opt.nranks < 1 || !(h->opt.omega > 0.0 && h->opt.omega <= 1.0) ||
       !(h->opt.omega_tri > 0.0 && h->opt.omega_tri <= 1.0))
-    return FASTILU_ERR_INVALID_ARG;
+    FAIL(FASTILU_ERR_INVALID_ARG);
   if (h->opt.device >= 0) {
     if (cudaSetDevice(h->opt.device) != cudaSuccess) return FASTILU_ERR_CUDA;
     h->device = h->opt.device;
@@ -631,21 +639,23 @@ extern "C" fastilu_status fastilu_create(fastilu_handle *out, int64_t n, const i
 }
 
 extern "C" fastilu_status fastilu_set_values(fastilu_handle h, const double *values) {
-  if (!h || !values || !h->d_aval) return FASTILU_ERR_INVALID_ARG;
+  if (!h || !values || !h->d_aval) FAIL(FASTILU_ERR_INVALID_ARG);
   cudaSetDevice(h->device);
   return upload_values(h, values, false);
 }
 
 extern "C" fastilu_status fastilu_set_values_device(fastilu_handle h, const double *values) {
-  if (!h || !values || !h->d_aval) return FASTILU_ERR_INVALID_ARG;
+  if (!h || !values || !h->d_aval) FAIL(FASTILU_ERR_INVALID_ARG);
   cudaSetDevice(h->device);
   return upload_values(h, values, true);
 }
 
 // --------------------------------------------------------------------------- compute
-extern "C" fastilu_status fastilu_compute(fastilu_handle h, int nsweeps) {
-  if (!h || nsweeps < 0) return FASTILU_ERR_INVALID_ARG;
-  if (!h->have_values || !h->d_aval) return FASTILU_ERR_STATE;
+// nsweeps synchronous sweeps; with rtol > 0, stop after the first sweep s whose residual of
+// iterate s-1 satisfies r(s-1) <= rtol ||Ahat|_S||_F (reading G15), at most nsweeps.
+static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, int *done) {
+  if (!h || nsweeps < 0) FAIL(FASTILU_ERR_INVALID_ARG);
+  if (!h->have_values || !h->d_aval) FAIL(FASTILU_ERR_STATE);
   cudaSetDevice(h->device);
   h->computed = false;
   h->err_index = -1;
@@ -677,8 +687,42 @@ extern "C" fastilu_status fastilu_compute(fastilu_handle h, int nsweeps) {
     CU(launch_init(P, h->d_arp, h->d_aci, h->d_apos, h->d_aval, h->d_s, h->d_ad, r0, r1,
                    h->d_ahat, h->d_vals[0], h->d_ud[0], h->d_err, h->G_init, st));
   CU(cudaEventRecord(h->ev[1], st));
+  double thr2 = -1.0;  // (rtol ||Ahat|_S||_F)^2, tolerance mode only
+  std::vector<double> r2tol;
+  if (rtol > 0.0) {
+    const int64_t na = h->tsell ? h->nsl * h->T.WA * 32 : h->nnzA_loc;
+    CU(launch_sumsq(h->d_ahat, na, h->d_partials, h->d_r2, st));
+    double a2 = 0.0;
+    CU(cudaMemcpyAsync(h->h_r2, h->d_r2, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    a2 = h->h_r2[0];
+    if (h->comm) {
+      ErrFlags dummy{~0ull, ~0ull};
+      fastilu_status cs = comm_allreduce_host(h->comm, &a2, 1, dummy);
+      if (cs) return cs;
+    }
+    thr2 = rtol * rtol * a2;
+  }
+  int executed = 0;
   // a4/a5: nsweeps synchronous sweeps, ping-pong buffers
   for (int sw = 1; sw <= nsweeps; sw++) {
+    executed = sw;
+    if (thr2 >= 0.0 && sw > 1) {  // r(sw-2) of the previous sweep decides whether to go on
+      CU(cudaMemcpyAsync(h->h_r2 + (sw - 2), h->d_r2 + (sw - 2), sizeof(double),
+                         cudaMemcpyDeviceToHost, st));
+      CU(cudaStreamSynchronize(st));
+      double v = h->h_r2[sw - 2];
+      if (h->comm) {
+        ErrFlags dummy{~0ull, ~0ull};
+        fastilu_status cs = comm_allreduce_host(h->comm, &v, 1, dummy);
+        if (cs) return cs;
+      }
+      r2tol.push_back(v);
+      if (v <= thr2) {
+        executed = sw - 1;
+        break;
+      }
+    }
     const int ib = (sw - 1) & 1, ob = sw & 1;
     if (h->comm) {
       fastilu_status cs = comm_factor_halo(h->comm, h->d_vals[ib], h->d_rp, h->d_ud[ib], st);
@@ -709,6 +753,8 @@ extern "C" fastilu_status fastilu_compute(fastilu_handle h, int nsweeps) {
     }
     CU(launch_reduce(h->d_partials, h->scfg.grid, h->d_r2 + (sw - 1), st));
   }
+  nsweeps = executed;
+  if (done) *done = executed;
   CU(cudaEventRecord(h->ev[2], st));
   CU(cudaMemcpyAsync(h->h_err, h->d_err, sizeof(ErrFlags), cudaMemcpyDeviceToHost, st));
   if (nsweeps)
@@ -725,6 +771,7 @@ extern "C" fastilu_status fastilu_compute(fastilu_handle h, int nsweeps) {
     fastilu_status cs = comm_allreduce_host(h->comm, r2.data(), (int)r2.size(), ef);
     if (cs) return cs;
   }
+  for (size_t q = 0; q < r2tol.size() && q < r2.size(); q++) r2[q] = r2tol[q];
   for (int i = 0; i < nsweeps; i++) h->resid[i] = std::sqrt(r2[i]);
   h->cur = nsweeps & 1;
   if (ef.zero_diag != ~0ull) {
@@ -737,6 +784,16 @@ extern "C" fastilu_status fastilu_compute(fastilu_handle h, int nsweeps) {
   }
   h->computed = true;
   return FASTILU_OK;
+}
+
+extern "C" fastilu_status fastilu_compute(fastilu_handle h, int nsweeps) {
+  return compute_impl(h, nsweeps, 0.0, nullptr);
+}
+
+extern "C" fastilu_status fastilu_compute_tol(fastilu_handle h, double rtol, int max_sweeps,
+                                              int *sweeps_done) {
+  if (!(rtol > 0.0) || max_sweeps < 1) FAIL(FASTILU_ERR_INVALID_ARG);
+  return compute_impl(h, max_sweeps, rtol, sweeps_done);
 }
 
 // --------------------------------------------------------------------------- apply
@@ -781,8 +838,8 @@ static fastilu_status apply_impl(fastilu_handle h, const double *b, double *x, i
 
 extern "C" fastilu_status fastilu_apply(fastilu_handle h, const double *b, double *x,
                                         int ntrisweeps) {
-  if (!h || ntrisweeps < 1 || (h->n > 0 && (!b || !x))) return FASTILU_ERR_INVALID_ARG;
-  if (!h->computed) return FASTILU_ERR_STATE;
+  if (!h || ntrisweeps < 1 || (h->n > 0 && (!b || !x))) FAIL(FASTILU_ERR_INVALID_ARG);
+  if (!h->computed) FAIL(FASTILU_ERR_STATE);
   cudaSetDevice(h->device);
   CU(cudaEventRecord(h->ev[3], h->stream));
   fastilu_status s = apply_impl(h, b, x, ntrisweeps);
@@ -793,8 +850,8 @@ extern "C" fastilu_status fastilu_apply(fastilu_handle h, const double *b, doubl
 
 extern "C" fastilu_status fastilu_apply_host(fastilu_handle h, const double *b, double *x,
                                              int ntrisweeps) {
-  if (!h || ntrisweeps < 1 || (h->n > 0 && (!b || !x))) return FASTILU_ERR_INVALID_ARG;
-  if (!h->computed) return FASTILU_ERR_STATE;
+  if (!h || ntrisweeps < 1 || (h->n > 0 && (!b || !x))) FAIL(FASTILU_ERR_INVALID_ARG);
+  if (!h->computed) FAIL(FASTILU_ERR_STATE);
   cudaSetDevice(h->device);
   if (!h->d_bx) CU(dalloc(&h->d_bx, 2 * h->n));
   CU(cudaMemcpyAsync(h->d_bx, b, sizeof(double) * h->n, cudaMemcpyHostToDevice, h->stream));
@@ -811,7 +868,7 @@ extern "C" fastilu_status fastilu_apply_host(fastilu_handle h, const double *b, 
 // --------------------------------------------------------------------------- introspection
 extern "C" fastilu_status fastilu_get_sizes(fastilu_handle h, int64_t *n, int64_t *nnz_S,
                                             int64_t *nnz_A) {
-  if (!h) return FASTILU_ERR_INVALID_ARG;
+  if (!h) FAIL(FASTILU_ERR_INVALID_ARG);
   if (n) *n = h->n;
   if (nnz_S) *nnz_S = (int64_t)h->h_ci.size();
   if (nnz_A) {
@@ -828,7 +885,7 @@ extern "C" fastilu_status fastilu_get_sizes(fastilu_handle h, int64_t *n, int64_
 
 extern "C" fastilu_status fastilu_get_pattern(fastilu_handle h, int64_t *row_ptr,
                                               int32_t *col_idx, int8_t *level) {
-  if (!h) return FASTILU_ERR_INVALID_ARG;
+  if (!h) FAIL(FASTILU_ERR_INVALID_ARG);
   if (row_ptr) std::memcpy(row_ptr, h->h_rp.data(), sizeof(int64_t) * h->h_rp.size());
   if (col_idx) std::memcpy(col_idx, h->h_ci.data(), sizeof(int32_t) * h->h_ci.size());
   if (level) std::memcpy(level, h->h_lev.data(), h->h_lev.size());
@@ -836,8 +893,8 @@ extern "C" fastilu_status fastilu_get_pattern(fastilu_handle h, int64_t *row_ptr
 }
 
 extern "C" fastilu_status fastilu_get_factors(fastilu_handle h, double *vals, double *s) {
-  if (!h) return FASTILU_ERR_INVALID_ARG;
-  if (!h->computed) return FASTILU_ERR_STATE;
+  if (!h) FAIL(FASTILU_ERR_INVALID_ARG);
+  if (!h->computed) FAIL(FASTILU_ERR_STATE);
   cudaSetDevice(h->device);
   CU(cudaStreamSynchronize(h->stream));
   if (vals && h->tsell) {  // gather the owned rows' S entries out of the template slots
@@ -863,7 +920,7 @@ extern "C" fastilu_status fastilu_get_factors(fastilu_handle h, double *vals, do
 
 extern "C" fastilu_status fastilu_get_residual_history(fastilu_handle h, double *hist, int cap,
                                                        int *count) {
-  if (!h) return FASTILU_ERR_INVALID_ARG;
+  if (!h) FAIL(FASTILU_ERR_INVALID_ARG);
   int c = std::min<int>(cap, (int)h->resid.size());
   for (int i = 0; i < c; i++) hist[i] = h->resid[i];
   if (count) *count = c;
@@ -871,7 +928,7 @@ extern "C" fastilu_status fastilu_get_residual_history(fastilu_handle h, double 
 }
 
 extern "C" fastilu_status fastilu_get_timings(fastilu_handle h, double *t3) {
-  if (!h || !t3) return FASTILU_ERR_INVALID_ARG;
+  if (!h || !t3) FAIL(FASTILU_ERR_INVALID_ARG);
   cudaSetDevice(h->device);
   float ta = 0.f;
   if (cudaEventQuery(h->ev[4]) == cudaSuccess) cudaEventElapsedTime(&ta, h->ev[3], h->ev[4]);
@@ -882,7 +939,7 @@ extern "C" fastilu_status fastilu_get_timings(fastilu_handle h, double *t3) {
 }
 
 extern "C" fastilu_status fastilu_get_info(fastilu_handle h, char *buf, int cap) {
-  if (!h || !buf || cap < 1) return FASTILU_ERR_INVALID_ARG;
+  if (!h || !buf || cap < 1) FAIL(FASTILU_ERR_INVALID_ARG);
   char tmp[512];
   if (h->tsell)
     snprintf(tmp, sizeof(tmp),

@@ -782,4 +782,27 @@ cudaError_t launch_reduce_reset(const double *partials, int np, double *dst,
   return cudaGetLastError();
 }
 
+__global__ void sumsq_kernel(const double *__restrict__ x, int64_t n, double *partials) {
+  double t = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    t = fma(x[i], x[i], t);
+  __shared__ double wsum[32];
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = t;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double u = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); w++) u += wsum[w];
+    partials[blockIdx.x] = u;
+  }
+}
+
+cudaError_t launch_sumsq(const double *x, int64_t n, double *partials, double *dst,
+                         cudaStream_t st) {
+  sumsq_kernel<<<kSumsqBlocks, 256, 0, st>>>(x, n, partials);
+  reduce_kernel<<<1, 1024, 0, st>>>(partials, kSumsqBlocks, dst);
+  return cudaGetLastError();
+}
+
 }  // namespace fastilu

@@ -136,6 +136,21 @@ def test_sweeps_reach_exact_ilu_on_gpu():
     assert np.array_equal(vals, oracle.exact_ilu(pat, ahat))
 
 
+@pytest.mark.parametrize("kind,g,k", [("27pt", 10, 1), ("27pt", 8, 2), ("7pt", 12, 0)])
+def test_sweeps_to_convergence(kind, g, k):
+    """BASELINE config 3 semantics ("sweeps to convergence", reading G15) at small size: the GPU
+    stops at the same sweep s* as the oracle and its factors are bitwise equal."""
+    a = P.make(kind, g)
+    f = F.FastILU(a.row_ptr, a.col_idx, a.values, k)
+    s_gpu = f.compute_tol(1e-10, 100)
+    fo, s_or = oracle.compute_tol(a, k, 1e-10, 100)
+    assert s_gpu == s_or and 5 < s_gpu < 100
+    vals, _ = f.factors()
+    assert np.array_equal(vals, fo.vals)
+    rtol_r = max(1e-12, (fo.pattern.nnz + 64) * np.finfo(float).eps)
+    np.testing.assert_allclose(f.residual_history(), fo.resid, rtol=rtol_r)
+
+
 def test_alias_and_host_apply():
     a = P.laplace3d_27pt(8)
     b = P.rhs_positive(a.n)
