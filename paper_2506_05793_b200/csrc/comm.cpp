@@ -170,10 +170,7 @@ static fastilu_status allgather_i64(Comm *c, const std::vector<int64_t> &mine,
   return FASTILU_OK;
 }
 
-fastilu_status comm_setup(Comm *&out, const fastilu_options &o, int64_t row_begin, int64_t n,
-                          int64_t G, int64_t H, const int64_t *h_rp, int64_t stat,
-                          int64_t *stat_global, int tsell_W, uint64_t layout_hash,
-                          cudaStream_t st) {
+fastilu_status comm_init(Comm *&out, const fastilu_options &o, cudaStream_t st) {
   out = nullptr;
   Comm *c = new (std::nothrow) Comm();
   if (!c) return FASTILU_ERR_OOM;
@@ -181,9 +178,6 @@ fastilu_status comm_setup(Comm *&out, const fastilu_options &o, int64_t row_begi
   c->kind = o.comm_kind;
   c->rank = o.rank;
   c->nranks = o.nranks;
-  c->G = G;
-  c->H = H;
-  c->n = n;
   CUC(cudaGetDevice(&c->dev));
   if (c->kind == FASTILU_COMM_LOCAL) {
     if (!o.group || o.group->nranks != o.nranks) FAIL(FASTILU_ERR_INVALID_ARG);
@@ -200,6 +194,21 @@ fastilu_status comm_setup(Comm *&out, const fastilu_options &o, int64_t row_begi
   }
   CUC(cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming));
   CUC(cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming));
+  (void)st;
+  return FASTILU_OK;
+}
+
+fastilu_status comm_allgather_i64(Comm *c, const std::vector<int64_t> &mine,
+                                  std::vector<int64_t> &all, cudaStream_t st) {
+  return allgather_i64(c, mine, all, st);
+}
+
+fastilu_status comm_layout(Comm *c, int64_t row_begin, int64_t n, int64_t G, int64_t H,
+                           const int64_t *h_rp, int64_t stat, int64_t *stat_global,
+                           int tsell_W, uint64_t layout_hash, cudaStream_t st) {
+  c->G = G;
+  c->H = H;
+  c->n = n;
   // partition exchange: row_begin, n, G, H, nnz of my trailing rows (by request), my ghost nnz
   std::vector<int64_t> all;
   fastilu_status s = allgather_i64(c, {row_begin, n, G, H}, all, st);

@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <vector>
 
 #include "../../include/fastilu.h"
 #include "device.h"
@@ -10,15 +11,19 @@ namespace fastilu {
 
 struct Comm;
 
-// Collective over the ranks of opts: exchanges the partition (row_begin, n, G, H) of every rank
-// and validates that ghost rows come only from the immediate neighbours.
-// Also sums `stat` (e.g. the number of strict-lower entries) over ranks into *stat_global so
-// that launch shapes that affect rounding (the trisolve's lanes per row) are chosen from global
-// statistics and results stay bitwise independent of the partition.
-fastilu_status comm_setup(Comm *&out, const fastilu_options &opts, int64_t row_begin, int64_t n,
-                          int64_t G, int64_t H, const int64_t *h_rp_local, int64_t stat,
-                          int64_t *stat_global, int tsell_W, uint64_t layout_hash,
-                          cudaStream_t st);
+// Collective: binds the rank to its transport (NCCL communicator or in-process group).
+fastilu_status comm_init(Comm *&out, const fastilu_options &opts, cudaStream_t st);
+// Collective all-gather of mine.size() int64 per rank into all[nranks][mine.size()].
+fastilu_status comm_allgather_i64(Comm *c, const std::vector<int64_t> &mine,
+                                  std::vector<int64_t> &all, cudaStream_t st);
+// Collective: exchanges the partition (row_begin, n, G, H) of every rank, validates that ghost
+// rows come only from the immediate neighbours and that the ghost/halo sizes match.  Also sums
+// `stat` (e.g. the number of strict-lower entries) over ranks into *stat_global so that launch
+// shapes that affect rounding are chosen from global statistics (results stay bitwise
+// independent of the partition).  tsell_W > 0: template-SELL layout of width W.
+fastilu_status comm_layout(Comm *c, int64_t row_begin, int64_t n, int64_t G, int64_t H,
+                           const int64_t *h_rp_local, int64_t stat, int64_t *stat_global,
+                           int tsell_W, uint64_t layout_hash, cudaStream_t st);
 // Vector halo on an extended vector [G | n | H]: lower ghosts from rank-1's last G owned
 // entries, upper ghosts from rank+1's first H owned entries.
 fastilu_status comm_vector_halo(Comm *c, double *x, cudaStream_t st, bool lower, bool upper);

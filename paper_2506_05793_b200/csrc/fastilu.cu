@@ -429,6 +429,10 @@ static fastilu_status create_impl(fastilu_handle h, int64_t n, const int64_t *ro
   if (!multi && (h->G != 0 || h->H != 0)) FAIL(FASTILU_ERR_BAD_MATRIX);
   // multi-GPU: whole 32-row slices of ghost rows (template-SELL layout), if the margin allows
   if (multi && h->G % 32 && (h->G + 31) / 32 * 32 <= own_r0) h->G = (h->G + 31) / 32 * 32;
+  if (multi) {
+    fastilu_status cs = comm_init(h->comm, h->opt, h->stream);
+    if (cs) return cs;
+  }
   if (h->G > own_r0) FAIL(FASTILU_ERR_UNSUPPORTED);  // ghost rows beyond the supplied margin
   h->lbase = h->row_begin - h->G;
   h->nloc = h->G + n;
@@ -517,14 +521,24 @@ static fastilu_status create_impl(fastilu_handle h, int64_t n, const int64_t *ro
   const double nl_avg = n ? (double)nl_own / n : 1.0;
   const double u_avg = n ? (double)(h->nnz_own - n - nl_own) / n : 1.0;
   // template-SELL fast path for structured patterns (else the CSR kernels below)
-  if (!std::getenv("FASTILU_NO_TSELL") && (!multi || (n % 32 == 0 && h->G % 32 == 0)) &&
-      jit_available(nullptr)) {
+  {
     std::vector<unsigned long long> tmask;
     std::vector<int32_t> tasrc;
-    if (build_template(rp, ci, h->nloc, arp, aci, nt, h->T, tmask, tasrc)) {
+    bool ok = !std::getenv("FASTILU_NO_TSELL") && (!multi || (n % 32 == 0 && h->G % 32 == 0)) &&
+              jit_available(nullptr) &&
+              build_template(rp, ci, h->nloc, arp, aci, nt, h->T, tmask, tasrc);
+    if (multi) {  // all ranks must agree on the layout (and on the template itself)
+      std::vector<int64_t> all;
+      fastilu_status cs = comm_allgather_i64(h->comm, {ok ? 1 : 0, ok ? (int64_t)h->T.hash : 0},
+                                             all, h->stream);
+      if (cs) return cs;
+      for (int r = 0; r < h->opt.nranks; r++)
+        if (!all[2 * r] || all[2 * r + 1] != all[1]) ok = false;
+    }
+    if (ok) {
       fastilu_status ts = setup_tsell(h, tmask, tasrc);
       if (ts == FASTILU_OK) h->tsell = true;
-      else if (ts != FASTILU_ERR_UNSUPPORTED) return ts;
+      else if (multi || ts != FASTILU_ERR_UNSUPPORTED) return ts;
     }
   }
   // structure classes for the class-program sweep (falls back to the hash kernel if absent)
@@ -596,9 +610,9 @@ static fastilu_status create_impl(fastilu_handle h, int64_t n, const int64_t *ro
   for (int i = 0; i < 5; i++) CU(cudaEventCreate(&h->ev[i]));
   if (multi) {
     int64_t nl_global = 0;
-    fastilu_status cs = comm_setup(h->comm, h->opt, h->row_begin, h->n, h->G, h->H, rp.data(),
-                                   nl_own, &nl_global, h->tsell ? h->T.W : 0,
-                                   h->tsell ? h->T.hash : 0, h->stream);
+    fastilu_status cs = comm_layout(h->comm, h->row_begin, h->n, h->G, h->H, rp.data(), nl_own,
+                                    &nl_global, h->tsell ? h->T.W : 0,
+                                    h->tsell ? h->T.hash : 0, h->stream);
     if (cs) return cs;
     const double nlg = (double)nl_global / (double)std::max<int64_t>(h->global_n, 1);
     int gt = 1;  // same rule as setup_configs, from the GLOBAL average (partition-independent)
