@@ -336,8 +336,10 @@ static fastilu_status setup_tsell(fastilu_handle h, const std::vector<unsigned l
   // accumulators per pass: all targets when they fit the register budget
   int chunk = T.W <= 72 ? T.W : (T.W + 1) / 2 <= 72 ? (T.W + 1) / 2 : 64;
   if (ev_ch) chunk = std::max(1, atoi(ev_ch));
+  const char *ev_mb = std::getenv("FASTILU_TSELL_MINB");
+  const int minb = ev_mb ? atoi(ev_mb) : 0;
   std::string log;
-  const std::string src = sweep_source(T, threads, chunk);
+  const std::string src = sweep_source(T, threads, chunk, minb);
   if (jit_get(src, "fastilu_tsell_sweep", h->device, &h->jit_sweep, &log)) {
     if (std::getenv("FASTILU_DEBUG")) fprintf(stderr, "fastilu: JIT failed: %s\n", log.c_str());
     FAIL(FASTILU_ERR_UNSUPPORTED);

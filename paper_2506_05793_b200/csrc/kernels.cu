@@ -556,10 +556,10 @@ cudaError_t launch_trisolve_first_U(const double *z, const double *udiag, const 
   return cudaGetLastError();
 }
 
-// One G-lane group handles R consecutive rows per iteration; the first 2G entries of every row
-// are loaded up front (column, value, then the gathered x) so that 2R independent gathers per
-// lane are in flight, the rest of a long row is streamed after.  Row sums are reduced across
-// the group (fixed shuffle tree), lane r writes row r.
+// One G-lane group per row: the lanes load G consecutive entries at a time (coalesced) and form
+// the rounded products l_ij x_j; the row sum is then taken in the oracle's order (ascending
+// columns, y - p_0 - p_1 - ...) by an ordered shuffle chain, so x is bitwise equal to the oracle
+// and to the template-SELL kernels (G14).
 template <int G, int R, bool LOWER>
 __global__ void __launch_bounds__(256)
 jacobi_kernel(DevPattern P, const double *__restrict__ vals, const double *__restrict__ ud,
@@ -569,51 +569,25 @@ jacobi_kernel(DevPattern P, const double *__restrict__ vals, const double *__res
   auto tile = cg::tiled_partition<G>(cg::this_thread_block());
   const int gpb = blockDim.x / G;
   const int lane = tile.thread_rank();
-  const int64_t stride = (int64_t)gridDim.x * gpb * R;
-  for (int64_t base = r0 + ((int64_t)blockIdx.x * gpb + threadIdx.x / G) * R; base < r1;
-       base += stride) {
-    int64_t b0[R], b1[R];
-#pragma unroll
-    for (int r = 0; r < R; r++) {
-      const int64_t row = base + r;
-      b0[r] = b1[r] = 0;
-      if (row < r1) {
-        const int64_t rb = P.rp[row];
-        const int nl = P.dloc[row];
-        b0[r] = LOWER ? rb : rb + nl + 1;
-        b1[r] = LOWER ? rb + nl : P.rp[row + 1];
-      }
+  const int64_t stride = (int64_t)gridDim.x * gpb;
+  for (int64_t row = r0 + (int64_t)blockIdx.x * gpb + threadIdx.x / G; row < r1; row += stride) {
+    const int64_t rb = P.rp[row];
+    const int nl = P.dloc[row];
+    const int64_t b0 = LOWER ? rb : rb + nl + 1;
+    const int64_t b1 = LOWER ? rb + nl : P.rp[row + 1];
+    double acc = rhs[row];
+    for (int64_t c = b0; c < b1; c += G) {
+      const int64_t p = c + lane;
+      const double pr = p < b1 ? __dmul_rn(vals[p], xo[P.ci[p]]) : 0.0;
+      const int cnt = (int)min((int64_t)G, b1 - c);
+      for (int q = 0; q < cnt; q++) acc = __dsub_rn(acc, tile.shfl(pr, q));
     }
-    int c0[R], c1[R];
-    double v0[R], v1[R], sum[R];
-#pragma unroll
-    for (int r = 0; r < R; r++) {
-      const int64_t p0 = b0[r] + lane, p1 = p0 + G;
-      c0[r] = p0 < b1[r] ? P.ci[p0] : -1;
-      v0[r] = p0 < b1[r] ? vals[p0] : 0.0;
-      c1[r] = p1 < b1[r] ? P.ci[p1] : -1;
-      v1[r] = p1 < b1[r] ? vals[p1] : 0.0;
-    }
-#pragma unroll
-    for (int r = 0; r < R; r++) {
-      const double x0 = c0[r] >= 0 ? xo[c0[r]] : 0.0;
-      const double x1 = c1[r] >= 0 ? xo[c1[r]] : 0.0;
-      sum[r] = fma(v1[r], x1, v0[r] * x0);
-    }
-#pragma unroll
-    for (int r = 0; r < R; r++)
-      for (int64_t p = b0[r] + lane + 2 * G; p < b1[r]; p += G) sum[r] = fma(vals[p], xo[P.ci[p]], sum[r]);
-#pragma unroll
-    for (int r = 0; r < R; r++) sum[r] = cg::reduce(tile, sum[r], cg::plus<double>());
-#pragma unroll
-    for (int r = 0; r < R; r++) {
-      const int64_t row = base + r;
-      if (lane == (r % G) && row < r1) {
-        double u = rhs[row] - sum[r];
-        if (!LOWER) u = __ddiv_rn(u, ud[row]);
-        const double v = (omega == 1.0) ? u : (1.0 - omega) * xo[row] + omega * u;
-        if (final) xfinal[row - Gh] = __dmul_rn(s[row], v); else xn[row] = v;
-      }
+    if (lane == 0) {
+      double u = acc;
+      if (!LOWER) u = __ddiv_rn(u, ud[row]);
+      const double v =
+          (omega == 1.0) ? u : __dadd_rn(__dmul_rn(1.0 - omega, xo[row]), __dmul_rn(omega, u));
+      if (final) xfinal[row - Gh] = __dmul_rn(s[row], v); else xn[row] = v;
     }
   }
 }
@@ -624,7 +598,7 @@ static cudaError_t launch_jacobi_t(const DevPattern &P, const double *vals, cons
                                    const double *s, int64_t r0, int64_t r1, int64_t Gh,
                                    double omega, bool final, int G, cudaStream_t st) {
   if (r1 <= r0) return cudaSuccess;
-  constexpr int R = 2;
+  constexpr int R = 1;
   const int threads = 256, gpb = threads / G;
   int64_t blocks = (r1 - r0 + (int64_t)gpb * R - 1) / ((int64_t)gpb * R);
   if (blocks > (1ll << 30)) blocks = 1ll << 30;

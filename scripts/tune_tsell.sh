@@ -1,13 +1,11 @@
 #!/bin/bash
-# Sweep-kernel tuning: accumulator chunk (registers) x threads per block, per workload.
+# Sweep-kernel tuning: threads per block x min blocks per SM (register cap), per workload.
 TAG=${1:-tune}
-for w in c3a_27pt_128_ilu1 c3b_27pt_128_ilu2; do
-  for th in 128 256; do
-    for ch in 0 40 32 20; do
-      if [ "$ch" = "0" ]; then unset FASTILU_TSELL_CHUNK; else export FASTILU_TSELL_CHUNK=$ch; fi
-      export FASTILU_TSELL_THREADS=$th
-      echo "== $w threads=$th chunk=$ch"
-      timeout 200 python bench.py --workload $w --steps 5 --warmup 2 --no-cpu --no-e2e 2>&1 | tail -1
-    done
+for w in ${WORKLOADS:-c3a_27pt_128_ilu1 c3b_27pt_128_ilu2}; do
+  for cfg in "128 0" "128 3" "128 4" "256 2" "64 6" "64 8"; do
+    set -- $cfg
+    export FASTILU_TSELL_THREADS=$1 FASTILU_TSELL_MINB=$2
+    echo "== $w threads=$1 minb=$2"
+    timeout 200 python bench.py --workload $w --steps 5 --warmup 2 --no-cpu --no-e2e 2>&1 | tail -1
   done
 done > gpurun_out/${TAG}_tune.log 2>&1

@@ -1,9 +1,10 @@
 """GPU parity: the CUDA path (through the C ABI) against the oracle, element by element.
 
 Tolerance (north_star): factors per entry |g - o| <= 1e-12 |o| (and g == o
-where o == 0); x per entry <= 1e-12 |o| with b > 0; pattern bit-exact.  The factor kernels use
-the oracle's operation order, so factors are in fact expected bitwise equal (asserted
-separately).  Inputs: seeded generators in problems/ only.
+where o == 0); x per entry <= 1e-12 |o| with b > 0; pattern bit-exact.  Every kernel uses the
+oracle's operation order (ascending pivots / columns, explicitly rounded products and
+differences), so factors and x are in fact bitwise equal (asserted separately).  Inputs: seeded
+generators in problems/ only.
 """
 import numpy as np
 import pytest
@@ -61,6 +62,8 @@ def full_check(a, k, ns, nt, omega=1.0, omega_tri=1.0, bitwise=True):
     np.testing.assert_allclose(f.residual_history(), fo.resid, rtol=rtol_r)
     xo = oracle.apply(fo, b, nt, omega_tri)
     assert_rel(x, xo, what="x")
+    if bitwise:  # every trisolve kernel sums in the oracle's order (G14)
+        assert np.array_equal(x, xo), "x not bitwise equal to the oracle"
     return f
 
 
