@@ -134,6 +134,16 @@ fastilu_status fastilu_apply(fastilu_handle h, const double *b, double *x, int n
  * synchronises.  This is the end-to-end entry point. */
 fastilu_status fastilu_apply_host(fastilu_handle h, const double *b, double *x, int ntrisweeps);
 
+/* FastILU-preconditioned restarted GMRES(restart) on A x = b (BASELINE config 5; the consumer of
+ * apply in the paper's experiments): right preconditioning with
+ * M^-1 = fastilu_apply(., ntrisweeps), x0 = 0, classical Gram-Schmidt with reorthogonalisation,
+ * stop when ||b - A x|| / ||b|| <= rtol (true residual at restarts) or after max_iters inner
+ * iterations.  b, x: DEVICE arrays of the owned rows.  Needs a successful compute.
+ * *iters = inner iterations, *relres = final relative residual.  Synchronises. */
+fastilu_status fastilu_gmres(fastilu_handle h, const double *b, double *x, int restart,
+                             double rtol, int max_iters, int ntrisweeps, int *iters,
+                             double *relres);
+
 /* Frees everything; fastilu_destroy(NULL) is a no-op. */
 fastilu_status fastilu_destroy(fastilu_handle h);
 

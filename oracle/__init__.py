@@ -18,6 +18,9 @@ Pins (tests/test_oracle_*.py, `-m "not gpu"`):
     residual non-increasing above the roundoff floor; diagonal A immediate.
   * trisolve: == substitution after nlevels sweeps (bitwise), T = I, 1 sweep
     = D^-1 b; substitution == scipy solve_triangular.
+  * gmres (NEXT row f1): A = I converges in one iteration; an exact LU preconditioner in at
+    most two; unpreconditioned SPD systems within n iterations to numpy.linalg.solve;
+    iteration counts of SURVEY.md G18's independent computation on the anisotropic problem.
 Functions here are all pinned; none is "parity unpinned".
 """
 from __future__ import annotations
@@ -267,6 +270,79 @@ def subst_upper(pat: Pattern, vals, z):
     lib().orc_subst_upper(pat.n, _p(pat.row_ptr, I64P), _p(pat.col_idx, I32P), _p(vals, F64P),
                           _p(z, F64P), _p(w, F64P))
     return w
+
+
+def spmv(a, v):
+    """y = A v for a CSR matrix (plain loop over rows in numpy, row sums left to right)."""
+    v = _f64(v)
+    rows = np.repeat(np.arange(a.n), np.diff(a.row_ptr))
+    return np.bincount(rows, weights=a.values * v[a.col_idx], minlength=a.n)
+
+
+def gmres(a, b, precond, restart: int = 60, rtol: float = 1e-6, max_iters: int = 1000):
+    """Restarted GMRES(m), right preconditioning x = M^-1 y, modified Gram-Schmidt, Givens
+    rotations, x0 = 0, converged when ||b - A x|| / ||b|| <= rtol (the paper's
+    protocol: GMRES(60), six orders of magnitude).  `precond(v)` applies M^-1.
+    Returns (x, inner iterations, final relative residual)."""
+    b = _f64(b)
+    n = b.shape[0]
+    x = np.zeros(n)
+    bnorm = float(np.linalg.norm(b))
+    if bnorm == 0.0:
+        return x, 0, 0.0
+    r = b.copy()
+    beta = bnorm
+    total = 0
+    while beta / bnorm > rtol and total < max_iters:
+        V = np.zeros((restart + 1, n))
+        Hm = np.zeros((restart + 1, restart))
+        cs = np.zeros(restart)
+        sn = np.zeros(restart)
+        g = np.zeros(restart + 1)
+        g[0] = beta
+        V[0] = r / beta
+        j = 0
+        while j < restart and total < max_iters:
+            w = spmv(a, precond(V[j]))
+            for q in range(j + 1):  # modified Gram-Schmidt
+                Hm[q, j] = float(np.dot(V[q], w))
+                w = w - Hm[q, j] * V[q]
+            Hm[j + 1, j] = float(np.linalg.norm(w))
+            if Hm[j + 1, j] > 0.0:
+                V[j + 1] = w / Hm[j + 1, j]
+            for q in range(j):
+                t = cs[q] * Hm[q, j] + sn[q] * Hm[q + 1, j]
+                Hm[q + 1, j] = -sn[q] * Hm[q, j] + cs[q] * Hm[q + 1, j]
+                Hm[q, j] = t
+            rr = float(np.hypot(Hm[j, j], Hm[j + 1, j]))
+            cs[j], sn[j] = (Hm[j, j] / rr, Hm[j + 1, j] / rr) if rr > 0 else (1.0, 0.0)
+            Hm[j, j], Hm[j + 1, j] = rr, 0.0
+            g[j + 1] = -sn[j] * g[j]
+            g[j] = cs[j] * g[j]
+            total += 1
+            j += 1
+            if abs(g[j]) <= rtol * bnorm or Hm[j, j - 1] == 0.0 and rr == 0.0:
+                break
+        y = np.zeros(j)
+        for q in range(j - 1, -1, -1):
+            y[q] = (g[q] - np.dot(Hm[q, q + 1:j], y[q + 1:j])) / Hm[q, q]
+        x = x + precond(V[:j].T @ y)
+        r = b - spmv(a, x)
+        beta = float(np.linalg.norm(r))
+    return x, total, beta / bnorm
+
+
+def fastilu_preconditioner(f: "Factors", ntri: int, omega_tri: float = 1.0):
+    """M^-1 v = s o U^-1 L^-1 (s o v) with ntri Jacobi sweeps per factor (the FastILU apply)."""
+    return lambda v: apply(f, v, ntri, omega_tri)
+
+
+def exact_preconditioner(f: "Factors"):
+    """M^-1 v = s o U^-1 L^-1 (s o v) by exact substitution (config 5 arm C)."""
+    def pre(v):
+        z = subst_lower(f.pattern, f.vals, f.s * _f64(v))
+        return f.s * subst_upper(f.pattern, f.vals, z)
+    return pre
 
 
 def windowed(a_full, plane: int, lo_plane: int, hi_plane: int, k: int, nsweeps: int,

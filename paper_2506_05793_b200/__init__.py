@@ -60,6 +60,8 @@ _SIGS = {
     "fastilu_apply": (C.c_int, [H, C.c_void_p, C.c_void_p, C.c_int]),
     "fastilu_apply_host": (C.c_int, [H, F64P, F64P, C.c_int]),
     "fastilu_destroy": (C.c_int, [H]),
+    "fastilu_gmres": (C.c_int, [H, C.c_void_p, C.c_void_p, C.c_int, C.c_double, C.c_int, C.c_int,
+                                C.POINTER(C.c_int), C.POINTER(C.c_double)]),
     "fastilu_get_sizes": (C.c_int, [H, I64P, I64P, I64P]),
     "fastilu_get_pattern": (C.c_int, [H, I64P, I32P, I8P]),
     "fastilu_get_factors": (C.c_int, [H, F64P, F64P]),
@@ -266,6 +268,17 @@ class FastILU:
         _check(lib().fastilu_apply_host(self._h, _p(b, F64P), _p(x, F64P), int(ntrisweeps)),
                "fastilu_apply_host", self._h)
         return x
+
+    def gmres(self, b, x, restart: int = 60, rtol: float = 1e-6, max_iters: int = 1000,
+              ntrisweeps: int = 5):
+        """Right-preconditioned GMRES(restart) on A x = b (device arrays); returns
+        (inner iterations, relative residual)."""
+        it = C.c_int(0)
+        rr = C.c_double(0.0)
+        _check(lib().fastilu_gmres(self._h, _ptr(b), _ptr(x), int(restart), float(rtol),
+                                   int(max_iters), int(ntrisweeps), C.byref(it), C.byref(rr)),
+               "fastilu_gmres", self._h)
+        return it.value, rr.value
 
     # -- introspection
     def pattern(self):

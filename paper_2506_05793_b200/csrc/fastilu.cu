@@ -74,6 +74,10 @@ struct fastilu_handle_s {
   void *jit_sweep = nullptr;
   int t_threads = 128, t_grid = 1, t_regs = 0, t_spill = 0;
   int64_t t_ntiles = 0;
+  // GMRES workspace (allocated on first use)
+  double *gm_V = nullptr, *gm_w = nullptr, *gm_ext = nullptr, *gm_u = nullptr, *gm_r = nullptr;
+  double *gm_part = nullptr, *gm_c = nullptr, *gm_hbuf = nullptr;  // gm_hbuf pinned host
+  int gm_m = 0, G_spmv = 32;
   ErrFlags *d_err = nullptr;
   ErrFlags *h_err = nullptr;  // pinned
   double *h_r2 = nullptr;     // pinned, hist_cap
@@ -570,7 +574,6 @@ static fastilu_status create_impl(fastilu_handle h, int64_t n, const int64_t *ro
     CU(dalloc(&h->d_rp, h->nloc + 1));
     CU(dalloc(&h->d_ci, h->nnz_loc));
     CU(dalloc(&h->d_dloc, h->nloc));
-    CU(dalloc(&h->d_aci, h->nnzA_loc));
     CU(dalloc(&h->d_apos, h->nnzA_loc));
     CU(dalloc(&h->d_ahat, h->nnzA_loc));  // ahat on A's pattern (ghost rows' stay 0)
     CU(cudaMemset(h->d_ahat, 0, sizeof(double) * h->nnzA_loc));
@@ -578,6 +581,7 @@ static fastilu_status create_impl(fastilu_handle h, int64_t n, const int64_t *ro
     for (int b = 0; b < 2; b++) CU(dalloc(&h->d_vals[b], h->nnz_loc));
   }
   CU(dalloc(&h->d_arp, h->nloc + 1));
+  CU(dalloc(&h->d_aci, h->nnzA_loc));  // A's local columns (CSR init, GMRES SpMV)
   CU(dalloc(&h->d_adiag, h->nloc));
   CU(dalloc(&h->d_aval, h->nnzA_loc));
   for (int b = 0; b < 2; b++) {
@@ -595,9 +599,15 @@ static fastilu_status create_impl(fastilu_handle h, int64_t n, const int64_t *ro
     CU(cudaMemcpy(h->d_ci, ci.data(), sizeof(int32_t) * ci.size(), cudaMemcpyHostToDevice));
     CU(cudaMemcpy(h->d_dloc, dloc.data(), sizeof(int32_t) * dloc.size(),
                   cudaMemcpyHostToDevice));
-    CU(cudaMemcpy(h->d_aci, aci.data(), sizeof(int32_t) * aci.size(), cudaMemcpyHostToDevice));
     CU(cudaMemcpy(h->d_apos, apos.data(), sizeof(int32_t) * apos.size(),
                   cudaMemcpyHostToDevice));
+  }
+  CU(cudaMemcpy(h->d_aci, aci.data(), sizeof(int32_t) * aci.size(), cudaMemcpyHostToDevice));
+  {
+    const double a_avg = n ? (double)(arp[h->nloc] - arp[h->G]) / (double)n : 1.0;
+    int gs = 4;
+    while (gs < a_avg && gs < 32) gs *= 2;
+    h->G_spmv = gs;
   }
   CU(cudaMemcpy(h->d_arp, arp.data(), sizeof(int64_t) * arp.size(), cudaMemcpyHostToDevice));
   CU(cudaMemcpy(h->d_adiag, adiag.data(), sizeof(int32_t) * adiag.size(),
@@ -881,6 +891,145 @@ extern "C" fastilu_status fastilu_apply_host(fastilu_handle h, const double *b, 
   return FASTILU_OK;
 }
 
+// --------------------------------------------------------------------------- GMRES (config 5)
+// Restarted GMRES(m) with right preconditioning x = M^-1 y, M^-1 = fastilu_apply (a fixed
+// linear operator: ntri Jacobi sweeps from 0), classical Gram-Schmidt with one
+// reorthogonalisation (CGS2: two batched multi-dot / multi-axpy passes per iteration instead of
+// m sequential MGS dots), Givens rotations on the host, x0 = 0, convergence on the relative
+// residual ||b - A x|| / ||b|| <= rtol.
+extern "C" fastilu_status fastilu_gmres(fastilu_handle h, const double *b, double *x,
+                                        int restart, double rtol, int max_iters,
+                                        int ntrisweeps, int *iters_out, double *relres_out) {
+  if (!h || restart < 1 || restart > 120 || !(rtol > 0.0) || max_iters < 1 || ntrisweeps < 1 ||
+      (h->n > 0 && (!b || !x)))
+    FAIL(FASTILU_ERR_INVALID_ARG);
+  if (!h->computed) FAIL(FASTILU_ERR_STATE);
+  cudaSetDevice(h->device);
+  cudaStream_t st = h->stream;
+  const int64_t n = h->n;
+  const int m = restart;
+  if (h->gm_m < m) {
+    void *old[] = {h->gm_V, h->gm_w, h->gm_ext, h->gm_u, h->gm_r, h->gm_part, h->gm_c};
+    for (void *p : old)
+      if (p) cudaFree(p);
+    if (h->gm_hbuf) cudaFreeHost(h->gm_hbuf);
+    CU(dalloc(&h->gm_V, (int64_t)(m + 1) * std::max<int64_t>(n, 1)));
+    CU(dalloc(&h->gm_w, n));
+    CU(dalloc(&h->gm_ext, h->E));
+    CU(cudaMemset(h->gm_ext, 0, sizeof(double) * h->E));
+    CU(dalloc(&h->gm_u, n));
+    CU(dalloc(&h->gm_r, n));
+    CU(dalloc(&h->gm_part, (int64_t)(m + 2) * kDotBlocks));
+    CU(dalloc(&h->gm_c, m + 2));
+    CU(cudaMallocHost((void **)&h->gm_hbuf, sizeof(double) * (m + 2)));
+    h->gm_m = m;
+  }
+  double *V = h->gm_V, *w = h->gm_w, *u = h->gm_u, *r = h->gm_r;
+  const int64_t ldv = std::max<int64_t>(n, 1);
+  // collective dot products: k local partial sums -> host -> sum over ranks
+  auto dots = [&](int k, const double *vecs, const double *vec, double *out) -> fastilu_status {
+    CU(launch_mdot(vecs, ldv, k, vec, n, h->gm_part, h->gm_c, st));
+    CU(cudaMemcpyAsync(h->gm_hbuf, h->gm_c, sizeof(double) * k, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    for (int q = 0; q < k; q++) out[q] = h->gm_hbuf[q];
+    if (h->comm) {
+      ErrFlags dummy{~0ull, ~0ull};
+      return comm_allreduce_host(h->comm, out, k, dummy);
+    }
+    return FASTILU_OK;
+  };
+  auto spmv = [&](const double *v, double *y) -> fastilu_status {  // y = A v
+    CU(cudaMemcpyAsync(h->gm_ext + h->G, v, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    if (h->comm) {
+      fastilu_status cs = comm_vector_halo(h->comm, h->gm_ext, st, true, true);
+      if (cs) return cs;
+    }
+    CU(launch_spmv(h->d_arp, h->d_aci, h->d_aval, h->gm_ext, y, h->G, h->G + n, h->G, h->G_spmv,
+                   st));
+    return FASTILU_OK;
+  };
+  auto nrm = [&](const double *v, double *out) -> fastilu_status {
+    fastilu_status fs = dots(1, v, v, out);
+    *out = std::sqrt(*out);
+    return fs;
+  };
+  fastilu_status fs;
+  CU(cudaEventRecord(h->ev[3], st));
+  CU(cudaMemsetAsync(x, 0, sizeof(double) * n, st));
+  CU(cudaMemcpyAsync(r, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+  double bnorm = 0.0;
+  if ((fs = nrm(b, &bnorm))) return fs;
+  double beta = bnorm;
+  int total = 0;
+  std::vector<double> H((size_t)(m + 1) * m), cs(m), sn(m), g(m + 1), hv(m + 2), h2(m + 2);
+  while (bnorm > 0.0 && beta / bnorm > rtol && total < max_iters) {
+    CU(launch_axpby(1.0 / beta, r, 0.0, V, n, st));  // V_0 = r / beta
+    std::fill(g.begin(), g.end(), 0.0);
+    g[0] = beta;
+    int j = 0;
+    for (; j < m && total < max_iters; j++) {
+      if ((fs = apply_impl(h, V + j * ldv, u, ntrisweeps))) return fs;  // u = M^-1 V_j
+      if ((fs = spmv(u, w))) return fs;                                   // w = A u
+      if ((fs = dots(j + 1, V, w, hv.data()))) return fs;                 // CGS pass 1
+      for (int q = 0; q <= j; q++) h->gm_hbuf[q] = hv[q];
+      CU(cudaMemcpyAsync(h->gm_c, h->gm_hbuf, sizeof(double) * (j + 1), cudaMemcpyHostToDevice,
+                         st));
+      CU(launch_maxpy(V, ldv, j + 1, h->gm_c, w, n, -1.0, st));
+      if ((fs = dots(j + 1, V, w, h2.data()))) return fs;                 // CGS pass 2
+      for (int q = 0; q <= j; q++) h->gm_hbuf[q] = h2[q];
+      CU(cudaMemcpyAsync(h->gm_c, h->gm_hbuf, sizeof(double) * (j + 1), cudaMemcpyHostToDevice,
+                         st));
+      CU(launch_maxpy(V, ldv, j + 1, h->gm_c, w, n, -1.0, st));
+      double hn = 0.0;
+      if ((fs = nrm(w, &hn))) return fs;
+      for (int q = 0; q <= j; q++) H[(size_t)q * m + j] = hv[q] + h2[q];
+      H[(size_t)(j + 1) * m + j] = hn;
+      if (hn > 0.0) CU(launch_axpby(1.0 / hn, w, 0.0, V + (j + 1) * ldv, n, st));
+      for (int q = 0; q < j; q++) {  // previous rotations
+        const double a = H[(size_t)q * m + j], c = H[(size_t)(q + 1) * m + j];
+        H[(size_t)q * m + j] = cs[q] * a + sn[q] * c;
+        H[(size_t)(q + 1) * m + j] = -sn[q] * a + cs[q] * c;
+      }
+      const double a = H[(size_t)j * m + j], c = H[(size_t)(j + 1) * m + j];
+      const double rr = std::hypot(a, c);
+      cs[j] = rr > 0.0 ? a / rr : 1.0;
+      sn[j] = rr > 0.0 ? c / rr : 0.0;
+      H[(size_t)j * m + j] = rr;
+      H[(size_t)(j + 1) * m + j] = 0.0;
+      g[j + 1] = -sn[j] * g[j];
+      g[j] = cs[j] * g[j];
+      total++;
+      if (std::fabs(g[j + 1]) <= rtol * bnorm || hn == 0.0) {
+        j++;
+        break;
+      }
+    }
+    // y = H^-1 g (upper triangular j x j), x += M^-1 (V y)
+    std::vector<double> y(j, 0.0);
+    for (int q = j - 1; q >= 0; q--) {
+      double t = g[q];
+      for (int c2 = q + 1; c2 < j; c2++) t -= H[(size_t)q * m + c2] * y[c2];
+      y[q] = t / H[(size_t)q * m + q];
+    }
+    for (int q = 0; q < j; q++) h->gm_hbuf[q] = y[q];
+    CU(cudaMemcpyAsync(h->gm_c, h->gm_hbuf, sizeof(double) * j, cudaMemcpyHostToDevice, st));
+    CU(cudaMemsetAsync(w, 0, sizeof(double) * n, st));
+    CU(launch_maxpy(V, ldv, j, h->gm_c, w, n, 1.0, st));
+    if ((fs = apply_impl(h, w, u, ntrisweeps))) return fs;
+    CU(launch_axpby(1.0, u, 1.0, x, n, st));
+    // true residual r = b - A x
+    if ((fs = spmv(x, w))) return fs;
+    CU(cudaMemcpyAsync(r, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    CU(launch_axpby(-1.0, w, 1.0, r, n, st));
+    if ((fs = nrm(r, &beta))) return fs;
+  }
+  CU(cudaEventRecord(h->ev[4], st));
+  CU(cudaStreamSynchronize(st));
+  if (iters_out) *iters_out = total;
+  if (relres_out) *relres_out = bnorm > 0.0 ? beta / bnorm : 0.0;
+  return FASTILU_OK;
+}
+
 // --------------------------------------------------------------------------- introspection
 extern "C" fastilu_status fastilu_get_sizes(fastilu_handle h, int64_t *n, int64_t *nnz_S,
                                             int64_t *nnz_A) {
@@ -983,11 +1132,13 @@ extern "C" fastilu_status fastilu_destroy(fastilu_handle h) {
                   h->d_ahat,  h->d_s,     h->d_ad,       h->d_y,    h->d_z[0],    h->d_z[1],
                   h->d_w[0],  h->d_w[1],  h->d_bx,       h->d_partials, h->d_r2,  h->d_err,
                   h->d_rclass, h->d_coff, h->d_caoff, h->d_prog, h->d_toff, h->d_toffA,
-                  h->d_tasrc, h->d_tw2a, h->d_tmask, h->d_counter};
+                  h->d_tasrc, h->d_tw2a, h->d_tmask, h->d_counter, h->gm_V, h->gm_w,
+                  h->gm_ext, h->gm_u, h->gm_r, h->gm_part, h->gm_c};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   if (h->h_err) cudaFreeHost(h->h_err);
   if (h->h_r2) cudaFreeHost(h->h_r2);
+  if (h->gm_hbuf) cudaFreeHost(h->gm_hbuf);
   for (int i = 0; i < 5; i++)
     if (h->ev[i]) cudaEventDestroy(h->ev[i]);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);

@@ -779,4 +779,136 @@ cudaError_t launch_sumsq(const double *x, int64_t n, double *partials, double *d
   return cudaGetLastError();
 }
 
+// ----------------------------------------------------------------------------------------
+// GMRES building blocks (config 5).  Reductions are deterministic (fixed grid, fixed trees).
+// ----------------------------------------------------------------------------------------
+template <int G>
+__global__ void __launch_bounds__(256)
+spmv_kernel(const int64_t *__restrict__ arp, const int32_t *__restrict__ aci,
+            const double *__restrict__ aval, const double *__restrict__ x,
+            double *__restrict__ y, int64_t r0, int64_t r1, int64_t Gh) {
+  auto tile = cg::tiled_partition<G>(cg::this_thread_block());
+  const int gpb = blockDim.x / G;
+  const int lane = tile.thread_rank();
+  const int64_t stride = (int64_t)gridDim.x * gpb;
+  for (int64_t row = r0 + (int64_t)blockIdx.x * gpb + threadIdx.x / G; row < r1; row += stride) {
+    double sum = 0.0;
+    for (int64_t q = arp[row] + lane; q < arp[row + 1]; q += G) sum = fma(aval[q], x[aci[q]], sum);
+    sum = cg::reduce(tile, sum, cg::plus<double>());
+    if (lane == 0) y[row - Gh] = sum;
+  }
+}
+
+cudaError_t launch_spmv(const int64_t *arp, const int32_t *aci, const double *aval,
+                        const double *x, double *y, int64_t r0, int64_t r1, int64_t Gh, int G,
+                        cudaStream_t st) {
+  if (r1 <= r0) return cudaSuccess;
+  const int threads = 256, gpb = threads / G;
+  int64_t blocks = (r1 - r0 + gpb - 1) / gpb;
+  if (blocks > (1ll << 30)) blocks = 1ll << 30;
+  switch (G) {
+    case 4: spmv_kernel<4><<<(unsigned)blocks, threads, 0, st>>>(arp, aci, aval, x, y, r0, r1, Gh); break;
+    case 8: spmv_kernel<8><<<(unsigned)blocks, threads, 0, st>>>(arp, aci, aval, x, y, r0, r1, Gh); break;
+    case 16: spmv_kernel<16><<<(unsigned)blocks, threads, 0, st>>>(arp, aci, aval, x, y, r0, r1, Gh); break;
+    default: spmv_kernel<32><<<(unsigned)blocks, threads, 0, st>>>(arp, aci, aval, x, y, r0, r1, Gh); break;
+  }
+  return cudaGetLastError();
+}
+
+// block b of the grid reduces its row range of every V_j . w (rows strided by the grid)
+__global__ void __launch_bounds__(256)
+mdot_kernel(const double *__restrict__ V, int64_t ldv, int k, const double *__restrict__ w,
+            int64_t n, double *__restrict__ partials) {
+  __shared__ double red[8][64];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int j0 = 0; j0 < k; j0 += 64) {
+    const int kk = min(64, k - j0);
+    double acc[8];
+    for (int jb = 0; jb < kk; jb += 8) {
+#pragma unroll
+      for (int q = 0; q < 8; q++) acc[q] = 0.0;
+      for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+           i += (int64_t)gridDim.x * blockDim.x) {
+        const double wi = w[i];
+#pragma unroll
+        for (int q = 0; q < 8; q++)
+          if (jb + q < kk) acc[q] = fma(V[(int64_t)(j0 + jb + q) * ldv + i], wi, acc[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < 8; q++) {
+        double v = acc[q];
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+        if (lane == 0 && jb + q < kk) red[warp][jb + q] = v;
+      }
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < kk; j += blockDim.x) {
+      double t = 0.0;
+      for (int q = 0; q < (int)(blockDim.x >> 5); q++) t += red[q][j];
+      partials[(int64_t)(j0 + j) * gridDim.x + blockIdx.x] = t;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void mdot_reduce_kernel(const double *__restrict__ partials, int nb, int k,
+                                   double *__restrict__ out) {
+  __shared__ double sh[256];
+  for (int j = blockIdx.x; j < k; j += gridDim.x) {
+    double t = 0.0;
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) t += partials[(int64_t)j * nb + b];
+    sh[threadIdx.x] = t;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+      if ((int)threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) out[j] = sh[0];
+    __syncthreads();
+  }
+}
+
+cudaError_t launch_mdot(const double *V, int64_t ldv, int k, const double *w, int64_t n,
+                        double *partials, double *out, cudaStream_t st) {
+  if (k <= 0) return cudaSuccess;
+  mdot_kernel<<<kDotBlocks, 256, 0, st>>>(V, ldv, k, w, n, partials);
+  mdot_reduce_kernel<<<min(k, 64), 256, 0, st>>>(partials, kDotBlocks, k, out);
+  return cudaGetLastError();
+}
+
+__global__ void maxpy_kernel(const double *__restrict__ V, int64_t ldv, int k,
+                             const double *__restrict__ c, double *__restrict__ w, int64_t n,
+                             double sign) {
+  __shared__ double sc[128];
+  for (int j = threadIdx.x; j < k && j < 128; j += blockDim.x) sc[j] = sign * c[j];
+  __syncthreads();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double t = w[i];
+    for (int j = 0; j < k; j++) t = fma(sc[j], V[(int64_t)j * ldv + i], t);
+    w[i] = t;
+  }
+}
+
+cudaError_t launch_maxpy(const double *V, int64_t ldv, int k, const double *c, double *w,
+                         int64_t n, double sign, cudaStream_t st) {
+  if (k <= 0) return cudaSuccess;
+  maxpy_kernel<<<vec_blocks(n), 256, 0, st>>>(V, ldv, k, c, w, n, sign);
+  return cudaGetLastError();
+}
+
+__global__ void axpby_kernel(double a, const double *__restrict__ x, double b,
+                             double *__restrict__ y, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = (b == 0.0) ? a * x[i] : fma(a, x[i], b * y[i]);
+}
+
+cudaError_t launch_axpby(double a, const double *x, double b, double *y, int64_t n,
+                         cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  axpby_kernel<<<vec_blocks(n), 256, 0, st>>>(a, x, b, y, n);
+  return cudaGetLastError();
+}
+
 }  // namespace fastilu
