@@ -72,7 +72,7 @@ struct fastilu_handle_s {
   unsigned long long *d_tmask = nullptr;
   unsigned int *d_counter = nullptr;
   void *jit_sweep = nullptr;
-  int t_threads = 128, t_grid = 1, t_regs = 0, t_spill = 0;
+  int t_threads = 128, t_grid = 1, t_regs = 0, t_spill = 0, t_rows_tile = 128;
   int64_t t_ntiles = 0;
   // GMRES workspace (allocated on first use)
   double *gm_V = nullptr, *gm_w = nullptr, *gm_ext = nullptr, *gm_u = nullptr, *gm_r = nullptr;
@@ -335,15 +335,16 @@ static fastilu_status setup_tsell(fastilu_handle h, const std::vector<unsigned l
   const Template &T = h->T;
   h->nsl = (h->nloc + 31) / 32;
   const char *ev_th = std::getenv("FASTILU_TSELL_THREADS");
-  const char *ev_ch = std::getenv("FASTILU_TSELL_CHUNK");
-  const int threads = ev_th ? std::max(32, atoi(ev_th) / 32 * 32) : 128;
-  // accumulators per pass: all targets when they fit the register budget
-  int chunk = T.W <= 72 ? T.W : (T.W + 1) / 2 <= 72 ? (T.W + 1) / 2 : 64;
-  if (ev_ch) chunk = std::max(1, atoi(ev_ch));
+  const char *ev_pa = std::getenv("FASTILU_TSELL_PARTS");
   const char *ev_mb = std::getenv("FASTILU_TSELL_MINB");
+  const int threads = ev_th ? std::max(32, atoi(ev_th) / 32 * 32) : 128;
+  // targets per warp: ~32 accumulators per thread (63 -> 2 parts, 115 -> 4 parts)
+  int parts = std::max(1, (T.W + 35) / 36);
+  if (parts == 3) parts = 4;
+  if (ev_pa) parts = std::max(1, atoi(ev_pa));
   const int minb = ev_mb ? atoi(ev_mb) : 0;
   std::string log;
-  const std::string src = sweep_source(T, threads, chunk, minb);
+  const std::string src = sweep_source(T, threads, parts, minb);
   if (jit_get(src, "fastilu_tsell_sweep", h->device, &h->jit_sweep, &log)) {
     if (std::getenv("FASTILU_DEBUG")) fprintf(stderr, "fastilu: JIT failed: %s\n", log.c_str());
     FAIL(FASTILU_ERR_UNSUPPORTED);
@@ -355,7 +356,8 @@ static fastilu_status setup_tsell(fastilu_handle h, const std::vector<unsigned l
             T.c0, T.WA, T.terms.size(), h->t_regs, h->t_spill, bps);
   if (bps < 1) FAIL(FASTILU_ERR_UNSUPPORTED);
   h->t_threads = threads;
-  h->t_ntiles = std::max<int64_t>(1, (h->n + threads - 1) / threads);
+  h->t_rows_tile = sweep_rows_per_tile(threads, parts);
+  h->t_ntiles = std::max<int64_t>(1, (h->n + h->t_rows_tile - 1) / h->t_rows_tile);
   h->t_grid = (int)std::min<int64_t>((int64_t)sm_count(h->device) * bps, h->t_ntiles);
   const int64_t nv = h->nsl * T.W * 32;
   for (int b = 0; b < 2; b++) {
@@ -1108,9 +1110,10 @@ extern "C" fastilu_status fastilu_get_info(fastilu_handle h, char *buf, int cap)
   char tmp[512];
   if (h->tsell)
     snprintf(tmp, sizeof(tmp),
-             "path=tsell W=%d c0=%d WA=%d terms=%zu threads=%d grid=%d regs=%d local=%d "
-             "tiles=%lld G=%lld H=%lld",
-             h->T.W, h->T.c0, h->T.WA, h->T.terms.size(), h->t_threads, h->t_grid, h->t_regs,
+             "path=tsell W=%d c0=%d WA=%d terms=%zu threads=%d rows/tile=%d grid=%d regs=%d "
+             "local=%d tiles=%lld G=%lld H=%lld",
+             h->T.W, h->T.c0, h->T.WA, h->T.terms.size(), h->t_threads, h->t_rows_tile,
+             h->t_grid, h->t_regs,
              h->t_spill, (long long)h->t_ntiles, (long long)h->G, (long long)h->H);
   else
     snprintf(tmp, sizeof(tmp),
