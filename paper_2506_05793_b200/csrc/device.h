@@ -104,7 +104,10 @@ struct TDev {
   const int32_t *asrc;    // [slice][a][lane]: index of A's entry in the local A arrays, or -1
 };
 
-cudaError_t launch_tsell_init(const TDev &t, const double *aval, const double *s,
+// A's CSR values -> template slots aT (nslices * WA * 32), rows [0, nrows)
+cudaError_t launch_tsell_gather_a(const TDev &t, const double *aval, int64_t nrows, double *aT,
+                                  cudaStream_t st);
+cudaError_t launch_tsell_init(const TDev &t, const double *aT, const double *s,
                               const double *ad, int64_t r0, int64_t r1, double *ahatT,
                               double *vals, double *udiag, ErrFlags *err, cudaStream_t st);
 cudaError_t launch_tsell_jacobi(const TDev &t, bool lower, const double *vals,

@@ -71,6 +71,7 @@ struct fastilu_handle_s {
   int8_t *d_tw2a = nullptr;
   unsigned long long *d_tmask = nullptr;
   unsigned int *d_counter = nullptr;
+  double *d_aT = nullptr;  // A's values in template slots (refreshed by set_values)
   void *jit_sweep = nullptr;
   int t_threads = 128, t_grid = 1, t_regs = 0, t_spill = 0, t_rows_tile = 128;
   int64_t t_ntiles = 0;
@@ -319,10 +320,13 @@ static fastilu_status setup_configs(fastilu_handle h, const std::vector<int64_t>
   return FASTILU_OK;
 }
 
+static TDev tdev(fastilu_handle h);
+
 static fastilu_status upload_values(fastilu_handle h, const double *values, bool device) {
   cudaMemcpyKind kind = device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
   CU(cudaMemcpyAsync(h->d_aval, values + h->a_in_off, sizeof(double) * h->nnzA_loc, kind,
                      h->stream));
+  if (h->tsell) CU(launch_tsell_gather_a(tdev(h), h->d_aval, h->nloc, h->d_aT, h->stream));
   if (!device) CU(cudaStreamSynchronize(h->stream));
   h->have_values = true;
   h->computed = false;
@@ -366,6 +370,8 @@ static fastilu_status setup_tsell(fastilu_handle h, const std::vector<unsigned l
   }
   CU(dalloc(&h->d_ahat, h->nsl * T.WA * 32));
   CU(cudaMemset(h->d_ahat, 0, sizeof(double) * h->nsl * T.WA * 32));
+  CU(dalloc(&h->d_aT, h->nsl * T.WA * 32));
+  CU(cudaMemset(h->d_aT, 0, sizeof(double) * h->nsl * T.WA * 32));
   CU(dalloc(&h->d_tmask, (int64_t)mask.size()));
   CU(dalloc(&h->d_tasrc, (int64_t)asrc.size()));
   CU(dalloc(&h->d_toff, T.W));
@@ -709,7 +715,7 @@ static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, i
   }
   // a3: ahat and the initial guess (iterate 0) for the owned rows
   if (h->tsell)
-    CU(launch_tsell_init(tdev(h), h->d_aval, h->d_s, h->d_ad, r0, r1, h->d_ahat, h->d_vals[0],
+    CU(launch_tsell_init(tdev(h), h->d_aT, h->d_s, h->d_ad, r0, r1, h->d_ahat, h->d_vals[0],
                          h->d_ud[0], h->d_err, st));
   else
     CU(launch_init(P, h->d_arp, h->d_aci, h->d_apos, h->d_aval, h->d_s, h->d_ad, r0, r1,
@@ -1136,7 +1142,7 @@ extern "C" fastilu_status fastilu_destroy(fastilu_handle h) {
                   h->d_w[0],  h->d_w[1],  h->d_bx,       h->d_partials, h->d_r2,  h->d_err,
                   h->d_rclass, h->d_coff, h->d_caoff, h->d_prog, h->d_toff, h->d_toffA,
                   h->d_tasrc, h->d_tw2a, h->d_tmask, h->d_counter, h->gm_V, h->gm_w,
-                  h->gm_ext, h->gm_u, h->gm_r, h->gm_part, h->gm_c};
+                  h->gm_ext, h->gm_u, h->gm_r, h->gm_part, h->gm_c, h->d_aT};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   if (h->h_err) cudaFreeHost(h->h_err);

@@ -640,9 +640,30 @@ __device__ __forceinline__ bool tbit(const unsigned long long *m, int w) {
   return (m[w >> 6] >> (w & 63)) & 1ull;
 }
 
-// a2/a3 on the template layout: ahat on A's sub-template and the initial guess (R4, R5).
+// A's values in CSR order -> A's template slots (once per fastilu_set_values; lane per row).
 __global__ void __launch_bounds__(256)
-tsell_init_kernel(TDev t, const double *__restrict__ aval, const double *__restrict__ s,
+tsell_gather_a_kernel(TDev t, const double *__restrict__ aval, int64_t nrows,
+                      double *__restrict__ aT) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nrows) return;
+  const int64_t sl = i >> 5, ln = i & 31;
+  for (int a = 0; a < t.WA; a++) {
+    const int32_t q = t.asrc[(sl * t.WA + a) * 32 + ln];
+    aT[(sl * t.WA + a) * 32 + ln] = q >= 0 ? aval[q] : 0.0;
+  }
+}
+
+cudaError_t launch_tsell_gather_a(const TDev &t, const double *aval, int64_t nrows, double *aT,
+                                  cudaStream_t st) {
+  if (nrows <= 0) return cudaSuccess;
+  tsell_gather_a_kernel<<<(unsigned)((nrows + 255) / 256), 256, 0, st>>>(t, aval, nrows, aT);
+  return cudaGetLastError();
+}
+
+// a2/a3 on the template layout: ahat on A's sub-template and the initial guess (R4, R5).
+// Reads A's values from their template copy aT (coalesced), writes ahatT and iterate 0.
+__global__ void __launch_bounds__(256)
+tsell_init_kernel(TDev t, const double *__restrict__ aT, const double *__restrict__ s,
                   const double *__restrict__ ad, int64_t r0, int64_t r1,
                   double *__restrict__ ahatT, double *__restrict__ vals,
                   double *__restrict__ udiag, ErrFlags *err) {
@@ -660,17 +681,16 @@ tsell_init_kernel(TDev t, const double *__restrict__ aval, const double *__restr
   unsigned long long m[2] = {0ull, 0ull};
   for (int q = 0; q < t.words; q++) m[q] = t.mask[(sl * t.words + q) * 32 + ln];
   const double si = s[i];
-  for (int a = 0; a < t.WA; a++) {
-    const int32_t q = t.asrc[(sl * t.WA + a) * 32 + ln];
-    const double ah = q >= 0 ? __dmul_rn(__dmul_rn(aval[q], si), s[i + soffA[a]]) : 0.0;
-    ahatT[(sl * t.WA + a) * 32 + ln] = ah;
-  }
+  const double *arow = aT + sl * t.WA * 32 + ln;
+  double *hrow = ahatT + sl * t.WA * 32 + ln;
   for (int w = 0; w < t.W; w++) {
     const int a = sw2a[w];
     double v = 0.0;  // fill entries and slots outside S: +0.0
-    if (a >= 0 && tbit(m, w)) {
-      const double ah = ahatT[(sl * t.WA + a) * 32 + ln];
-      v = (w < t.c0) ? __ddiv_rn(ah, ad[i + soff[w]]) : ah;
+    if (a >= 0) {
+      // (a_ij s_i) s_j; A's absent template slots hold 0 and give +0 (never read as S entries)
+      const double ah = tbit(m, w) ? __dmul_rn(__dmul_rn(arow[a * 32], si), s[i + soffA[a]]) : 0.0;
+      hrow[a * 32] = ah;
+      if (tbit(m, w)) v = (w < t.c0) ? __ddiv_rn(ah, ad[i + soff[w]]) : ah;
     }
     vals[(sl * t.W + w) * 32 + ln] = v;
     if (w == t.c0) {
@@ -680,11 +700,11 @@ tsell_init_kernel(TDev t, const double *__restrict__ aval, const double *__restr
   }
 }
 
-cudaError_t launch_tsell_init(const TDev &t, const double *aval, const double *s,
+cudaError_t launch_tsell_init(const TDev &t, const double *aT, const double *s,
                               const double *ad, int64_t r0, int64_t r1, double *ahatT,
                               double *vals, double *udiag, ErrFlags *err, cudaStream_t st) {
   if (r1 <= r0) return cudaSuccess;
-  tsell_init_kernel<<<(unsigned)((r1 - r0 + 255) / 256), 256, 0, st>>>(t, aval, s, ad, r0, r1,
+  tsell_init_kernel<<<(unsigned)((r1 - r0 + 255) / 256), 256, 0, st>>>(t, aT, s, ad, r0, r1,
                                                                        ahatT, vals, udiag, err);
   return cudaGetLastError();
 }
