@@ -81,6 +81,9 @@ typedef struct {
   int64_t global_n;           /* total number of rows over all ranks                        */
   int64_t row_begin;          /* first global row owned by this rank                        */
   int64_t n_lead;             /* rows of A supplied BEFORE row_begin (see create)           */
+  /* ---- options the paper evaluates ---- */
+  double shift;               /* Manteuffel shift alpha >= 0: the factors are computed for     */
+                              /* A' = A + alpha diag(|a_ii|); default 0           */
 } fastilu_options;
 
 /* Fills *opts with the defaults above (single GPU, omega = omega_tri = 1). */

@@ -73,13 +73,14 @@ def lib():
         L.orc_symbolic.argtypes = [C.c_int64, I64P, I32P, C.c_int, C.POINTER(I64P),
                                    C.POINTER(I32P), C.POINTER(I32P), I64P]
         L.orc_free.argtypes = [C.c_void_p]
-        L.orc_scale_init.argtypes = [C.c_int64, I64P, I32P, F64P, I64P, I32P, F64P, F64P, F64P, I64P]
+        L.orc_scale_init.argtypes = [C.c_int64, I64P, I32P, F64P, I64P, I32P, C.c_double, F64P,
+                                     F64P, F64P, I64P]
         L.orc_bad_diagonal.argtypes = [C.c_int64, I64P, I32P, F64P]
         L.orc_bad_diagonal.restype = C.c_int64
         L.orc_sweep.argtypes = [C.c_int64, I64P, I32P, F64P, F64P, F64P, C.c_double, F64P]
         L.orc_sweep.restype = None
         L.orc_compute.argtypes = [C.c_int64, I64P, I32P, F64P, I64P, I32P, C.c_int, C.c_double,
-                                  F64P, F64P, F64P, F64P, I64P]
+                                  C.c_double, F64P, F64P, F64P, F64P, I64P]
         L.orc_exact_ilu.argtypes = [C.c_int64, I64P, I32P, F64P, F64P, I64P]
         for f in ("orc_jacobi_lower", "orc_jacobi_upper"):
             getattr(L, f).argtypes = [C.c_int64, I64P, I32P, F64P, F64P, C.c_int, C.c_double, F64P]
@@ -146,8 +147,8 @@ def symbolic(row_ptr, col_idx, k: int) -> Pattern:
     return Pattern(srp, sci, slev)
 
 
-def scale_init(a, pat: Pattern):
-    """Returns (s, ahat_S, vals0_S) -- readings R4, R5."""
+def scale_init(a, pat: Pattern, shift: float = 0.0):
+    """Returns (s, ahat_S, vals0_S) -- readings R4, R5 (R9: Manteuffel shift)."""
     rp, ci, av = _i64(a.row_ptr), _i32(a.col_idx), _f64(a.values)
     n = a.n
     s = np.empty(n)
@@ -155,8 +156,8 @@ def scale_init(a, pat: Pattern):
     vals = np.empty(pat.nnz)
     bad = C.c_int64(-1)
     st = lib().orc_scale_init(n, _p(rp, I64P), _p(ci, I32P), _p(av, F64P), _p(pat.row_ptr, I64P),
-                              _p(pat.col_idx, I32P), _p(s, F64P), _p(ahat, F64P), _p(vals, F64P),
-                              C.byref(bad))
+                              _p(pat.col_idx, I32P), float(shift), _p(s, F64P), _p(ahat, F64P),
+                              _p(vals, F64P), C.byref(bad))
     if st != 0:
         raise OracleError(st, bad.value)
     return s, ahat, vals
@@ -183,8 +184,10 @@ class Factors:
         self.pattern, self.s, self.ahat, self.vals, self.resid = pat, s, ahat, vals, resid
 
 
-def compute(a, k: int, nsweeps: int, omega: float = 1.0, pat: Pattern | None = None) -> Factors:
-    """Symbolic + scale/init + nsweeps synchronous sweeps (whole FastILU compute)."""
+def compute(a, k: int, nsweeps: int, omega: float = 1.0, pat: Pattern | None = None,
+            shift: float = 0.0) -> Factors:
+    """Symbolic + scale/init + nsweeps synchronous sweeps (whole FastILU compute); shift is the
+    Manteuffel shift of reading R9."""
     if pat is None:
         pat = symbolic(a.row_ptr, a.col_idx, k)
     rp, ci, av = _i64(a.row_ptr), _i32(a.col_idx), _f64(a.values)
@@ -195,7 +198,8 @@ def compute(a, k: int, nsweeps: int, omega: float = 1.0, pat: Pattern | None = N
     hist = np.zeros(max(nsweeps, 1))
     bad = C.c_int64(-1)
     st = lib().orc_compute(n, _p(rp, I64P), _p(ci, I32P), _p(av, F64P), _p(pat.row_ptr, I64P),
-                           _p(pat.col_idx, I32P), int(nsweeps), float(omega), _p(s, F64P),
+                           _p(pat.col_idx, I32P), int(nsweeps), float(omega), float(shift),
+                           _p(s, F64P),
                            _p(ahat, F64P), _p(vals, F64P), _p(hist, F64P), C.byref(bad))
     if st != 0:
         raise OracleError(st, bad.value)

@@ -28,6 +28,9 @@
  *      u_ii.
  *   R7 level-of-fill: sum rule lev(i,j) = min(lev(i,j), lev(i,k)+lev(k,j)+1)
  *      over pivots k < min(i,j) processed in ascending order, keep lev <= K.
+ *   R9 Manteuffel shift alpha >= 0: the factors are those of
+ *      A' = A + alpha diag(|a_ii|), i.e. a'_ii = a_ii + alpha |a_ii| (rounded product, then
+ *      sum); alpha = 0 leaves A unchanged.
  *   R8 zero pivot: FASTILU_ERR_ZERO_PIVOT when any iterate 0..nsweeps has a
  *      diagonal u_ii that is 0 or non-finite; the error index is the smallest
  *      such row over all iterates.
@@ -190,15 +193,21 @@ static int64_t find_in_row(const int64_t *rp, const int32_t *ci, int64_t r,
 /*   s_i = 1/sqrt(|a_ii|);  ahat_ij = (a_ij * s_i) * s_j  (on S, 0 for fill)  */
 /*   vals: l0_ij = ahat_ij / ahat_jj (j < i), u0_ij = ahat_ij (i <= j).       */
 /* ------------------------------------------------------------------------ */
+static double shifted(double aii, double shift) {  /* reading R9 */
+  double t = shift * fabs(aii);
+  return aii + t;
+}
+
 int orc_scale_init(int64_t n, const int64_t *rp, const int32_t *ci,
-                   const double *a, const int64_t *srp, const int32_t *sci,
+                   const double *a, const int64_t *srp, const int32_t *sci, double shift,
                    double *s, double *ahat, double *vals, int64_t *bad) {
   *bad = -1;
   for (int64_t i = 0; i < n; i++) {
     int64_t q = find_in_row(rp, ci, i, (int32_t)i);
     if (q < 0) { *bad = i; return ORC_ERR_MISSING_DIAG; }
-    if (a[q] == 0.0) { *bad = i; return ORC_ERR_ZERO_DIAG; }
-    s[i] = 1.0 / sqrt(fabs(a[q]));
+    double aii = shifted(a[q], shift);
+    if (aii == 0.0) { *bad = i; return ORC_ERR_ZERO_DIAG; }
+    s[i] = 1.0 / sqrt(fabs(aii));
   }
   for (int64_t p = 0; p < srp[n]; p++) ahat[p] = 0.0;
   for (int64_t i = 0; i < n; i++) {
@@ -206,7 +215,8 @@ int orc_scale_init(int64_t n, const int64_t *rp, const int32_t *ci,
       int32_t j = ci[q];
       int64_t p = find_in_row(srp, sci, i, j);
       if (p < 0) return ORC_ERR_BAD_MATRIX; /* S must contain A */
-      ahat[p] = (a[q] * s[i]) * s[j];
+      double aij = (j == i) ? shifted(a[q], shift) : a[q];
+      ahat[p] = (aij * s[i]) * s[j];
     }
   }
   for (int64_t i = 0; i < n; i++) {
@@ -286,9 +296,9 @@ void orc_sweep(int64_t n, const int64_t *srp, const int32_t *sci,
 /* ------------------------------------------------------------------------ */
 int orc_compute(int64_t n, const int64_t *rp, const int32_t *ci,
                 const double *a, const int64_t *srp, const int32_t *sci,
-                int nsweeps, double omega, double *s, double *ahat,
+                int nsweeps, double omega, double shift, double *s, double *ahat,
                 double *vals, double *resid_hist, int64_t *bad) {
-  int st = orc_scale_init(n, rp, ci, a, srp, sci, s, ahat, vals, bad);
+  int st = orc_scale_init(n, rp, ci, a, srp, sci, shift, s, ahat, vals, bad);
   if (st != ORC_OK) return st;
   int64_t nnz = srp[n];
   double *tmp = (double *)malloc(sizeof(double) * (size_t)(nnz > 0 ? nnz : 1));

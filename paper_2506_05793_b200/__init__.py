@@ -39,7 +39,7 @@ class Options(C.Structure):
                 ("stream", C.c_void_p), ("num_threads", C.c_int), ("rank", C.c_int),
                 ("nranks", C.c_int), ("comm_kind", C.c_int), ("nccl_unique_id", C.c_void_p),
                 ("group", C.c_void_p), ("global_n", C.c_int64), ("row_begin", C.c_int64),
-                ("n_lead", C.c_int64)]
+                ("n_lead", C.c_int64), ("shift", C.c_double)]
 
 
 I64P = C.POINTER(C.c_int64)
@@ -209,7 +209,8 @@ class FastILU:
                  omega_tri: float = 1.0, device: int = -1, stream=None, num_threads: int = 0,
                  rank: int = 0, nranks: int = 1, comm_kind: int = COMM_NONE,
                  nccl_unique_id: bytes | None = None, group=None, global_n: int = -1,
-                 row_begin: int = 0, n_lead: int = 0, n: int | None = None):
+                 row_begin: int = 0, n_lead: int = 0, n: int | None = None,
+                 shift: float = 0.0):
         L = lib()
         self._h = H()
         o = fastilu_default_options()
@@ -221,6 +222,7 @@ class FastILU:
         o.nccl_unique_id = C.cast(self._uid, C.c_void_p) if self._uid is not None else None
         o.group = group
         o.global_n, o.row_begin, o.n_lead = int(global_n), int(row_begin), int(n_lead)
+        o.shift = float(shift)
         self._rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
         self._ci = np.ascontiguousarray(col_idx, dtype=np.int32)
         vals = None if values is None else np.ascontiguousarray(values, dtype=np.float64)

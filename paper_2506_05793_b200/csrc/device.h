@@ -60,14 +60,15 @@ struct ErrFlags {
   unsigned long long zero_pivot;  // min local row with u_ii == 0 / non-finite in an iterate
 };
 
+// Manteuffel shift: a_ii' = a_ii + shift |a_ii| (shift = 0: unchanged, bitwise)
 cudaError_t launch_scale(const int64_t *arp, const int32_t *adiag, const double *aval,
                          int64_t r0, int64_t r1, double *s, double *ad, ErrFlags *err,
-                         cudaStream_t st);
+                         double shift, cudaStream_t st);
 
 cudaError_t launch_init(const DevPattern &P, const int64_t *arp, const int32_t *aci,
                         const int32_t *apos, const double *aval, const double *s,
                         const double *ad, int64_t r0, int64_t r1, double *ahatA, double *vals,
-                        double *udiag, ErrFlags *err, int G, cudaStream_t st);
+                        double *udiag, ErrFlags *err, int G, double shift, cudaStream_t st);
 
 // sets the smem attribute and returns the resident blocks per SM for cfg
 cudaError_t sweep_configure(const SweepCfg &cfg, int *blocks_per_sm);
@@ -109,7 +110,8 @@ cudaError_t launch_tsell_gather_a(const TDev &t, const double *aval, int64_t nro
                                   cudaStream_t st);
 cudaError_t launch_tsell_init(const TDev &t, const double *aT, const double *s,
                               const double *ad, int64_t r0, int64_t r1, double *ahatT,
-                              double *vals, double *udiag, ErrFlags *err, cudaStream_t st);
+                              double *vals, double *udiag, ErrFlags *err, double shift,
+                              cudaStream_t st);
 cudaError_t launch_tsell_jacobi(const TDev &t, bool lower, const double *vals,
                                 const double *udiag, const double *rhs, const double *xo,
                                 double *xn, double *xfinal, const double *s, int64_t r0,

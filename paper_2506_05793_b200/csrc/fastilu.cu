@@ -122,6 +122,7 @@ extern "C" void fastilu_default_options(fastilu_options *o) {
   o->global_n = -1;
   o->row_begin = 0;
   o->n_lead = 0;
+  o->shift = 0.0;
 }
 
 extern "C" int64_t fastilu_required_lead_rows(int64_t bandwidth, int level_k) {
@@ -654,7 +655,7 @@ extern "C" fastilu_status fastilu_create(fastilu_handle *out, int64_t n, const i
   if (opts) h->opt = *opts; else fastilu_default_options(&h->opt);
   if (n < 0 || !row_ptr || (n > 0 && !col_idx) || level_k < 0 || level_k > 127 ||
       h->opt.nranks < 1 || !(h->opt.omega > 0.0 && h->opt.omega <= 1.0) ||
-      !(h->opt.omega_tri > 0.0 && h->opt.omega_tri <= 1.0))
+      !(h->opt.omega_tri > 0.0 && h->opt.omega_tri <= 1.0) || !(h->opt.shift >= 0.0))
     FAIL(FASTILU_ERR_INVALID_ARG);
   if (h->opt.device >= 0) {
     if (cudaSetDevice(h->opt.device) != cudaSuccess) return FASTILU_ERR_CUDA;
@@ -708,7 +709,8 @@ static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, i
   const int64_t r0 = h->G, r1 = h->G + h->n;
   CU(cudaEventRecord(h->ev[0], st));
   // a2: scaling for every local row (lower ghosts included), then the upper ghosts' s / ad
-  CU(launch_scale(h->d_arp, h->d_adiag, h->d_aval, 0, h->nloc, h->d_s, h->d_ad, h->d_err, st));
+  CU(launch_scale(h->d_arp, h->d_adiag, h->d_aval, 0, h->nloc, h->d_s, h->d_ad, h->d_err,
+                  h->opt.shift, st));
   if (h->comm) {  // lower ghosts' s / ahat_ii are computed locally from the lead rows of A
     fastilu_status cs = comm_vector_halo(h->comm, h->d_s, st, false, true);
     if (cs) return cs;
@@ -716,10 +718,10 @@ static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, i
   // a3: ahat and the initial guess (iterate 0) for the owned rows
   if (h->tsell)
     CU(launch_tsell_init(tdev(h), h->d_aT, h->d_s, h->d_ad, r0, r1, h->d_ahat, h->d_vals[0],
-                         h->d_ud[0], h->d_err, st));
+                         h->d_ud[0], h->d_err, h->opt.shift, st));
   else
     CU(launch_init(P, h->d_arp, h->d_aci, h->d_apos, h->d_aval, h->d_s, h->d_ad, r0, r1,
-                   h->d_ahat, h->d_vals[0], h->d_ud[0], h->d_err, h->G_init, st));
+                   h->d_ahat, h->d_vals[0], h->d_ud[0], h->d_err, h->G_init, h->opt.shift, st));
   CU(cudaEventRecord(h->ev[1], st));
   double thr2 = -1.0;  // (rtol ||Ahat|_S||_F)^2, tolerance mode only
   std::vector<double> r2tol;

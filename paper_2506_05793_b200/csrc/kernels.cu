@@ -32,10 +32,12 @@ static __device__ __forceinline__ bool bad_pivot(double d) { return !(d != 0.0 &
 // ----------------------------------------------------------------------------------------
 __global__ void scale_kernel(const int64_t *__restrict__ arp, const int32_t *__restrict__ adiag,
                              const double *__restrict__ aval, int64_t r0, int64_t r1,
-                             double *__restrict__ s, double *__restrict__ ad, ErrFlags *err) {
+                             double *__restrict__ s, double *__restrict__ ad, ErrFlags *err,
+                             double shift) {
   for (int64_t r = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < r1;
        r += (int64_t)gridDim.x * blockDim.x) {
-    const double a = aval[arp[r] + adiag[r]];
+    const double a0 = aval[arp[r] + adiag[r]];
+    const double a = __dadd_rn(a0, __dmul_rn(shift, fabs(a0)));  // Manteuffel: a + alpha |a|
     if (a == 0.0) atomicMin(&err->zero_diag, (unsigned long long)r);
     const double si = __ddiv_rn(1.0, __dsqrt_rn(fabs(a)));
     s[r] = si;
@@ -45,11 +47,11 @@ __global__ void scale_kernel(const int64_t *__restrict__ arp, const int32_t *__r
 
 cudaError_t launch_scale(const int64_t *arp, const int32_t *adiag, const double *aval,
                          int64_t r0, int64_t r1, double *s, double *ad, ErrFlags *err,
-                         cudaStream_t st) {
+                         double shift, cudaStream_t st) {
   if (r1 <= r0) return cudaSuccess;
   int64_t blocks = (r1 - r0 + 255) / 256;
   if (blocks > 65535 * 16) blocks = 65535 * 16;
-  scale_kernel<<<(unsigned)blocks, 256, 0, st>>>(arp, adiag, aval, r0, r1, s, ad, err);
+  scale_kernel<<<(unsigned)blocks, 256, 0, st>>>(arp, adiag, aval, r0, r1, s, ad, err, shift);
   return cudaGetLastError();
 }
 
@@ -62,7 +64,7 @@ init_kernel(DevPattern P, const int64_t *__restrict__ arp, const int32_t *__rest
             const int32_t *__restrict__ apos, const double *__restrict__ aval,
             const double *__restrict__ s, const double *__restrict__ ad, int64_t r0, int64_t r1,
             double *__restrict__ ahatA, double *__restrict__ vals, double *__restrict__ udiag,
-            ErrFlags *err) {
+            ErrFlags *err, double shift) {
   auto tile = cg::tiled_partition<G>(cg::this_thread_block());
   const int gpb = blockDim.x / G;
   const int lane = tile.thread_rank();
@@ -75,7 +77,8 @@ init_kernel(DevPattern P, const int64_t *__restrict__ arp, const int32_t *__rest
     for (int64_t q = arp[row] + lane; q < arp[row + 1]; q += G) {
       const int32_t j = aci[q];
       const int64_t p = rb + apos[q];
-      const double ah = __dmul_rn(__dmul_rn(aval[q], si), s[j]);
+      const double av = (j == row) ? __dadd_rn(aval[q], __dmul_rn(shift, fabs(aval[q]))) : aval[q];
+      const double ah = __dmul_rn(__dmul_rn(av, si), s[j]);
       ahatA[q] = ah;
       vals[p] = (j < row) ? __ddiv_rn(ah, ad[j]) : ah;
       if (j == row) {
@@ -90,14 +93,14 @@ init_kernel(DevPattern P, const int64_t *__restrict__ arp, const int32_t *__rest
 cudaError_t launch_init(const DevPattern &P, const int64_t *arp, const int32_t *aci,
                         const int32_t *apos, const double *aval, const double *s,
                         const double *ad, int64_t r0, int64_t r1, double *ahatA, double *vals,
-                        double *udiag, ErrFlags *err, int G, cudaStream_t st) {
+                        double *udiag, ErrFlags *err, int G, double shift, cudaStream_t st) {
   if (r1 <= r0) return cudaSuccess;
   const int threads = 256, gpb = threads / G;
   int64_t blocks = (r1 - r0 + gpb - 1) / gpb;
   if (blocks > (1ll << 30)) blocks = 1ll << 30;
 #define FASTILU_INIT(GG)                                                                   \
   init_kernel<GG><<<(unsigned)blocks, threads, 0, st>>>(P, arp, aci, apos, aval, s, ad, r0, r1, \
-                                                         ahatA, vals, udiag, err)
+                                                         ahatA, vals, udiag, err, shift)
   switch (G) {
     case 4: FASTILU_INIT(4); break;
     case 8: FASTILU_INIT(8); break;
@@ -666,7 +669,7 @@ __global__ void __launch_bounds__(256)
 tsell_init_kernel(TDev t, const double *__restrict__ aT, const double *__restrict__ s,
                   const double *__restrict__ ad, int64_t r0, int64_t r1,
                   double *__restrict__ ahatT, double *__restrict__ vals,
-                  double *__restrict__ udiag, ErrFlags *err) {
+                  double *__restrict__ udiag, ErrFlags *err, double shift) {
   __shared__ int32_t soff[128], soffA[128];
   __shared__ int8_t sw2a[128];
   for (int q = threadIdx.x; q < t.W; q += blockDim.x) {
@@ -688,7 +691,9 @@ tsell_init_kernel(TDev t, const double *__restrict__ aT, const double *__restric
     double v = 0.0;  // fill entries and slots outside S: +0.0
     if (a >= 0) {
       // (a_ij s_i) s_j; A's absent template slots hold 0 and give +0 (never read as S entries)
-      const double ah = tbit(m, w) ? __dmul_rn(__dmul_rn(arow[a * 32], si), s[i + soffA[a]]) : 0.0;
+      double av = arow[a * 32];
+      if (w == t.c0) av = __dadd_rn(av, __dmul_rn(shift, fabs(av)));  // Manteuffel shift
+      const double ah = tbit(m, w) ? __dmul_rn(__dmul_rn(av, si), s[i + soffA[a]]) : 0.0;
       hrow[a * 32] = ah;
       if (tbit(m, w)) v = (w < t.c0) ? __ddiv_rn(ah, ad[i + soff[w]]) : ah;
     }
@@ -702,10 +707,11 @@ tsell_init_kernel(TDev t, const double *__restrict__ aT, const double *__restric
 
 cudaError_t launch_tsell_init(const TDev &t, const double *aT, const double *s,
                               const double *ad, int64_t r0, int64_t r1, double *ahatT,
-                              double *vals, double *udiag, ErrFlags *err, cudaStream_t st) {
+                              double *vals, double *udiag, ErrFlags *err, double shift,
+                              cudaStream_t st) {
   if (r1 <= r0) return cudaSuccess;
-  tsell_init_kernel<<<(unsigned)((r1 - r0 + 255) / 256), 256, 0, st>>>(t, aT, s, ad, r0, r1,
-                                                                       ahatT, vals, udiag, err);
+  tsell_init_kernel<<<(unsigned)((r1 - r0 + 255) / 256), 256, 0, st>>>(
+      t, aT, s, ad, r0, r1, ahatT, vals, udiag, err, shift);
   return cudaGetLastError();
 }
 

@@ -19,8 +19,9 @@ pytestmark = pytest.mark.gpu
 RTOL = 1e-12
 
 
-def gpu_run(a, k, ns, nt=0, b=None, omega=1.0, omega_tri=1.0, alias=False):
-    f = F.FastILU(a.row_ptr, a.col_idx, a.values, k, omega=omega, omega_tri=omega_tri)
+def gpu_run(a, k, ns, nt=0, b=None, omega=1.0, omega_tri=1.0, alias=False, shift=0.0):
+    f = F.FastILU(a.row_ptr, a.col_idx, a.values, k, omega=omega, omega_tri=omega_tri,
+                  shift=shift)
     f.compute(ns)
     vals, s = f.factors()
     x = None
@@ -43,10 +44,10 @@ def assert_rel(g, o, rtol=RTOL, what=""):
     assert err.size == 0 or err.max() <= rtol, f"{what}: max rel err {err.max():.3e} at {i}"
 
 
-def full_check(a, k, ns, nt, omega=1.0, omega_tri=1.0, bitwise=True):
+def full_check(a, k, ns, nt, omega=1.0, omega_tri=1.0, bitwise=True, shift=0.0):
     b = P.rhs_positive(a.n)
-    f, vals, s, x = gpu_run(a, k, ns, nt, b, omega, omega_tri)
-    fo = oracle.compute(a, k, ns, omega)
+    f, vals, s, x = gpu_run(a, k, ns, nt, b, omega, omega_tri, shift=shift)
+    fo = oracle.compute(a, k, ns, omega, shift=shift)
     rp, ci, lev = f.pattern()
     assert np.array_equal(rp, fo.pattern.row_ptr)
     assert np.array_equal(ci, fo.pattern.col_idx)
@@ -119,6 +120,15 @@ def test_random_sparse(seed, k):
 
 def test_damping():
     full_check(P.laplace3d_27pt(9), 1, 4, 5, omega=0.7, omega_tri=0.8)
+
+
+@pytest.mark.parametrize("path", ["tsell", "csr"])
+def test_manteuffel_shift(path, monkeypatch):
+    """Option 'Shift' (reading R9) on both layouts."""
+    if path == "csr":
+        monkeypatch.setenv("FASTILU_NO_TSELL", "1")
+    f = full_check(P.laplace3d_27pt(10), 1, 3, 4, shift=0.25)
+    assert f.info().startswith(f"path={path}")
 
 
 @pytest.mark.parametrize("nt", [1, 2])

@@ -347,3 +347,19 @@ def test_windowed_equals_global_interior():
             assert np.array_equal(fg.pattern.col_idx[gi], fw.pattern.col_idx[wi] + lo)
             assert np.array_equal(fg.vals[gi], fw.vals[wi])
         assert np.array_equal(xg[z * plane:(z + 1) * plane], xw[z * plane - lo:(z + 1) * plane - lo])
+
+
+# ----------------------------------------------------------------------------- Manteuffel shift
+def test_shift_is_factoring_the_shifted_matrix():
+    """Reading R9: compute with shift alpha == compute on
+    A' = A + alpha diag(|a_ii|) built explicitly here (bitwise); alpha = 0 changes nothing."""
+    a = P.laplace3d_27pt(5)
+    alpha = 0.3
+    v = a.values.copy()
+    rows = np.repeat(np.arange(a.n), np.diff(a.row_ptr))
+    d = a.col_idx == rows
+    v[d] = v[d] + alpha * np.abs(v[d])
+    f1 = oracle.compute(a, 1, 3, shift=alpha)
+    f2 = oracle.compute(P.Csr(a.row_ptr, a.col_idx, v), 1, 3)
+    assert np.array_equal(f1.vals, f2.vals) and np.array_equal(f1.s, f2.s)
+    assert np.array_equal(oracle.compute(a, 1, 3, shift=0.0).vals, oracle.compute(a, 1, 3).vals)
