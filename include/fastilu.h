@@ -121,6 +121,13 @@ fastilu_status fastilu_set_values_device(fastilu_handle h, const double *values_
  * Returns ZERO_DIAG / ZERO_PIVOT with the row in fastilu_error_index. */
 fastilu_status fastilu_compute(fastilu_handle h, int nsweeps);
 
+/* Option "Warm up": FastILU(0), FastILU(1), ..., FastILU(k), each with nsweeps
+ * sweeps, the factors of level L-1 initialising the entries of S_{L-1} inside S_L (new fill
+ * entries start at +0.0; level 0 starts from the usual initial guess).  The residual history
+ * has nsweeps (k+1) entries.  Template-SELL layout only (FASTILU_ERR_UNSUPPORTED otherwise
+ * when k > 0). */
+fastilu_status fastilu_compute_warmup(fastilu_handle h, int nsweeps);
+
 /* "Sweeps to convergence" (BASELINE config 3; reading G15): like fastilu_compute but
  * stops after the first sweep s whose by-product residual of iterate s-1 satisfies
  * r(s-1) = ||(Ahat - L U)|_S||_F <= rtol ||Ahat|_S||_F, or after max_sweeps.  The factors are

@@ -222,6 +222,32 @@ def compute_tol(a, k: int, rtol: float, max_sweeps: int = 100, omega: float = 1.
     return Factors(pat, s, ahat, vals, np.array(hist)), sw
 
 
+def compute_warmup(a, k: int, nsweeps: int, omega: float = 1.0, shift: float = 0.0):
+    """Option "Warm up" (PAPER.md:721; DESIGN.md R10): FastILU(L) for L = 0..k, nsweeps each;
+    the factors of level L-1 initialise the entries of S_{L-1} inside S_L, new fill entries
+    start at +0.0, level 0 starts from the initial guess (R4).  Residual history concatenated."""
+    hist = []
+    prev = None
+    for L in range(k + 1):
+        pat = symbolic(a.row_ptr, a.col_idx, L)
+        s, ahat, vals = scale_init(a, pat, shift)
+        if prev is not None:
+            ppat, pvals = prev
+            key = np.repeat(np.arange(pat.n, dtype=np.int64), np.diff(pat.row_ptr)) * pat.n \
+                + pat.col_idx
+            pkey = np.repeat(np.arange(ppat.n, dtype=np.int64), np.diff(ppat.row_ptr)) * ppat.n \
+                + ppat.col_idx
+            pos = np.searchsorted(key, pkey)
+            assert np.array_equal(key[pos], pkey)  # S_{L-1} is contained in S_L
+            vals = np.zeros(pat.nnz)
+            vals[pos] = pvals
+        for _ in range(nsweeps):
+            vals, r = sweep(pat, ahat, vals, omega)
+            hist.append(r)
+        prev = (pat, vals)
+    return Factors(pat, s, ahat, vals, np.array(hist))
+
+
 def exact_ilu(pat: Pattern, ahat):
     ahat = _f64(ahat)
     vals = np.empty_like(ahat)

@@ -57,6 +57,7 @@ _SIGS = {
     "fastilu_set_values_device": (C.c_int, [H, C.c_void_p]),
     "fastilu_compute": (C.c_int, [H, C.c_int]),
     "fastilu_compute_tol": (C.c_int, [H, C.c_double, C.c_int, C.POINTER(C.c_int)]),
+    "fastilu_compute_warmup": (C.c_int, [H, C.c_int]),
     "fastilu_apply": (C.c_int, [H, C.c_void_p, C.c_void_p, C.c_int]),
     "fastilu_apply_host": (C.c_int, [H, F64P, F64P, C.c_int]),
     "fastilu_destroy": (C.c_int, [H]),
@@ -251,6 +252,11 @@ class FastILU:
 
     def compute(self, nsweeps: int):
         _check(lib().fastilu_compute(self._h, int(nsweeps)), "fastilu_compute", self._h)
+
+    def compute_warmup(self, nsweeps: int):
+        """Warm-up option: FastILU(0..k) with nsweeps each (fastilu_compute_warmup)."""
+        _check(lib().fastilu_compute_warmup(self._h, int(nsweeps)), "fastilu_compute_warmup",
+               self._h)
 
     def compute_tol(self, rtol: float, max_sweeps: int = 100) -> int:
         """Sweeps until r(s-1) <= rtol ||Ahat|_S||_F (or max_sweeps); returns s."""

@@ -72,6 +72,7 @@ struct fastilu_handle_s {
   unsigned long long *d_tmask = nullptr;
   unsigned int *d_counter = nullptr;
   double *d_aT = nullptr;  // A's values in template slots (refreshed by set_values)
+  std::vector<unsigned long long *> d_lmask;  // warm-up: presence masks of levels 0..K-1
   void *jit_sweep = nullptr;
   int t_threads = 128, t_grid = 1, t_regs = 0, t_spill = 0, t_rows_tile = 128;
   int64_t t_ntiles = 0;
@@ -555,6 +556,17 @@ static fastilu_status create_impl(fastilu_handle h, int64_t n, const int64_t *ro
       if (ts == FASTILU_OK) h->tsell = true;
       else if (multi || ts != FASTILU_ERR_UNSUPPORTED) return ts;
     }
+    if (h->tsell && K > 0) {  // nested level masks for the warm-up option
+      std::vector<int8_t> llev(pat.lev.begin() + s_base, pat.lev.begin() + s_base + h->nnz_loc);
+      for (int L = 0; L < K; L++) {
+        std::vector<unsigned long long> lm;
+        level_mask(rp, ci, llev, h->nloc, h->T, L, nt, lm);
+        unsigned long long *d = nullptr;
+        CU(dalloc(&d, (int64_t)lm.size()));
+        CU(cudaMemcpy(d, lm.data(), 8 * lm.size(), cudaMemcpyHostToDevice));
+        h->d_lmask.push_back(d);
+      }
+    }
   }
   // structure classes for the class-program sweep (falls back to the hash kernel if absent)
   ClassProgram cp;
@@ -688,8 +700,14 @@ extern "C" fastilu_status fastilu_set_values_device(fastilu_handle h, const doub
 // --------------------------------------------------------------------------- compute
 // nsweeps synchronous sweeps; with rtol > 0, stop after the first sweep s whose residual of
 // iterate s-1 satisfies r(s-1) <= rtol ||Ahat|_S||_F (reading G15), at most nsweeps.
-static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, int *done) {
+static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, int *done,
+                                   bool warmup = false) {
   if (!h || nsweeps < 0) FAIL(FASTILU_ERR_INVALID_ARG);
+  const int per_level = nsweeps;
+  if (warmup) {  // FastILU(0), ..., FastILU(K) with nsweeps each
+    if (!h->tsell && h->K > 0) FAIL(FASTILU_ERR_UNSUPPORTED);
+    nsweeps = per_level * (h->K + 1);
+  }
   if (!h->have_values || !h->d_aval) FAIL(FASTILU_ERR_STATE);
   cudaSetDevice(h->device);
   h->computed = false;
@@ -771,6 +789,10 @@ static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, i
       const double *old = h->d_vals[ib], *ahat = h->d_ahat, *udo = h->d_ud[ib];
       double *outp = h->d_vals[ob], *udn = h->d_ud[ob], *part = h->d_partials;
       const unsigned long long *mk = h->d_tmask;
+      if (warmup && per_level > 0) {
+        const int lvl = (sw - 1) / per_level;
+        if (lvl < h->K) mk = h->d_lmask[lvl];
+      }
       long long a0 = r0, a1 = r1;
       double om = h->opt.omega;
       unsigned long long *zp = &h->d_err->zero_pivot;
@@ -824,6 +846,10 @@ static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, i
 
 extern "C" fastilu_status fastilu_compute(fastilu_handle h, int nsweeps) {
   return compute_impl(h, nsweeps, 0.0, nullptr);
+}
+
+extern "C" fastilu_status fastilu_compute_warmup(fastilu_handle h, int nsweeps) {
+  return compute_impl(h, nsweeps, 0.0, nullptr, true);
 }
 
 extern "C" fastilu_status fastilu_compute_tol(fastilu_handle h, double rtol, int max_sweeps,
@@ -1150,6 +1176,7 @@ extern "C" fastilu_status fastilu_destroy(fastilu_handle h) {
   if (h->h_err) cudaFreeHost(h->h_err);
   if (h->h_r2) cudaFreeHost(h->h_r2);
   if (h->gm_hbuf) cudaFreeHost(h->gm_hbuf);
+  for (auto *p : h->d_lmask) cudaFree(p);
   for (int i = 0; i < 5; i++)
     if (h->ev[i]) cudaEventDestroy(h->ev[i]);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);

@@ -131,6 +131,17 @@ def test_manteuffel_shift(path, monkeypatch):
     assert f.info().startswith(f"path={path}")
 
 
+@pytest.mark.parametrize("kind,g,k", [("27pt", 10, 2), ("27pt", 9, 1), ("7pt", 12, 2)])
+def test_warmup(kind, g, k):
+    """Option 'Warm up' (reading R10): bitwise equal to the oracle's warm-up."""
+    a = P.make(kind, g)
+    f = F.FastILU(a.row_ptr, a.col_idx, a.values, k)
+    f.compute_warmup(2)
+    fo = oracle.compute_warmup(a, k, 2)
+    assert np.array_equal(f.factors()[0], fo.vals)
+    np.testing.assert_allclose(f.residual_history(), fo.resid, rtol=1e-11)
+
+
 @pytest.mark.parametrize("nt", [1, 2])
 def test_few_trisweeps(nt):
     full_check(P.laplace3d_7pt(12), 0, 2, nt)

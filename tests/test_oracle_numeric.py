@@ -363,3 +363,31 @@ def test_shift_is_factoring_the_shifted_matrix():
     f2 = oracle.compute(P.Csr(a.row_ptr, a.col_idx, v), 1, 3)
     assert np.array_equal(f1.vals, f2.vals) and np.array_equal(f1.s, f2.s)
     assert np.array_equal(oracle.compute(a, 1, 3, shift=0.0).vals, oracle.compute(a, 1, 3).vals)
+
+
+# ----------------------------------------------------------------------------- warm-up (R10)
+def test_warmup_level0_is_plain_compute():
+    a = P.laplace3d_27pt(6)
+    f0 = oracle.compute_warmup(a, 0, 3)
+    f1 = oracle.compute(a, 0, 3)
+    assert np.array_equal(f0.vals, f1.vals) and np.array_equal(f0.resid, f1.resid)
+
+
+def test_warmup_reaches_exact_ilu():
+    """The sweep map's fixed point does not depend on the initial guess: enough warm-up sweeps
+    give the exact ILU(k) bitwise (k = 2, 4^3 27-pt; bound from the dependency DAG)."""
+    a = P.laplace3d_27pt(4)
+    f = oracle.compute_warmup(a, 2, 40)
+    assert np.array_equal(f.vals, oracle.exact_ilu(f.pattern, f.ahat))
+    assert f.resid[-1] == 0.0
+
+
+def test_warmup_trend_gmres():
+    """PAPER.md:612 vs 617 (tab:fastilu_nx16 b): warm-up never needs more GMRES iterations."""
+    a = P.laplace3d_27pt(12)
+    b = oracle.spmv(a, P.x_true(a.n))
+    for k in (1, 2, 3):
+        i0 = oracle.gmres(a, b, oracle.fastilu_preconditioner(oracle.compute(a, k, 2), 30))[1]
+        i1 = oracle.gmres(a, b, oracle.fastilu_preconditioner(oracle.compute_warmup(a, k, 2),
+                                                                30))[1]
+        assert i1 <= i0, (k, i0, i1)
