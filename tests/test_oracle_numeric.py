@@ -379,7 +379,7 @@ def test_warmup_reaches_exact_ilu():
     a = P.laplace3d_27pt(4)
     f = oracle.compute_warmup(a, 2, 40)
     assert np.array_equal(f.vals, oracle.exact_ilu(f.pattern, f.ahat))
-    assert f.resid[-1] == 0.0
+    assert f.resid[-1] <= 1e-15  # the defect a - l u_jj keeps one rounding at the fixed point
 
 
 def test_warmup_trend_gmres():
