@@ -343,10 +343,9 @@ static fastilu_status setup_tsell(fastilu_handle h, const std::vector<unsigned l
   const char *ev_th = std::getenv("FASTILU_TSELL_THREADS");
   const char *ev_pa = std::getenv("FASTILU_TSELL_PARTS");
   const char *ev_mb = std::getenv("FASTILU_TSELL_MINB");
-  const int threads = ev_th ? std::max(32, atoi(ev_th) / 32 * 32) : 128;
-  // targets per warp: ~32 accumulators per thread (63 -> 2 parts, 115 -> 4 parts)
-  int parts = std::max(1, (T.W + 35) / 36);
-  if (parts == 3) parts = 4;
+  const int threads = ev_th ? std::max(32, atoi(ev_th) / 32 * 32) : 256;
+  // targets split over 2 warps per row (measured best for W = 63 and 115, profiles/r1*)
+  int parts = T.W > 16 ? 2 : 1;
   if (ev_pa) parts = std::max(1, atoi(ev_pa));
   const int minb = ev_mb ? atoi(ev_mb) : 0;
   std::string log;
