@@ -121,6 +121,12 @@ fastilu_status fastilu_set_values_device(fastilu_handle h, const double *values_
  * Returns ZERO_DIAG / ZERO_PIVOT with the row in fastilu_error_index. */
 fastilu_status fastilu_compute(fastilu_handle h, int nsweeps);
 
+/* The paper's asynchronous in-place sweeps: every thread updates its entries in
+ * place, reading whatever mix of old and already-updated values it finds (Gauss-Seidel-like,
+ * non-deterministic; same fixed point).  The residual history is the by-product of those
+ * mixed reads.  Template-SELL layout, single GPU (FASTILU_ERR_UNSUPPORTED otherwise). */
+fastilu_status fastilu_compute_async(fastilu_handle h, int nsweeps);
+
 /* Option "Warm up": FastILU(0), FastILU(1), ..., FastILU(k), each with nsweeps
  * sweeps, the factors of level L-1 initialising the entries of S_{L-1} inside S_L (new fill
  * entries start at +0.0; level 0 starts from the usual initial guess).  The residual history

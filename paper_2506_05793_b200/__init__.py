@@ -58,6 +58,7 @@ _SIGS = {
     "fastilu_compute": (C.c_int, [H, C.c_int]),
     "fastilu_compute_tol": (C.c_int, [H, C.c_double, C.c_int, C.POINTER(C.c_int)]),
     "fastilu_compute_warmup": (C.c_int, [H, C.c_int]),
+    "fastilu_compute_async": (C.c_int, [H, C.c_int]),
     "fastilu_apply": (C.c_int, [H, C.c_void_p, C.c_void_p, C.c_int]),
     "fastilu_apply_host": (C.c_int, [H, F64P, F64P, C.c_int]),
     "fastilu_destroy": (C.c_int, [H]),
@@ -252,6 +253,11 @@ class FastILU:
 
     def compute(self, nsweeps: int):
         _check(lib().fastilu_compute(self._h, int(nsweeps)), "fastilu_compute", self._h)
+
+    def compute_async(self, nsweeps: int):
+        """The paper's asynchronous in-place sweeps (non-deterministic; fastilu_compute_async)."""
+        _check(lib().fastilu_compute_async(self._h, int(nsweeps)), "fastilu_compute_async",
+               self._h)
 
     def compute_warmup(self, nsweeps: int):
         """Warm-up option: FastILU(0..k) with nsweeps each (fastilu_compute_warmup)."""

@@ -74,6 +74,8 @@ struct fastilu_handle_s {
   double *d_aT = nullptr;  // A's values in template slots (refreshed by set_values)
   std::vector<unsigned long long *> d_lmask;  // warm-up: presence masks of levels 0..K-1
   void *jit_sweep = nullptr;
+  void *jit_sweep_async = nullptr;  // compiled on the first asynchronous compute
+  int t_parts = 1, t_minb = 0;
   int t_threads = 128, t_grid = 1, t_regs = 0, t_spill = 0, t_rows_tile = 128;
   int64_t t_ntiles = 0;
   // GMRES workspace (allocated on first use)
@@ -361,6 +363,8 @@ static fastilu_status setup_tsell(fastilu_handle h, const std::vector<unsigned l
             T.c0, T.WA, T.terms.size(), h->t_regs, h->t_spill, bps);
   if (bps < 1) FAIL(FASTILU_ERR_UNSUPPORTED);
   h->t_threads = threads;
+  h->t_parts = parts;
+  h->t_minb = minb;
   h->t_rows_tile = sweep_rows_per_tile(threads, parts);
   h->t_ntiles = std::max<int64_t>(1, (h->n + h->t_rows_tile - 1) / h->t_rows_tile);
   h->t_grid = (int)std::min<int64_t>((int64_t)sm_count(h->device) * bps, h->t_ntiles);
@@ -700,8 +704,17 @@ extern "C" fastilu_status fastilu_set_values_device(fastilu_handle h, const doub
 // nsweeps synchronous sweeps; with rtol > 0, stop after the first sweep s whose residual of
 // iterate s-1 satisfies r(s-1) <= rtol ||Ahat|_S||_F (reading G15), at most nsweeps.
 static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, int *done,
-                                   bool warmup = false) {
+                                   bool warmup = false, bool async = false) {
   if (!h || nsweeps < 0) FAIL(FASTILU_ERR_INVALID_ARG);
+  if (async) {  // in-place variant of the template kernel (single GPU)
+    if (!h->tsell || h->comm) FAIL(FASTILU_ERR_UNSUPPORTED);
+    if (!h->jit_sweep_async) {
+      std::string log;
+      const std::string src = sweep_source(h->T, h->t_threads, h->t_parts, h->t_minb, true);
+      if (jit_get(src, "fastilu_tsell_sweep_async", h->device, &h->jit_sweep_async, &log))
+        FAIL(FASTILU_ERR_UNSUPPORTED);
+    }
+  }
   const int per_level = nsweeps;
   if (warmup) {  // FastILU(0), ..., FastILU(K) with nsweeps each
     if (!h->tsell && h->K > 0) FAIL(FASTILU_ERR_UNSUPPORTED);
@@ -760,6 +773,7 @@ static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, i
   // a4/a5: nsweeps synchronous sweeps, ping-pong buffers
   for (int sw = 1; sw <= nsweeps; sw++) {
     executed = sw;
+    const int ib_async = 0;  // asynchronous sweeps stay in buffer 0 (in place)
     if (thr2 >= 0.0 && sw > 1) {  // r(sw-2) of the previous sweep decides whether to go on
       CU(cudaMemcpyAsync(h->h_r2 + (sw - 2), h->d_r2 + (sw - 2), sizeof(double),
                          cudaMemcpyDeviceToHost, st));
@@ -776,7 +790,7 @@ static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, i
         break;
       }
     }
-    const int ib = (sw - 1) & 1, ob = sw & 1;
+    const int ib = async ? ib_async : (sw - 1) & 1, ob = async ? ib_async : sw & 1;
     if (h->comm) {
       fastilu_status cs = comm_factor_halo(h->comm, h->d_vals[ib], h->d_rp, h->d_ud[ib], st);
       if (cs) return cs;
@@ -797,7 +811,9 @@ static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, i
       unsigned long long *zp = &h->d_err->zero_pivot;
       unsigned int *ctr = h->d_counter;
       void *args[] = {&old, &outp, &ahat, &mk, &udo, &udn, &a0, &a1, &om, &part, &zp, &ctr};
-      if (jit_launch(h->jit_sweep, h->t_grid, h->t_threads, st, args)) return FASTILU_ERR_CUDA;
+      if (jit_launch(async ? h->jit_sweep_async : h->jit_sweep, h->t_grid, h->t_threads, st,
+                     args))
+        return FASTILU_ERR_CUDA;
       CU(launch_reduce_reset(h->d_partials, (int)h->t_ntiles, h->d_r2 + (sw - 1), h->d_counter,
                              st));
       continue;
@@ -830,7 +846,7 @@ static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, i
   }
   for (size_t q = 0; q < r2tol.size() && q < r2.size(); q++) r2[q] = r2tol[q];
   for (int i = 0; i < nsweeps; i++) h->resid[i] = std::sqrt(r2[i]);
-  h->cur = nsweeps & 1;
+  h->cur = async ? 0 : (nsweeps & 1);
   if (ef.zero_diag != ~0ull) {
     h->err_index = (int64_t)ef.zero_diag;
     return FASTILU_ERR_ZERO_DIAG;
@@ -845,6 +861,10 @@ static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, i
 
 extern "C" fastilu_status fastilu_compute(fastilu_handle h, int nsweeps) {
   return compute_impl(h, nsweeps, 0.0, nullptr);
+}
+
+extern "C" fastilu_status fastilu_compute_async(fastilu_handle h, int nsweeps) {
+  return compute_impl(h, nsweeps, 0.0, nullptr, false, true);
 }
 
 extern "C" fastilu_status fastilu_compute_warmup(fastilu_handle h, int nsweeps) {

@@ -248,3 +248,32 @@ def test_errors():
 def test_config2_full_size_7pt_128_ilu0():
     """BASELINE configs[1] at full size (n = 2,097,152), element by element."""
     full_check(P.laplace3d_7pt(128), 0, 3, 5)
+
+
+# ------------------------------------------------------------ asynchronous in-place sweeps
+def test_async_reaches_the_fixed_point():
+    """in-place (asynchronous) sweeps are non-deterministic but share the
+    synchronous sweeps' fixed point: after enough sweeps the factors equal the exact ILU(k)."""
+    a = P.laplace3d_27pt(8)
+    f = F.FastILU(a.row_ptr, a.col_idx, a.values, 1)
+    f.compute_async(80)
+    pat = oracle.symbolic(a.row_ptr, a.col_idx, 1)
+    _, ahat, _ = oracle.scale_init(a, pat)
+    np.testing.assert_allclose(f.factors()[0], oracle.exact_ilu(pat, ahat), rtol=1e-13,
+                               atol=1e-15)
+
+
+def test_async_quality_vs_synchronous():
+    """Gauss-Seidel-like updates: the defect ||(Ahat - LU)|_S|| of the factors after two
+    asynchronous sweeps (evaluated by the oracle) is not worse than after two synchronous ones."""
+    a = P.laplace3d_27pt(16)
+    f = F.FastILU(a.row_ptr, a.col_idx, a.values, 1)
+    f.compute_async(2)
+    va = f.factors()[0]
+    f.compute(2)
+    vs = f.factors()[0]
+    pat = oracle.symbolic(a.row_ptr, a.col_idx, 1)
+    _, ahat, _ = oracle.scale_init(a, pat)
+    ra = oracle.sweep(pat, ahat, va)[1]
+    rs = oracle.sweep(pat, ahat, vs)[1]
+    assert ra <= rs * 1.05, (ra, rs)
