@@ -76,6 +76,7 @@ struct fastilu_handle_s {
   void *jit_sweep = nullptr;
   void *jit_sweep_async = nullptr;  // compiled on the first asynchronous compute
   int t_parts = 1, t_minb = 0;
+  bool t_prefetch = true;
   int t_threads = 128, t_grid = 1, t_regs = 0, t_spill = 0, t_rows_tile = 128;
   int64_t t_ntiles = 0;
   // GMRES workspace (allocated on first use)
@@ -349,9 +350,13 @@ static fastilu_status setup_tsell(fastilu_handle h, const std::vector<unsigned l
   // targets split over 2 warps per row (measured best for W = 63 and 115, profiles/r1*)
   int parts = T.W > 16 ? 2 : 1;
   if (ev_pa) parts = std::max(1, atoi(ev_pa));
-  const int minb = ev_mb ? atoi(ev_mb) : 0;
+  // keep two 256-thread blocks per SM for templates whose accumulators fit 128 registers
+  const int minb = ev_mb ? atoi(ev_mb) : (threads == 256 && T.W <= 72 ? 2 : 0);
   std::string log;
-  const std::string src = sweep_source(T, threads, parts, minb);
+  const bool pf = !(std::getenv("FASTILU_TSELL_PREFETCH") &&
+                    atoi(std::getenv("FASTILU_TSELL_PREFETCH")) == 0);
+  h->t_prefetch = pf;
+  const std::string src = sweep_source(T, threads, parts, minb, false, pf);
   if (jit_get(src, "fastilu_tsell_sweep", h->device, &h->jit_sweep, &log)) {
     if (std::getenv("FASTILU_DEBUG")) fprintf(stderr, "fastilu: JIT failed: %s\n", log.c_str());
     FAIL(FASTILU_ERR_UNSUPPORTED);
@@ -710,7 +715,8 @@ static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, i
     if (!h->tsell || h->comm) FAIL(FASTILU_ERR_UNSUPPORTED);
     if (!h->jit_sweep_async) {
       std::string log;
-      const std::string src = sweep_source(h->T, h->t_threads, h->t_parts, h->t_minb, true);
+      const std::string src =
+          sweep_source(h->T, h->t_threads, h->t_parts, h->t_minb, true, h->t_prefetch);
       if (jit_get(src, "fastilu_tsell_sweep_async", h->device, &h->jit_sweep_async, &log))
         FAIL(FASTILU_ERR_UNSUPPORTED);
     }
