@@ -370,8 +370,8 @@ static fastilu_status setup_tsell(fastilu_handle h, const std::vector<unsigned l
   h->t_threads = threads;
   h->t_parts = parts;
   h->t_minb = minb;
-  h->t_rows_tile = 32;
-  h->t_ntiles = std::max<int64_t>(1, sweep_items(h->n, parts));  // work items (slice, part)
+  h->t_rows_tile = sweep_rows_per_tile(threads, parts);
+  h->t_ntiles = std::max<int64_t>(1, (h->n + h->t_rows_tile - 1) / h->t_rows_tile);
   h->t_grid = (int)std::min<int64_t>((int64_t)sm_count(h->device) * bps, h->t_ntiles);
   const int64_t nv = h->nsl * T.W * 32;
   for (int b = 0; b < 2; b++) {
@@ -1169,9 +1169,9 @@ extern "C" fastilu_status fastilu_get_info(fastilu_handle h, char *buf, int cap)
   char tmp[512];
   if (h->tsell)
     snprintf(tmp, sizeof(tmp),
-             "path=tsell W=%d c0=%d WA=%d terms=%zu threads=%d parts=%d grid=%d regs=%d "
-             "local=%d items=%lld G=%lld H=%lld",
-             h->T.W, h->T.c0, h->T.WA, h->T.terms.size(), h->t_threads, h->t_parts,
+             "path=tsell W=%d c0=%d WA=%d terms=%zu threads=%d rows/tile=%d grid=%d regs=%d "
+             "local=%d tiles=%lld G=%lld H=%lld",
+             h->T.W, h->T.c0, h->T.WA, h->T.terms.size(), h->t_threads, h->t_rows_tile,
              h->t_grid, h->t_regs,
              h->t_spill, (long long)h->t_ntiles, (long long)h->G, (long long)h->H);
   else
