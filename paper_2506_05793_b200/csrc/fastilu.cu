@@ -72,6 +72,10 @@ struct fastilu_handle_s {
   unsigned long long *d_tmask = nullptr;
   unsigned int *d_counter = nullptr;
   double *d_aT = nullptr;  // A's values in template slots (refreshed by set_values)
+  // fused multi-sweep trisolve (template path, single GPU)
+  double *d_tribuf = nullptr;
+  unsigned int *d_triws = nullptr;
+  int tri_cap = 0, tri_grid = 0;
   std::vector<unsigned long long *> d_lmask;  // warm-up: presence masks of levels 0..K-1
   void *jit_sweep = nullptr;
   void *jit_sweep_async = nullptr;  // compiled on the first asynchronous compute
@@ -353,8 +357,9 @@ static fastilu_status setup_tsell(fastilu_handle h, const std::vector<unsigned l
   // keep two 256-thread blocks per SM for templates whose accumulators fit 128 registers
   const int minb = ev_mb ? atoi(ev_mb) : (threads == 256 && T.W <= 72 ? 2 : 0);
   std::string log;
-  const bool pf = !(std::getenv("FASTILU_TSELL_PREFETCH") &&
-                    atoi(std::getenv("FASTILU_TSELL_PREFETCH")) == 0);
+  // L2 prefetch of the next tile: measured slower at 256^3 (profiles/r1*), off by default
+  const bool pf = std::getenv("FASTILU_TSELL_PREFETCH") &&
+                  atoi(std::getenv("FASTILU_TSELL_PREFETCH")) != 0;
   h->t_prefetch = pf;
   const std::string src = sweep_source(T, threads, parts, minb, false, pf);
   if (jit_get(src, "fastilu_tsell_sweep", h->device, &h->jit_sweep, &log)) {
@@ -884,8 +889,44 @@ extern "C" fastilu_status fastilu_compute_tol(fastilu_handle h, double rtol, int
 }
 
 // --------------------------------------------------------------------------- apply
+static fastilu_status apply_fused(fastilu_handle h, const double *b, double *x, int ntri) {
+  cudaStream_t st = h->stream;
+  if (ntri > h->tri_cap) {
+    if (h->d_tribuf) cudaFree(h->d_tribuf);
+    if (h->d_triws) cudaFree(h->d_triws);
+    h->d_tribuf = nullptr;
+    h->d_triws = nullptr;
+    CU(dalloc(&h->d_tribuf, (int64_t)2 * ntri * h->E));
+    CU(cudaMemset(h->d_tribuf, 0, sizeof(double) * 2 * ntri * h->E));
+    const size_t ws = tsell_trisolve_ws_bytes(ntri, h->n);
+    CU(cudaMalloc((void **)&h->d_triws, ws));
+    h->tri_cap = ntri;
+    if (!h->tri_grid) {  // resident capacity: blocks wait on each other
+      int bps = 0;
+      CU(tsell_trisolve_occupancy(&bps));
+      h->tri_grid = std::max(1, sm_count(h->device) * bps);
+    }
+  }
+  const int64_t r0 = h->G, r1 = h->G + h->n;
+  const int64_t ntiles = (h->n + 255) / 256;
+  const int grid = (int)std::min<int64_t>(h->tri_grid, ntiles);
+  const double om = h->opt.omega_tri;
+  const double *vals = h->d_vals[h->cur], *ud = h->d_ud[h->cur];
+  double *zb = h->d_tribuf, *wb = h->d_tribuf + (int64_t)ntri * h->E;
+  // y = s o b into d_y (the L solve's right-hand side)
+  CU(launch_trisolve_first_L(b, h->d_s, h->d_y, zb, r0, r1, h->G, 1.0, st));
+  CU(launch_tsell_trisolve_fused(tdev(h), true, false, ntri, vals, nullptr, h->d_y, h->d_s, zb,
+                                 nullptr, r0, r1, h->E, h->G, om, h->d_triws, grid, st));
+  const double *zf = zb + (int64_t)(ntri - 1) * h->E;
+  CU(launch_tsell_trisolve_fused(tdev(h), false, true, ntri, vals, ud, zf, h->d_s, wb, x, r0, r1,
+                                 h->E, h->G, om, h->d_triws, grid, st));
+  return FASTILU_OK;
+}
+
 static fastilu_status apply_impl(fastilu_handle h, const double *b, double *x, int ntri) {
   cudaStream_t st = h->stream;
+  if (h->tsell && !h->comm && !std::getenv("FASTILU_NO_FUSED_TRISOLVE"))
+    return apply_fused(h, b, x, ntri);
   DevPattern P{h->d_rp, h->d_ci, h->d_dloc};
   const int64_t r0 = h->G, r1 = h->G + h->n;
   const double om = h->opt.omega_tri;
@@ -1195,7 +1236,8 @@ extern "C" fastilu_status fastilu_destroy(fastilu_handle h) {
                   h->d_w[0],  h->d_w[1],  h->d_bx,       h->d_partials, h->d_r2,  h->d_err,
                   h->d_rclass, h->d_coff, h->d_caoff, h->d_prog, h->d_toff, h->d_toffA,
                   h->d_tasrc, h->d_tw2a, h->d_tmask, h->d_counter, h->gm_V, h->gm_w,
-                  h->gm_ext, h->gm_u, h->gm_r, h->gm_part, h->gm_c, h->d_aT};
+                  h->gm_ext, h->gm_u, h->gm_r, h->gm_part, h->gm_c, h->d_aT, h->d_tribuf,
+                  h->d_triws};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   if (h->h_err) cudaFreeHost(h->h_err);
