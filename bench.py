@@ -55,44 +55,67 @@ def peaks():
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    """nvidia-smi sampling (B200_PROFILING.md clocks line).  Started before the warm-up (the tool
+    needs ~0.3 s to start); samples carry wall-clock stamps and only those inside the timed
+    window [mark_start, mark_stop] are summarised (all samples if the window caught < 3)."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, dev):
-        self.dev = dev
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.t0 = self.t1 = None
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(dev), f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "100"],
-                                      stdout=self.f, stderr=subprocess.DEVNULL)
+                                       "--format=csv,noheader,nounits", "-lms", "50"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                                      text=True, bufsize=1)
+            import threading
+            self.rows = []
+            self.th = threading.Thread(target=self._reader, daemon=True)
+            self.th.start()
         except Exception:
             self.p = None
+
+    def _reader(self):
+        for line in self.p.stdout:
+            self.rows.append((time.time(), line.strip()))
+
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_stop(self):
+        self.t1 = time.time()
 
     def stop(self):
         if self.p is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.12)
         self.p.terminate()
         self.p.wait()
-        self.f.flush()
-        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        self.th.join(timeout=1)
         os.unlink(self.f.name)
+        rows = self.rows
+        win = [r for r in rows if self.t0 and self.t1 and self.t0 <= r[0] <= self.t1 + 0.05]
+        scope = "timed region"
+        if len(win) < 3:
+            win, scope = rows, "whole run (timed region too short for the sampler)"
         sm, smax, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in rows:
+        for _, line in win:
+            r = line.split(",")
             try:
-                sm.append(float(r[1]))
-                smax.append(float(r[2]))
-                for nm, v in zip(names, r[5:9]):
+                sm.append(float(r[0]))
+                smax.append(float(r[1]))
+                for nm, v in zip(names, r[4:8]):
                     if v.strip().lower() in ("active", "1"):
                         reasons.add(nm)
             except (ValueError, IndexError):
                 continue
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "scope": scope}
 
 
 def build_matrix(kind, g):
@@ -206,15 +229,16 @@ def run_ours(args, wl):
         f.compute(ns)
         f.apply(b, x, nt)
 
+    clocks = Clocks(local)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    clocks = Clocks(local)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t_sweeps, t_apply, t_init = [], [], []
     torch.cuda.synchronize()
+    clocks.mark_start()
     ev0.record(stream)
     for _ in range(args.steps):
         step()
@@ -223,6 +247,7 @@ def run_ours(args, wl):
         t_init.append(tm["init_ms"])
     ev1.record(stream)
     torch.cuda.synchronize()
+    clocks.mark_stop()
     clk = clocks.stop()
     ms = ev0.elapsed_time(ev1) / args.steps
     # apply alone (events inside the library), measured on the last step

@@ -72,6 +72,15 @@ struct fastilu_handle_s {
   unsigned long long *d_tmask = nullptr;
   unsigned int *d_counter = nullptr;
   double *d_aT = nullptr;  // A's values in template slots (refreshed by set_values)
+  // fused multi-sweep compute (template path, single GPU): iterates 0..ns in pool buffers
+  void *jit_fused = nullptr;
+  int fused_grid = 0;
+  std::vector<double *> fpool_v, fpool_u;  // extra value / diagonal buffers (iterates >= 2)
+  double **d_fptr_v = nullptr, **d_fptr_u = nullptr;
+  double *d_fpart = nullptr;
+  unsigned int *d_fws = nullptr;
+  int fused_cap = 0;
+  const double *vals_cur = nullptr, *ud_cur = nullptr;  // factors of the last compute
   // fused multi-sweep trisolve (template path, single GPU)
   double *d_tribuf = nullptr;
   unsigned int *d_triws = nullptr;
@@ -711,6 +720,77 @@ extern "C" fastilu_status fastilu_set_values_device(fastilu_handle h, const doub
 }
 
 // --------------------------------------------------------------------------- compute
+// All nsweeps synchronous sweeps in ONE persistent wavefront kernel (template path, single GPU):
+// sweep s of row i reads iterate s-1 of rows <= i only, so tiles are processed in row order and
+// each block runs every sweep of its tile, waiting until all earlier tiles finished the previous
+// sweep; iterate s lives in its own buffer.  Same per-row arithmetic as the per-sweep kernel.
+static fastilu_status sweeps_fused(fastilu_handle h, int ns, cudaStream_t st) {
+  const Template &T = h->T;
+  if (!h->jit_fused) {
+    std::string log;
+    const std::string src = sweep_source(T, h->t_threads, h->t_parts, h->t_minb, false, false,
+                                         true);
+    if (jit_get(src, "fastilu_tsell_compute_fused", h->device, &h->jit_fused, &log))
+      FAIL(FASTILU_ERR_UNSUPPORTED);
+    int bps = 0;
+    jit_func_info(h->jit_fused, nullptr, nullptr, h->t_threads, &bps);
+    if (bps < 1) FAIL(FASTILU_ERR_UNSUPPORTED);
+    h->fused_grid = sm_count(h->device) * bps;
+  }
+  const int64_t rpt = h->t_rows_tile;
+  const int64_t ntiles = (h->n + rpt - 1) / rpt;
+  const int64_t nv = h->nsl * T.W * 32;
+  if (ns > h->fused_cap) {
+    for (int q = (int)h->fpool_v.size(); q < ns - 1; q++) {  // iterates 2..ns
+      double *v = nullptr, *u = nullptr;
+      CU(dalloc(&v, nv));
+      CU(cudaMemset(v, 0, sizeof(double) * nv));  // absent slots stay +0.0
+      CU(dalloc(&u, h->E));
+      CU(cudaMemset(u, 0, sizeof(double) * h->E));
+      h->fpool_v.push_back(v);
+      h->fpool_u.push_back(u);
+    }
+    if (h->d_fptr_v) cudaFree(h->d_fptr_v);
+    if (h->d_fptr_u) cudaFree(h->d_fptr_u);
+    if (h->d_fpart) cudaFree(h->d_fpart);
+    if (h->d_fws) cudaFree(h->d_fws);
+    std::vector<double *> pv{h->d_vals[0], h->d_vals[1]}, pu{h->d_ud[0], h->d_ud[1]};
+    for (size_t q = 0; q < h->fpool_v.size(); q++) {
+      pv.push_back(h->fpool_v[q]);
+      pu.push_back(h->fpool_u[q]);
+    }
+    CU(dalloc(&h->d_fptr_v, (int64_t)pv.size()));
+    CU(dalloc(&h->d_fptr_u, (int64_t)pu.size()));
+    CU(cudaMemcpy(h->d_fptr_v, pv.data(), sizeof(double *) * pv.size(), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(h->d_fptr_u, pu.data(), sizeof(double *) * pu.size(), cudaMemcpyHostToDevice));
+    CU(dalloc(&h->d_fpart, (int64_t)ns * ntiles));
+    CU(cudaMalloc((void **)&h->d_fws, sizeof(unsigned int) * (1 + ns) + (size_t)ns * ntiles + 16));
+    h->fused_cap = ns;
+  }
+  const size_t ws = sizeof(unsigned int) * (1 + ns) + (size_t)ns * ntiles;
+  CU(cudaMemsetAsync(h->d_fws, 0, ws, st));
+  double **bufs = h->d_fptr_v, **udbufs = h->d_fptr_u;
+  int nsw = ns;
+  unsigned int *ctr = h->d_fws, *prefix = h->d_fws + 1;
+  unsigned char *flags = reinterpret_cast<unsigned char *>(h->d_fws + 1 + ns);
+  const double *ahat = h->d_ahat;
+  const unsigned long long *mk = h->d_tmask;
+  long long a0 = h->G, a1 = h->G + h->n;
+  double om = h->opt.omega;
+  double *part = h->d_fpart;
+  unsigned long long *zp = &h->d_err->zero_pivot;
+  void *args[] = {&bufs, &udbufs, &nsw, &prefix, &flags, &ahat, &mk, &a0, &a1, &om, &part, &zp,
+                  &ctr};
+  const int grid = (int)std::min<int64_t>(h->fused_grid, ntiles);
+  if (jit_launch(h->jit_fused, grid, h->t_threads, st, args)) FAIL(FASTILU_ERR_CUDA);
+  for (int sw = 1; sw <= ns; sw++)
+    CU(launch_reduce(h->d_fpart + (int64_t)(sw - 1) * ntiles, (int)ntiles, h->d_r2 + (sw - 1),
+                     st));
+  h->vals_cur = ns == 0 ? h->d_vals[0] : ns == 1 ? h->d_vals[1] : h->fpool_v[ns - 2];
+  h->ud_cur = ns == 0 ? h->d_ud[0] : ns == 1 ? h->d_ud[1] : h->fpool_u[ns - 2];
+  return FASTILU_OK;
+}
+
 // nsweeps synchronous sweeps; with rtol > 0, stop after the first sweep s whose residual of
 // iterate s-1 satisfies r(s-1) <= rtol ||Ahat|_S||_F (reading G15), at most nsweeps.
 static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, int *done,
@@ -781,8 +861,15 @@ static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, i
     thr2 = rtol * rtol * a2;
   }
   int executed = 0;
+  const bool fused = h->tsell && !h->comm && !warmup && !async && thr2 < 0.0 && nsweeps > 0 &&
+                     !std::getenv("FASTILU_NO_FUSED_SWEEPS");
+  if (fused) {
+    fastilu_status fs = sweeps_fused(h, nsweeps, st);
+    if (fs) return fs;
+    executed = nsweeps;
+  }
   // a4/a5: nsweeps synchronous sweeps, ping-pong buffers
-  for (int sw = 1; sw <= nsweeps; sw++) {
+  for (int sw = 1; sw <= nsweeps && !fused; sw++) {
     executed = sw;
     const int ib_async = 0;  // asynchronous sweeps stay in buffer 0 (in place)
     if (thr2 >= 0.0 && sw > 1) {  // r(sw-2) of the previous sweep decides whether to go on
@@ -858,6 +945,10 @@ static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, i
   for (size_t q = 0; q < r2tol.size() && q < r2.size(); q++) r2[q] = r2tol[q];
   for (int i = 0; i < nsweeps; i++) h->resid[i] = std::sqrt(r2[i]);
   h->cur = async ? 0 : (nsweeps & 1);
+  if (!fused) {
+    h->vals_cur = h->d_vals[h->cur];
+    h->ud_cur = h->d_ud[h->cur];
+  }
   if (ef.zero_diag != ~0ull) {
     h->err_index = (int64_t)ef.zero_diag;
     return FASTILU_ERR_ZERO_DIAG;
@@ -911,7 +1002,7 @@ static fastilu_status apply_fused(fastilu_handle h, const double *b, double *x, 
   const int64_t ntiles = (h->n + 255) / 256;
   const int grid = (int)std::min<int64_t>(h->tri_grid, ntiles);
   const double om = h->opt.omega_tri;
-  const double *vals = h->d_vals[h->cur], *ud = h->d_ud[h->cur];
+  const double *vals = h->vals_cur, *ud = h->ud_cur;
   double *zb = h->d_tribuf, *wb = h->d_tribuf + (int64_t)ntri * h->E;
   // y = s o b into d_y (the L solve's right-hand side)
   CU(launch_trisolve_first_L(b, h->d_s, h->d_y, zb, r0, r1, h->G, 1.0, st));
@@ -930,8 +1021,8 @@ static fastilu_status apply_impl(fastilu_handle h, const double *b, double *x, i
   DevPattern P{h->d_rp, h->d_ci, h->d_dloc};
   const int64_t r0 = h->G, r1 = h->G + h->n;
   const double om = h->opt.omega_tri;
-  const double *vals = h->d_vals[h->cur];
-  const double *ud = h->d_ud[h->cur];
+  const double *vals = h->vals_cur;
+  const double *ud = h->ud_cur;
   // a8: L sweeps.  t = 1: z1 = w y with y = s o b (z0 = 0)
   CU(launch_trisolve_first_L(b, h->d_s, h->d_y, h->d_z[0], r0, r1, h->G, om, st));
   for (int t = 2; t <= ntri; t++) {
@@ -1167,8 +1258,7 @@ extern "C" fastilu_status fastilu_get_factors(fastilu_handle h, double *vals, do
   if (vals && h->tsell) {  // gather the owned rows' S entries out of the template slots
     const Template &T = h->T;
     std::vector<double> tv((size_t)h->nsl * T.W * 32);
-    CU(cudaMemcpy(tv.data(), h->d_vals[h->cur], sizeof(double) * tv.size(),
-                  cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(tv.data(), h->vals_cur, sizeof(double) * tv.size(), cudaMemcpyDeviceToHost));
     for (int64_t r = 0; r < h->n; r++) {
       const int64_t i = h->G + r, g = h->row_begin + r;
       for (int64_t p = h->h_rp[r]; p < h->h_rp[r + 1]; p++) {
@@ -1178,7 +1268,7 @@ extern "C" fastilu_status fastilu_get_factors(fastilu_handle h, double *vals, do
       }
     }
   } else if (vals) {
-    CU(cudaMemcpy(vals, h->d_vals[h->cur] + h->own_off, sizeof(double) * h->nnz_own,
+    CU(cudaMemcpy(vals, h->vals_cur + h->own_off, sizeof(double) * h->nnz_own,
                   cudaMemcpyDeviceToHost));
   }
   if (s) CU(cudaMemcpy(s, h->d_s + h->G, sizeof(double) * h->n, cudaMemcpyDeviceToHost));
@@ -1237,13 +1327,15 @@ extern "C" fastilu_status fastilu_destroy(fastilu_handle h) {
                   h->d_rclass, h->d_coff, h->d_caoff, h->d_prog, h->d_toff, h->d_toffA,
                   h->d_tasrc, h->d_tw2a, h->d_tmask, h->d_counter, h->gm_V, h->gm_w,
                   h->gm_ext, h->gm_u, h->gm_r, h->gm_part, h->gm_c, h->d_aT, h->d_tribuf,
-                  h->d_triws};
+                  h->d_triws, h->d_fptr_v, h->d_fptr_u, h->d_fpart, h->d_fws};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   if (h->h_err) cudaFreeHost(h->h_err);
   if (h->h_r2) cudaFreeHost(h->h_r2);
   if (h->gm_hbuf) cudaFreeHost(h->gm_hbuf);
   for (auto *p : h->d_lmask) cudaFree(p);
+  for (auto *p : h->fpool_v) cudaFree(p);
+  for (auto *p : h->fpool_u) cudaFree(p);
   for (int i = 0; i < 5; i++)
     if (h->ev[i]) cudaEventDestroy(h->ev[i]);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
