@@ -277,3 +277,20 @@ def test_async_quality_vs_synchronous():
     ra = oracle.sweep(pat, ahat, va)[1]
     rs = oracle.sweep(pat, ahat, vs)[1]
     assert ra <= rs * 1.05, (ra, rs)
+
+
+@pytest.mark.parametrize("kind,g,k,ns,nt", [("27pt", 14, 1, 3, 5), ("27pt", 10, 2, 4, 3),
+                                             ("7pt", 24, 0, 2, 5), ("27pt", 9, 1, 1, 1)])
+def test_fused_wavefront_equals_per_sweep_kernels(kind, g, k, ns, nt, monkeypatch):
+    """The persistent wavefront kernels (all sweeps of compute / all Jacobi sweeps of apply in
+    one pass) compute exactly what the per-sweep kernels compute."""
+    a = P.make(kind, g)
+    b = P.rhs_positive(a.n)
+    _, v1, _, x1 = gpu_run(a, k, ns, nt, b)
+    monkeypatch.setenv("FASTILU_NO_FUSED_SWEEPS", "1")
+    monkeypatch.setenv("FASTILU_NO_FUSED_TRISOLVE", "1")
+    _, v2, _, x2 = gpu_run(a, k, ns, nt, b)
+    assert np.array_equal(v1, v2) and np.array_equal(x1, x2)
+    fo = oracle.compute(a, k, ns)
+    assert np.array_equal(v1, fo.vals)
+    assert np.array_equal(x1, oracle.apply(fo, b, nt))
