@@ -125,7 +125,8 @@ cudaError_t launch_tsell_trisolve_fused(const TDev &t, bool lower, bool final_x,
                                         const double *vals, const double *ud, const double *rhs,
                                         const double *s, double *buf, double *xout, int64_t r0,
                                         int64_t r1, int64_t E, int64_t Gh, double omega,
-                                        unsigned int *sync_ws, int grid, cudaStream_t st);
+                                        int64_t bandwidth, unsigned int *sync_ws, int grid,
+                                        cudaStream_t st);
 size_t tsell_trisolve_ws_bytes(int ntri, int64_t rows);
 cudaError_t tsell_trisolve_occupancy(int *blocks_per_sm);
 // deterministic sum of partials into *dst; also resets the tile counter (if non-null) to 0

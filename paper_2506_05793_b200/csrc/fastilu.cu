@@ -764,22 +764,24 @@ static fastilu_status sweeps_fused(fastilu_handle h, int ns, cudaStream_t st) {
     CU(cudaMemcpy(h->d_fptr_v, pv.data(), sizeof(double *) * pv.size(), cudaMemcpyHostToDevice));
     CU(cudaMemcpy(h->d_fptr_u, pu.data(), sizeof(double *) * pu.size(), cudaMemcpyHostToDevice));
     CU(dalloc(&h->d_fpart, (int64_t)ns * ntiles));
-    CU(cudaMalloc((void **)&h->d_fws, sizeof(unsigned int) * (1 + ns) + (size_t)ns * ntiles + 16));
+    CU(cudaMalloc((void **)&h->d_fws, 128 + (size_t)ns * ntiles + 16));
     h->fused_cap = ns;
   }
-  const size_t ws = sizeof(unsigned int) * (1 + ns) + (size_t)ns * ntiles;
+  const size_t ws = 128 + (size_t)ns * ntiles;
   CU(cudaMemsetAsync(h->d_fws, 0, ws, st));
   double **bufs = h->d_fptr_v, **udbufs = h->d_fptr_u;
   int nsw = ns;
-  unsigned int *ctr = h->d_fws, *prefix = h->d_fws + 1;
-  unsigned char *flags = reinterpret_cast<unsigned char *>(h->d_fws + 1 + ns);
+  unsigned int *ctr = h->d_fws;
+  unsigned char *flags = reinterpret_cast<unsigned char *>(h->d_fws) + 128;
+  // tiles a tile's sweep reads from: pivots and divisors lie within the lower bandwidth
+  int dep = (int)std::min<int64_t>(ntiles, (-(int64_t)T.off[0] + rpt - 1) / rpt + 1);
   const double *ahat = h->d_ahat;
   const unsigned long long *mk = h->d_tmask;
   long long a0 = h->G, a1 = h->G + h->n;
   double om = h->opt.omega;
   double *part = h->d_fpart;
   unsigned long long *zp = &h->d_err->zero_pivot;
-  void *args[] = {&bufs, &udbufs, &nsw, &prefix, &flags, &ahat, &mk, &a0, &a1, &om, &part, &zp,
+  void *args[] = {&bufs, &udbufs, &nsw, &dep, &flags, &ahat, &mk, &a0, &a1, &om, &part, &zp,
                   &ctr};
   const int grid = (int)std::min<int64_t>(h->fused_grid, ntiles);
   if (jit_launch(h->jit_fused, grid, h->t_threads, st, args)) FAIL(FASTILU_ERR_CUDA);
@@ -1006,11 +1008,12 @@ static fastilu_status apply_fused(fastilu_handle h, const double *b, double *x, 
   double *zb = h->d_tribuf, *wb = h->d_tribuf + (int64_t)ntri * h->E;
   // y = s o b into d_y (the L solve's right-hand side)
   CU(launch_trisolve_first_L(b, h->d_s, h->d_y, zb, r0, r1, h->G, 1.0, st));
+  const int64_t bwl = -(int64_t)h->T.off[0], bwu = (int64_t)h->T.off[h->T.W - 1];
   CU(launch_tsell_trisolve_fused(tdev(h), true, false, ntri, vals, nullptr, h->d_y, h->d_s, zb,
-                                 nullptr, r0, r1, h->E, h->G, om, h->d_triws, grid, st));
+                                 nullptr, r0, r1, h->E, h->G, om, bwl, h->d_triws, grid, st));
   const double *zf = zb + (int64_t)(ntri - 1) * h->E;
   CU(launch_tsell_trisolve_fused(tdev(h), false, true, ntri, vals, ud, zf, h->d_s, wb, x, r0, r1,
-                                 h->E, h->G, om, h->d_triws, grid, st));
+                                 h->E, h->G, om, bwu, h->d_triws, grid, st));
   return FASTILU_OK;
 }
 

@@ -13,6 +13,8 @@
 #include <cooperative_groups/reduce.h>
 #include <cooperative_groups/scan.h>
 
+#include <algorithm>
+
 #include "device.h"
 
 namespace cg = cooperative_groups;
@@ -941,8 +943,9 @@ cudaError_t launch_axpby(double a, const double *x, double b, double *y, int64_t
 // Fused multi-sweep Jacobi trisolve on the template layout (single GPU).  Sweep t of row i reads
 // iterate t-1 of rows on ONE side of i only (j < i for L, j > i for U), so tiles of rows are
 // processed in dependency order (ascending for L, descending for U; acquired from a counter)
-// and each block runs all ntri sweeps of its tile, waiting before sweep t until every earlier
-// tile has finished sweep t-1 (per-sweep completion prefix, advanced lock-free).  Iterates live
+// and each block runs all ntri sweeps of its tile, waiting before sweep t until the dep_tiles
+// tiles just before it (the rows its sweep reads: the template bandwidth) have finished sweep
+// t-1 -- every thread checks one completion flag, no sequential prefix chain.  Iterates live
 // in separate buffers buf[t-1] (extended length E), so nothing is overwritten early; the
 // factors of a tile are read from DRAM once and re-read from L1/L2 for the other sweeps.  The
 // arithmetic per row is the per-sweep kernel's (oracle order), so x is unchanged bitwise.
@@ -955,9 +958,26 @@ struct FusedTri {
   double *buf;        // ntri * E
   double *xout;       // final output (lower: z in buf; upper & final_x: x = s o w)
   unsigned int *counter;
-  unsigned int *prefix;  // ntri (tiles completed in order, per sweep)
-  unsigned char *flags;  // ntri * ntiles
+  unsigned char *flags;  // ntri * ntiles: tile finished sweep t
+  int dep_tiles;         // tiles a sweep of a tile depends on (before it in acquisition order)
 };
+
+// Block-wide wait until flags[ta-1], ..., flags[ta-dep] are all set (tiles < 0 count as set).
+__device__ __forceinline__ void wait_window(const unsigned char *flags, long long ta, int dep) {
+  for (int base = 0; base < dep; base += blockDim.x) {
+    const int q = base + (int)threadIdx.x;
+    const long long tt = ta - 1 - q;
+    const volatile unsigned char *fl = flags;
+    int ns = 32;
+    for (;;) {
+      const int ok = (q >= dep || tt < 0) ? 1 : (int)fl[tt];
+      if (__syncthreads_and(ok)) break;
+      __nanosleep(ns);
+      if (ns < 1024) ns *= 2;
+    }
+  }
+  __threadfence();
+}
 
 __global__ void __launch_bounds__(256)
 tsell_trisolve_fused_kernel(TDev t, FusedTri f) {
@@ -986,14 +1006,7 @@ tsell_trisolve_fused_kernel(TDev t, FusedTri f) {
       if (!f.lower) d_i = f.ud[i];
     }
     for (int sw = 1; sw <= f.ntri; sw++) {
-      if (sw > 1) {  // every earlier tile must have finished sweep sw-1
-        if (threadIdx.x == 0) {
-          volatile unsigned int *pp = f.prefix + (sw - 2);
-          while ((long long)*pp < ta) __nanosleep(64);
-        }
-        __syncthreads();
-        __threadfence();
-      }
+      if (sw > 1) wait_window(f.flags + (int64_t)(sw - 2) * f.ntiles, ta, f.dep_tiles);
       if (live) {
         double acc = rhs_i, prev = 0.0;
         if (sw > 1) {
@@ -1013,19 +1026,10 @@ tsell_trisolve_fused_kernel(TDev t, FusedTri f) {
         else
           f.buf[(int64_t)(sw - 1) * f.E + i] = v;
       }
+      __threadfence();
       __syncthreads();
-      if (threadIdx.x == 0) {  // publish: flag, then advance the prefix over completed tiles
-        __threadfence();
-        volatile unsigned char *fl = f.flags + (int64_t)(sw - 1) * f.ntiles;
-        fl[ta] = 1;
-        __threadfence();
-        unsigned int *pp = f.prefix + (sw - 1);
-        for (;;) {
-          const unsigned int p = *(volatile unsigned int *)pp;
-          if ((long long)p >= f.ntiles || !fl[p]) break;
-          atomicCAS(pp, p, p + 1);
-        }
-      }
+      if (threadIdx.x == 0)  // publish: this tile finished sweep sw
+        *(volatile unsigned char *)(f.flags + (int64_t)(sw - 1) * f.ntiles + ta) = 1;
     }
   }
 }
@@ -1034,12 +1038,13 @@ cudaError_t launch_tsell_trisolve_fused(const TDev &t, bool lower, bool final_x,
                                         const double *vals, const double *ud, const double *rhs,
                                         const double *s, double *buf, double *xout, int64_t r0,
                                         int64_t r1, int64_t E, int64_t Gh, double omega,
-                                        unsigned int *sync_ws, int grid, cudaStream_t st) {
+                                        int64_t bandwidth, unsigned int *sync_ws, int grid,
+                                        cudaStream_t st) {
   if (r1 <= r0) return cudaSuccess;
   const int threads = 256;
   const int64_t ntiles = (r1 - r0 + threads - 1) / threads;
-  // workspace: [counter][prefix ntri][flags ntri*ntiles bytes]
-  const size_t ws = sizeof(unsigned int) * (1 + ntri) + (size_t)ntri * ntiles;
+  // workspace: [counter (128 B)][flags ntri*ntiles bytes]
+  const size_t ws = 128 + (size_t)ntri * ntiles;
   cudaError_t e = cudaMemsetAsync(sync_ws, 0, ws, st);
   if (e != cudaSuccess) return e;
   FusedTri f;
@@ -1059,8 +1064,8 @@ cudaError_t launch_tsell_trisolve_fused(const TDev &t, bool lower, bool final_x,
   f.buf = buf;
   f.xout = xout;
   f.counter = sync_ws;
-  f.prefix = sync_ws + 1;
-  f.flags = reinterpret_cast<unsigned char *>(sync_ws + 1 + ntri);
+  f.flags = reinterpret_cast<unsigned char *>(sync_ws) + 128;
+  f.dep_tiles = (int)std::min<int64_t>(ntiles, (bandwidth + threads - 1) / threads + 1);
   tsell_trisolve_fused_kernel<<<grid, threads, 0, st>>>(t, f);
   return cudaGetLastError();
 }
@@ -1071,7 +1076,7 @@ cudaError_t tsell_trisolve_occupancy(int *blocks_per_sm) {
 }
 
 size_t tsell_trisolve_ws_bytes(int ntri, int64_t rows) {
-  return sizeof(unsigned int) * (1 + ntri) + (size_t)ntri * ((rows + 255) / 256) + 16;
+  return 128 + (size_t)ntri * ((rows + 255) / 256) + 16;
 }
 
 }  // namespace fastilu
