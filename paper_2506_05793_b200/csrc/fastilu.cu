@@ -720,6 +720,13 @@ extern "C" fastilu_status fastilu_set_values_device(fastilu_handle h, const doub
 }
 
 // --------------------------------------------------------------------------- compute
+// Wavefront (multi-sweep) kernels: opt-in with FASTILU_FUSED=1 (measured slower than the
+// per-sweep kernels so far, profiles/ and DESIGN.md); FASTILU_NO_FUSED_* force them off.
+static bool fused_enabled(const char *off_var) {
+  const char *on = std::getenv("FASTILU_FUSED");
+  return on && atoi(on) != 0 && !std::getenv(off_var);
+}
+
 // All nsweeps synchronous sweeps in ONE persistent wavefront kernel (template path, single GPU):
 // sweep s of row i reads iterate s-1 of rows <= i only, so tiles are processed in row order and
 // each block runs every sweep of its tile, waiting until all earlier tiles finished the previous
@@ -864,7 +871,7 @@ static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, i
   }
   int executed = 0;
   const bool fused = h->tsell && !h->comm && !warmup && !async && thr2 < 0.0 && nsweeps > 0 &&
-                     !std::getenv("FASTILU_NO_FUSED_SWEEPS");
+                     fused_enabled("FASTILU_NO_FUSED_SWEEPS");
   if (fused) {
     fastilu_status fs = sweeps_fused(h, nsweeps, st);
     if (fs) return fs;
@@ -1019,7 +1026,7 @@ static fastilu_status apply_fused(fastilu_handle h, const double *b, double *x, 
 
 static fastilu_status apply_impl(fastilu_handle h, const double *b, double *x, int ntri) {
   cudaStream_t st = h->stream;
-  if (h->tsell && !h->comm && !std::getenv("FASTILU_NO_FUSED_TRISOLVE"))
+  if (h->tsell && !h->comm && fused_enabled("FASTILU_NO_FUSED_TRISOLVE"))
     return apply_fused(h, b, x, ntri);
   DevPattern P{h->d_rp, h->d_ci, h->d_dloc};
   const int64_t r0 = h->G, r1 = h->G + h->n;

@@ -979,6 +979,8 @@ __device__ __forceinline__ void wait_window(const unsigned char *flags, long lon
   __threadfence();
 }
 
+constexpr int kTriRows = 4;  // rows per thread of a fused-trisolve tile (1024-row tiles)
+
 __global__ void __launch_bounds__(256)
 tsell_trisolve_fused_kernel(TDev t, FusedTri f) {
   __shared__ int32_t soff[128];
@@ -986,6 +988,7 @@ tsell_trisolve_fused_kernel(TDev t, FusedTri f) {
   for (int q = threadIdx.x; q < t.W; q += blockDim.x) soff[q] = t.off[q];
   __syncthreads();
   const int w0 = f.lower ? 0 : t.c0 + 1, w1 = f.lower ? t.c0 : t.W;
+  const int64_t tile_rows = (int64_t)blockDim.x * kTriRows;
   for (;;) {
     if (threadIdx.x == 0) s_tile = (long long)atomicAdd(f.counter, 1u);
     __syncthreads();
@@ -993,38 +996,35 @@ tsell_trisolve_fused_kernel(TDev t, FusedTri f) {
     __syncthreads();
     if (ta >= f.ntiles) break;
     const long long tile = f.lower ? ta : f.ntiles - 1 - ta;
-    const int64_t i = f.r0 + tile * blockDim.x + threadIdx.x;
-    const bool live = i < f.r1;
-    unsigned long long m[2] = {0ull, 0ull};
-    const double *row = nullptr;
-    double rhs_i = 0.0, d_i = 1.0;
-    if (live) {
-      const int64_t sl = i >> 5, ln = i & 31;
-      for (int q = 0; q < t.words; q++) m[q] = t.mask[(sl * t.words + q) * 32 + ln];
-      row = f.vals + sl * t.W * 32 + ln;
-      rhs_i = f.rhs[i];
-      if (!f.lower) d_i = f.ud[i];
-    }
     for (int sw = 1; sw <= f.ntri; sw++) {
       if (sw > 1) wait_window(f.flags + (int64_t)(sw - 2) * f.ntiles, ta, f.dep_tiles);
-      if (live) {
-        double acc = rhs_i, prev = 0.0;
-        if (sw > 1) {
-          const double *xo = f.buf + (int64_t)(sw - 2) * f.E;
-          for (int w = w0; w < w1; w++)
-            if (tbit(m, w)) acc = __dsub_rn(acc, __dmul_rn(row[w * 32], xo[i + soff[w]]));
-          prev = xo[i];
+      for (int rr = 0; rr < kTriRows; rr++) {
+        // upper solves walk their tile top-down too (rows above first), lower bottom-up
+        const int sub = f.lower ? rr : kTriRows - 1 - rr;
+        const int64_t i = f.r0 + tile * tile_rows + (int64_t)sub * blockDim.x + threadIdx.x;
+        if (i < f.r1) {
+          const int64_t sl = i >> 5, ln = i & 31;
+          unsigned long long m[2] = {0ull, 0ull};
+          for (int q = 0; q < t.words; q++) m[q] = t.mask[(sl * t.words + q) * 32 + ln];
+          const double *row = f.vals + sl * t.W * 32 + ln;
+          double acc = f.rhs[i], prev = 0.0;
+          if (sw > 1) {
+            const double *xo = f.buf + (int64_t)(sw - 2) * f.E;
+            for (int w = w0; w < w1; w++)
+              if (tbit(m, w)) acc = __dsub_rn(acc, __dmul_rn(row[w * 32], xo[i + soff[w]]));
+            prev = xo[i];
+          }
+          if (!f.lower) acc = __ddiv_rn(acc, f.ud[i]);
+          const double v = (f.omega == 1.0)
+                               ? acc
+                               : (sw == 1 ? __dmul_rn(f.omega, acc)
+                                          : __dadd_rn(__dmul_rn(1.0 - f.omega, prev),
+                                                      __dmul_rn(f.omega, acc)));
+          if (sw == f.ntri && f.final_x)
+            f.xout[i - f.Gh] = __dmul_rn(f.s[i], v);
+          else
+            f.buf[(int64_t)(sw - 1) * f.E + i] = v;
         }
-        if (!f.lower) acc = __ddiv_rn(acc, d_i);
-        const double v = (f.omega == 1.0)
-                             ? acc
-                             : (sw == 1 ? __dmul_rn(f.omega, acc)
-                                        : __dadd_rn(__dmul_rn(1.0 - f.omega, prev),
-                                                    __dmul_rn(f.omega, acc)));
-        if (sw == f.ntri && f.final_x)
-          f.xout[i - f.Gh] = __dmul_rn(f.s[i], v);
-        else
-          f.buf[(int64_t)(sw - 1) * f.E + i] = v;
       }
       __threadfence();
       __syncthreads();
@@ -1042,7 +1042,8 @@ cudaError_t launch_tsell_trisolve_fused(const TDev &t, bool lower, bool final_x,
                                         cudaStream_t st) {
   if (r1 <= r0) return cudaSuccess;
   const int threads = 256;
-  const int64_t ntiles = (r1 - r0 + threads - 1) / threads;
+  const int64_t tile_rows = (int64_t)threads * kTriRows;
+  const int64_t ntiles = (r1 - r0 + tile_rows - 1) / tile_rows;
   // workspace: [counter (128 B)][flags ntri*ntiles bytes]
   const size_t ws = 128 + (size_t)ntri * ntiles;
   cudaError_t e = cudaMemsetAsync(sync_ws, 0, ws, st);
@@ -1065,7 +1066,7 @@ cudaError_t launch_tsell_trisolve_fused(const TDev &t, bool lower, bool final_x,
   f.xout = xout;
   f.counter = sync_ws;
   f.flags = reinterpret_cast<unsigned char *>(sync_ws) + 128;
-  f.dep_tiles = (int)std::min<int64_t>(ntiles, (bandwidth + threads - 1) / threads + 1);
+  f.dep_tiles = (int)std::min<int64_t>(ntiles, (bandwidth + tile_rows - 1) / tile_rows + 1);
   tsell_trisolve_fused_kernel<<<grid, threads, 0, st>>>(t, f);
   return cudaGetLastError();
 }
@@ -1076,7 +1077,7 @@ cudaError_t tsell_trisolve_occupancy(int *blocks_per_sm) {
 }
 
 size_t tsell_trisolve_ws_bytes(int ntri, int64_t rows) {
-  return 128 + (size_t)ntri * ((rows + 255) / 256) + 16;
+  return 128 + (size_t)ntri * ((rows + 255) / 256) + 16;  // >= flags for kTriRows >= 1
 }
 
 }  // namespace fastilu

@@ -286,9 +286,9 @@ def test_fused_wavefront_equals_per_sweep_kernels(kind, g, k, ns, nt, monkeypatc
     one pass) compute exactly what the per-sweep kernels compute."""
     a = P.make(kind, g)
     b = P.rhs_positive(a.n)
+    monkeypatch.setenv("FASTILU_FUSED", "1")
     _, v1, _, x1 = gpu_run(a, k, ns, nt, b)
-    monkeypatch.setenv("FASTILU_NO_FUSED_SWEEPS", "1")
-    monkeypatch.setenv("FASTILU_NO_FUSED_TRISOLVE", "1")
+    monkeypatch.delenv("FASTILU_FUSED")
     _, v2, _, x2 = gpu_run(a, k, ns, nt, b)
     assert np.array_equal(v1, v2) and np.array_equal(x1, x2)
     fo = oracle.compute(a, k, ns)
