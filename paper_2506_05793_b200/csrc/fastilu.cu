@@ -744,7 +744,7 @@ static fastilu_status sweeps_fused(fastilu_handle h, int ns, cudaStream_t st) {
     if (bps < 1) FAIL(FASTILU_ERR_UNSUPPORTED);
     h->fused_grid = sm_count(h->device) * bps;
   }
-  const int64_t rpt = h->t_rows_tile;
+  const int64_t rpt = sweep_rows_per_tile(h->t_threads, h->t_parts, true);
   const int64_t ntiles = (h->n + rpt - 1) / rpt;
   const int64_t nv = h->nsl * T.W * 32;
   if (ns > h->fused_cap) {
