@@ -184,7 +184,9 @@ def run_ours(args, wl):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
-    stream = torch.cuda.current_stream(dev)
+    # a dedicated (non-default) stream: the library enqueues on it and every timing event is
+    # recorded on it (the legacy default stream's handle 0 would make the library use its own)
+    stream = torch.cuda.Stream(dev)
 
     t0 = time.perf_counter()
     if world == 1:
@@ -218,12 +220,13 @@ def run_ours(args, wl):
         dist.all_reduce(tt)
         nnz_S_total = int(tt.item())
     rp, ci, _ = f.pattern()
-    rows = np.repeat(np.arange(n), np.diff(rp))
+    rows = np.repeat(np.arange(n, dtype=np.int64) + row_begin, np.diff(rp))
     nnz_Ls = int(np.count_nonzero(ci < rows))
     del rows, rp, ci
     bm = byte_model(n, nnz_A, nnz_S, nnz_Ls, ns, nt)
     b = torch.tensor(P.rhs_positive(n), device=dev)
     x = torch.empty_like(b)
+    torch.cuda.synchronize(dev)
 
     def step():
         f.compute(ns)
