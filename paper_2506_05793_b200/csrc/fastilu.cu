@@ -88,7 +88,7 @@ struct fastilu_handle_s {
   std::vector<unsigned long long *> d_lmask;  // warm-up: presence masks of levels 0..K-1
   void *jit_sweep = nullptr;
   void *jit_sweep_async = nullptr;  // compiled on the first asynchronous compute
-  int t_parts = 1, t_minb = 0;
+  int t_parts = 1, t_minb = 0, t_sstride = 1;
   bool t_prefetch = true;
   int t_threads = 128, t_grid = 1, t_regs = 0, t_spill = 0, t_rows_tile = 128;
   int64_t t_ntiles = 0;
@@ -383,9 +383,21 @@ static fastilu_status setup_tsell(fastilu_handle h, const std::vector<unsigned l
   if (bps < 1) FAIL(FASTILU_ERR_UNSUPPORTED);
   h->t_threads = threads;
   h->t_parts = parts;
+  // slice stride of a tile: the template's grid line (smallest positive offset that is a
+  // multiple of 32 rows), in slices; 1 if none
+  h->t_sstride = 1;
+  for (int w = T.c0 + 1; w < T.W; w++)
+    if (T.off[w] >= 32 && T.off[w] % 32 == 0) {
+      h->t_sstride = T.off[w] / 32;
+      break;
+    }
+  if (std::getenv("FASTILU_TSELL_SSTRIDE")) h->t_sstride = std::max(1, atoi(std::getenv("FASTILU_TSELL_SSTRIDE")));
   h->t_minb = minb;
   h->t_rows_tile = sweep_rows_per_tile(threads, parts);
-  h->t_ntiles = std::max<int64_t>(1, (h->n + h->t_rows_tile - 1) / h->t_rows_tile);
+  {
+    const int64_t nsl_own = (h->n + 31) / 32, spt = h->t_rows_tile / 32, ss = h->t_sstride;
+    h->t_ntiles = std::max<int64_t>(1, (nsl_own + spt * ss - 1) / (spt * ss) * ss);
+  }
   h->t_grid = (int)std::min<int64_t>((int64_t)sm_count(h->device) * bps, h->t_ntiles);
   const int64_t nv = h->nsl * T.W * 32;
   for (int b = 0; b < 2; b++) {
@@ -788,8 +800,9 @@ static fastilu_status sweeps_fused(fastilu_handle h, int ns, cudaStream_t st) {
   double om = h->opt.omega;
   double *part = h->d_fpart;
   unsigned long long *zp = &h->d_err->zero_pivot;
+  int sstr1 = 1;  // the wavefront kernel walks consecutive slices
   void *args[] = {&bufs, &udbufs, &nsw, &dep, &flags, &ahat, &mk, &a0, &a1, &om, &part, &zp,
-                  &ctr};
+                  &ctr, &sstr1};
   const int grid = (int)std::min<int64_t>(h->fused_grid, ntiles);
   if (jit_launch(h->jit_fused, grid, h->t_threads, st, args)) FAIL(FASTILU_ERR_CUDA);
   for (int sw = 1; sw <= ns; sw++)
@@ -917,7 +930,8 @@ static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, i
       double om = h->opt.omega;
       unsigned long long *zp = &h->d_err->zero_pivot;
       unsigned int *ctr = h->d_counter;
-      void *args[] = {&old, &outp, &ahat, &mk, &udo, &udn, &a0, &a1, &om, &part, &zp, &ctr};
+      int sstr = h->t_sstride;
+      void *args[] = {&old, &outp, &ahat, &mk, &udo, &udn, &a0, &a1, &om, &part, &zp, &ctr, &sstr};
       if (jit_launch(async ? h->jit_sweep_async : h->jit_sweep, h->t_grid, h->t_threads, st,
                      args))
         return FASTILU_ERR_CUDA;
@@ -1311,10 +1325,10 @@ extern "C" fastilu_status fastilu_get_info(fastilu_handle h, char *buf, int cap)
   if (h->tsell)
     snprintf(tmp, sizeof(tmp),
              "path=tsell W=%d c0=%d WA=%d terms=%zu threads=%d rows/tile=%d grid=%d regs=%d "
-             "local=%d tiles=%lld G=%lld H=%lld",
+             "local=%d tiles=%lld sstride=%d G=%lld H=%lld",
              h->T.W, h->T.c0, h->T.WA, h->T.terms.size(), h->t_threads, h->t_rows_tile,
              h->t_grid, h->t_regs,
-             h->t_spill, (long long)h->t_ntiles, (long long)h->G, (long long)h->H);
+             h->t_spill, (long long)h->t_ntiles, h->t_sstride, (long long)h->G, (long long)h->H);
   else
     snprintf(tmp, sizeof(tmp),
              "path=%s G_lanes=%d E=%d threads=%d grid=%d classes=%lld tri_lanes=%d G=%lld H=%lld",
