@@ -299,7 +299,7 @@ def run_ours(args, wl):
                "ms_per_step": ems}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu and kind != "3dof":
         planes = args.cpu_planes or default_cpu_planes(kind, g, k)
         r = cpu_sample(kind, g, k, ns, nt, planes)
         cpu = {"value": r["value"], "unit": UNIT, "cores": 1, "kind": "oracle",

@@ -385,12 +385,9 @@ static fastilu_status setup_tsell(fastilu_handle h, const std::vector<unsigned l
   h->t_parts = parts;
   // slice stride of a tile: the template's grid line (smallest positive offset that is a
   // multiple of 32 rows), in slices; 1 if none
+  // (measured neutral at 128^3/256^3 -- the sweep is not L1-bound -- so consecutive slices
+  // stay the default; FASTILU_TSELL_SSTRIDE=g/32 enables it)
   h->t_sstride = 1;
-  for (int w = T.c0 + 1; w < T.W; w++)
-    if (T.off[w] >= 32 && T.off[w] % 32 == 0) {
-      h->t_sstride = T.off[w] / 32;
-      break;
-    }
   if (std::getenv("FASTILU_TSELL_SSTRIDE")) h->t_sstride = std::max(1, atoi(std::getenv("FASTILU_TSELL_SSTRIDE")));
   h->t_minb = minb;
   h->t_rows_tile = sweep_rows_per_tile(threads, parts);

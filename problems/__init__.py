@@ -224,10 +224,15 @@ WORKLOADS = {
     "c3b_27pt_128_ilu2": ("27pt", 128, 2, 3, 5),
     "c4_27pt_256_ilu1": ("27pt", 256, 1, 3, 5),
     "c5_aniso7pt_256_ilu0": ("aniso7pt", 256, 0, 2, 5),
+    # the paper's own FastILU(3) problem of tab:fastilu_sweep: 3-dof 27-pt
+    # pattern on 32^3 nodes (n = 98,304, nnz(S) = 45,729,504); context workload only
+    "t6_3dof_32_ilu3": ("3dof", 32, 3, 3, 5),
 }
 
 
 def make(kind: str, g: int, gz: int | None = None, planes=None) -> Csr:
+    if kind == "3dof" and (gz is not None or planes is not None):
+        raise ValueError("the 3-dof pattern is generated on full g^3 grids only")
     if kind == "7pt":
         return laplace3d_7pt(g, gz=gz, planes=planes)
     if kind == "27pt":
