@@ -154,6 +154,30 @@ cudaError_t launch_maxpy(const double *V, int64_t ldv, int k, const double *c, d
 cudaError_t launch_axpby(double a, const double *x, double b, double *y, int64_t n,
                          cudaStream_t st);
 
+// ---- block path (bsr.cu): S made of dense BS x BS blocks (BS = 2, 3, 4), single GPU.
+// Blocks stored contiguously, ST = BS*BS rounded up to even doubles per block; block b of block
+// row I covers scalar rows BS I .. BS I + BS - 1 and columns BS bcol[b] ...
+struct BsrDev {
+  int bs;
+  int64_t nb, nblk;
+  const int64_t *bptr;   // nb + 1
+  const int32_t *brow;   // nblk: block row of each block
+  const int32_t *bcol;   // nblk
+  const int32_t *bdiag;  // nb: index of the diagonal block of each block row
+  const int64_t *tptr;   // nblk + 1: term range of each target block
+  const int2 *terms;     // (block (I,K), block (K,J)), K ascending, K < min(I, J)
+};
+cudaError_t bsr_sweep_occupancy(int bs, int threads, int *blocks_per_sm);
+cudaError_t launch_bsr_sweep(const BsrDev &B, const double *ahb, const double *old, double *out,
+                             double omega, double *partials, ErrFlags *err, int grid,
+                             int threads, cudaStream_t st);
+cudaError_t launch_bsr_from_csr(const BsrDev &B, const int64_t *rp, const double *vals,
+                                double *vb, int64_t nrows, cudaStream_t st);
+cudaError_t launch_bsr_to_csr(const BsrDev &B, const int64_t *rp, const double *vb, double *vals,
+                              double *ud, int64_t nrows, cudaStream_t st);
+cudaError_t launch_bsr_ahat(const BsrDev &B, const int64_t *arp, const int32_t *apos,
+                            const double *ahatA, double *ahb, int64_t nrows, cudaStream_t st);
+
 int sm_count(int device);
 
 }  // namespace fastilu

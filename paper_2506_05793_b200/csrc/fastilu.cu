@@ -17,6 +17,7 @@
 #include "comm.h"
 #include "device.h"
 #include "host.h"
+#include "blocks.h"
 #include "jit.h"
 #include "tsell.h"
 
@@ -72,6 +73,15 @@ struct fastilu_handle_s {
   unsigned long long *d_tmask = nullptr;
   unsigned int *d_counter = nullptr;
   double *d_aT = nullptr;  // A's values in template slots (refreshed by set_values)
+  // block path (bsr.cu, blocks.h): block-dense patterns, single GPU
+  bool bsr = false;
+  BsrDev B{};
+  int64_t *d_bptr = nullptr, *d_tptr = nullptr;
+  int32_t *d_brow = nullptr, *d_bcol = nullptr, *d_bdiag = nullptr;
+  int2 *d_terms = nullptr;
+  double *d_vb[2] = {nullptr, nullptr}, *d_ahb = nullptr;
+  int bsr_grid = 0, bsr_threads = 256;
+  int64_t bsr_nterms = 0;
   // fused multi-sweep compute (template path, single GPU): iterates 0..ns in pool buffers
   void *jit_fused = nullptr;
   int fused_grid = 0;
@@ -599,15 +609,60 @@ static fastilu_status create_impl(fastilu_handle h, int64_t n, const int64_t *ro
       }
     }
   }
+  // block-dense patterns (3-dof elasticity type): block sweep with host-built term lists
+  BlockPattern bp;
+  if (!h->tsell && !multi && !std::getenv("FASTILU_NO_BSR")) {
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    const int64_t max_terms = (int64_t)(fr / 4 / 8);  // term list <= a quarter of free memory
+    h->bsr = build_blocks(rp, ci, h->nloc, nt, max_terms, bp);
+  }
   // structure classes for the class-program sweep (falls back to the hash kernel if absent)
   ClassProgram cp;
-  const bool have_prog = !h->tsell &&
+  const bool have_prog = !h->tsell && !h->bsr &&
       !std::getenv("FASTILU_NO_CLASSES") &&
       build_classes(rp, ci, dloc, h->nloc, h->G, h->G + n, arp, apos, nt, (size_t)256 << 20,
                     1 << 16, cp);
   fastilu_status fs = h->tsell ? FASTILU_OK
                               : setup_configs(h, rp, ci, m_max, u_avg, nl_avg, maxU, have_prog, nt);
-  if (fs) return fs;
+  if (fs && !(h->bsr && fs == FASTILU_ERR_UNSUPPORTED)) return fs;  // rows too long for smem
+  if (h->bsr) {
+    int gi = 4, gt = 1;
+    while (gi < (double)h->nnz_own / std::max<int64_t>(h->n, 1) && gi < 32) gi *= 2;
+    while (2 * gt < nl_avg && gt < 32) gt *= 2;
+    h->G_init = gi;
+    h->G_tri = gt;
+    const int64_t st = (bp.bs * bp.bs + 1) & ~1;
+    CU(dalloc(&h->d_bptr, bp.nb + 1));
+    CU(dalloc(&h->d_brow, bp.nblk));
+    CU(dalloc(&h->d_bcol, bp.nblk));
+    CU(dalloc(&h->d_bdiag, bp.nb));
+    CU(dalloc(&h->d_tptr, bp.nblk + 1));
+    CU(cudaMalloc((void **)&h->d_terms, sizeof(int2) * (size_t)std::max<int64_t>(bp.nterms, 1)));
+    for (int b = 0; b < 2; b++) {
+      CU(dalloc(&h->d_vb[b], bp.nblk * st));
+      CU(cudaMemset(h->d_vb[b], 0, sizeof(double) * bp.nblk * st));
+    }
+    CU(dalloc(&h->d_ahb, bp.nblk * st));
+    CU(cudaMemset(h->d_ahb, 0, sizeof(double) * bp.nblk * st));  // fill entries: +0.0
+    CU(cudaMemcpy(h->d_bptr, bp.bptr.data(), 8 * bp.bptr.size(), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(h->d_brow, bp.brow.data(), 4 * bp.brow.size(), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(h->d_bcol, bp.bcol.data(), 4 * bp.bcol.size(), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(h->d_bdiag, bp.bdiag.data(), 4 * bp.bdiag.size(), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(h->d_tptr, bp.tptr.data(), 8 * bp.tptr.size(), cudaMemcpyHostToDevice));
+    if (bp.nterms)
+      CU(cudaMemcpy(h->d_terms, bp.terms.data(), 4 * bp.terms.size(), cudaMemcpyHostToDevice));
+    h->bsr_nterms = bp.nterms;
+    h->B = BsrDev{bp.bs,     bp.nb,      bp.nblk,     h->d_bptr, h->d_brow,
+                  h->d_bcol, h->d_bdiag, h->d_tptr,   h->d_terms};
+    int bps = 0;
+    if (bsr_sweep_occupancy(bp.bs, h->bsr_threads, &bps) != cudaSuccess || bps < 1)
+      return FASTILU_ERR_CUDA;
+    h->bsr_grid = (int)std::max<int64_t>(
+        1, std::min<int64_t>((int64_t)sm_count(h->device) * bps,
+                             (bp.nblk + h->bsr_threads - 1) / h->bsr_threads));
+    h->scfg.grid = std::max(h->scfg.grid, h->bsr_grid);  // partials capacity
+  }
   if (h->scfg.prog) {
     h->nclasses = cp.nclasses;
     CU(dalloc(&h->d_rclass, (int64_t)cp.row_class.size()));
@@ -862,6 +917,10 @@ static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, i
   else
     CU(launch_init(P, h->d_arp, h->d_aci, h->d_apos, h->d_aval, h->d_s, h->d_ad, r0, r1,
                    h->d_ahat, h->d_vals[0], h->d_ud[0], h->d_err, h->G_init, h->opt.shift, st));
+  if (h->bsr) {  // iterate 0 and ahat into the block layout
+    CU(launch_bsr_from_csr(h->B, h->d_rp, h->d_vals[0], h->d_vb[0], h->n, st));
+    CU(launch_bsr_ahat(h->B, h->d_arp, h->d_apos, h->d_ahat, h->d_ahb, h->n, st));
+  }
   CU(cudaEventRecord(h->ev[1], st));
   double thr2 = -1.0;  // (rtol ||Ahat|_S||_F)^2, tolerance mode only
   std::vector<double> r2tol;
@@ -936,6 +995,12 @@ static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, i
                              st));
       continue;
     }
+    if (h->bsr) {
+      CU(launch_bsr_sweep(h->B, h->d_ahb, h->d_vb[ib], h->d_vb[ob], h->opt.omega, h->d_partials,
+                          h->d_err, h->bsr_grid, h->bsr_threads, st));
+      CU(launch_reduce(h->d_partials, h->bsr_grid, h->d_r2 + (sw - 1), st));
+      continue;
+    }
     if (h->scfg.prog) {
       ProgView pv{h->d_rclass, h->d_coff, h->d_caoff, h->d_prog};
       CU(launch_sweep_prog(sa, pv, h->scfg, st));
@@ -946,6 +1011,9 @@ static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, i
   }
   nsweeps = executed;
   if (done) *done = executed;
+  if (h->bsr)  // factors back to S row order (+ u_ii) for apply / get_factors
+    CU(launch_bsr_to_csr(h->B, h->d_rp, h->d_vb[nsweeps & 1], h->d_vals[nsweeps & 1],
+                         h->d_ud[nsweeps & 1], h->n, st));
   CU(cudaEventRecord(h->ev[2], st));
   CU(cudaMemcpyAsync(h->h_err, h->d_err, sizeof(ErrFlags), cudaMemcpyDeviceToHost, st));
   if (nsweeps)
@@ -1326,6 +1394,11 @@ extern "C" fastilu_status fastilu_get_info(fastilu_handle h, char *buf, int cap)
              h->T.W, h->T.c0, h->T.WA, h->T.terms.size(), h->t_threads, h->t_rows_tile,
              h->t_grid, h->t_regs,
              h->t_spill, (long long)h->t_ntiles, h->t_sstride, (long long)h->G, (long long)h->H);
+  else if (h->bsr)
+    snprintf(tmp, sizeof(tmp),
+             "path=bsr%d blocks=%lld terms=%lld threads=%d grid=%d tri_lanes=%d G=%lld H=%lld",
+             h->B.bs, (long long)h->B.nblk, (long long)h->bsr_nterms,
+             h->bsr_threads, h->bsr_grid, h->G_tri, (long long)h->G, (long long)h->H);
   else
     snprintf(tmp, sizeof(tmp),
              "path=%s G_lanes=%d E=%d threads=%d grid=%d classes=%lld tri_lanes=%d G=%lld H=%lld",
@@ -1348,7 +1421,9 @@ extern "C" fastilu_status fastilu_destroy(fastilu_handle h) {
                   h->d_rclass, h->d_coff, h->d_caoff, h->d_prog, h->d_toff, h->d_toffA,
                   h->d_tasrc, h->d_tw2a, h->d_tmask, h->d_counter, h->gm_V, h->gm_w,
                   h->gm_ext, h->gm_u, h->gm_r, h->gm_part, h->gm_c, h->d_aT, h->d_tribuf,
-                  h->d_triws, h->d_fptr_v, h->d_fptr_u, h->d_fpart, h->d_fws};
+                  h->d_triws, h->d_fptr_v, h->d_fptr_u, h->d_fpart, h->d_fws,
+                  h->d_bptr, h->d_tptr, h->d_brow, h->d_bcol, h->d_bdiag, h->d_terms,
+                  h->d_vb[0], h->d_vb[1], h->d_ahb};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   if (h->h_err) cudaFreeHost(h->h_err);

@@ -141,6 +141,29 @@ def elasticity_pattern_3dof(g: int) -> Csr:
     return Csr(rp, ci, vals)
 
 
+def multi_dof_pattern(g: int, dofs: int, seed: int | None = None) -> Csr:
+    """`dofs` unknowns per node, dense dofs x dofs blocks on the 27-point node graph (as
+    elasticity_pattern_3dof, any block size).  Off-diagonal values -1, or, with a seed,
+    -U[0.5, 1.5); diagonal 27 dofs + 1 + (seeded: U[0, 1)), so rows are strictly dominant."""
+    node = laplace3d_27pt(g)
+    nn = node.n
+    cnt = np.diff(node.row_ptr)
+    rp = np.zeros(dofs * nn + 1, dtype=np.int64)
+    np.cumsum(np.repeat(cnt * dofs, dofs), out=rp[1:])
+    ci = np.empty(int(rp[-1]), dtype=np.int32)
+    rng = np.random.default_rng(seed) if seed is not None else None
+    vals = -rng.uniform(0.5, 1.5, size=int(rp[-1])) if rng is not None else np.full(int(rp[-1]), -1.0)
+    for v in range(nn):
+        cols = node.col_idx[node.row_ptr[v]:node.row_ptr[v + 1]].astype(np.int64)
+        blk = (dofs * cols[:, None] + np.arange(dofs)[None, :]).ravel()
+        for d in range(dofs):
+            r = dofs * v + d
+            s = rp[r]
+            ci[s:s + blk.size] = blk
+            vals[s + np.searchsorted(blk, r)] = 27.0 * dofs + 1.0 + (rng.uniform() if rng else 0.0)
+    return Csr(rp, ci, vals)
+
+
 def tridiagonal(n: int, seed: int = SEED) -> Csr:
     """Random diagonally dominant tridiagonal matrix (values seeded)."""
     rng = np.random.default_rng(seed)
