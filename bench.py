@@ -34,6 +34,32 @@ UNIT = "nnz-updates/s"
 SV, SI = 8, 4
 
 
+# FP64 lane throughput of one B200: 148 SMs x 64 FP64 lanes x 1.965 GHz.  The
+# sweep's rounded product and rounded difference are separate instructions (no FMA, for the
+# oracle's bitwise order), so one flop per lane-cycle.
+FP64_LANE_TFLOPS = 148 * 64 * 1.965e9 / 1e12
+
+
+def bsr_roofline(info, n, sweep_ms):
+    """Block path: flops per sweep from the term count.  Each pivot-block term is BS^3 rounded
+    multiply-subtracts; each off-diagonal target block adds BS^2 (BS-1)/2 tail terms inside block
+    min(I,J), each diagonal block sum_{d,e} min(d,e) (3,537,519,556 terms per
+    sweep for the Table-6 problem)."""
+    import re
+    bs = int(re.search(r"path=bsr(\d)", info).group(1))
+    nterms = int(re.search(r"terms=(\d+)", info).group(1))
+    nblk = int(re.search(r"blocks=(\d+)", info).group(1))
+    nb = n // bs
+    tail = bs * bs * (bs - 1) // 2 * (nblk - nb) + sum(min(d, e) for d in range(bs)
+                                                        for e in range(bs)) * nb
+    terms = bs ** 3 * nterms + tail
+    achieved = 2 * terms / (sweep_ms * 1e-3) / 1e12
+    return {"bound": "alu", "kernel": "bsr_sweep_kernel", "achieved": achieved,
+            "peak": FP64_LANE_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_LANE_TFLOPS,
+            "peak_source": "derived: 148 SMs x 64 FP64 lanes x 1.965 GHz, one rounded mul or sub "
+                           "per lane-cycle (no FMA)", "traffic": None, "terms_per_sweep": terms}
+
+
 def byte_model(n, nnz_A, nnz_S, nnz_Ls, ns, nt):
     """Algorithmic bytes."""
     sp = 4 if nnz_S < 2**31 else 8
@@ -305,7 +331,13 @@ def run_ours(args, wl):
         cpu = {"value": r["value"], "unit": UNIT, "cores": 1, "kind": "oracle",
                "sample": r["sample"]}
 
-    launches_per_step = 2 + 2 * ns + 2 * nt
+    info = f.info()
+    launches_per_step = 2 + 2 * ns + 2 * nt + (3 if info.startswith("path=bsr") else 0)
+    roof = {"bound": "hbm", "kernel": "sweep_kernel", "achieved": achieved, "peak": peak,
+            "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+            "algorithmic_bytes_per_launch": bm["B_f"]}
+    if info.startswith("path=bsr"):
+        roof = bsr_roofline(info, n, sweep_ms / max(ns, 1))
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -322,14 +354,11 @@ def run_ours(args, wl):
             "sweep_ms": sweep_ms, "init_ms": float(np.mean(t_init)), "apply_ms": t_apply,
             "trisolve_gbs": bm["B_apply"] / (t_apply * 1e-3) / 1e9 if t_apply > 0 else None,
             "composite_gbs": (bm["B_init"] + ns * bm["B_f"] + bm["B_apply"]) / (ms * 1e-3) / 1e9,
-            "roofline": {"bound": "hbm", "kernel": "sweep_kernel", "achieved": achieved,
-                         "peak": peak, "peak_source": peak_src, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "algorithmic_bytes_per_launch": bm["B_f"]},
+            "roofline": roof,
             "clocks": clk, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
             "cpu_baseline": cpu,
             "setup_s": {"generate": t_gen, "create": t_setup},
-            "kernel_config": f.info(),
+            "kernel_config": info,
         }
         print(json.dumps(line), flush=True)
     f.close()

@@ -36,6 +36,18 @@ static __device__ __forceinline__ void ld_block(const double *__restrict__ p, do
   }
 }
 
+// generic address (shared-memory stage or global)
+template <int BB, int ST>
+static __device__ __forceinline__ void ld_block_any(const double *p, double (&v)[BB]) {
+  const double2 *q = reinterpret_cast<const double2 *>(p);
+#pragma unroll
+  for (int h = 0; h < ST / 2; h++) {
+    const double2 x = q[h];
+    v[2 * h] = x.x;
+    if (2 * h + 1 < BB) v[2 * h + 1] = x.y;
+  }
+}
+
 template <int BB, int ST>
 static __device__ __forceinline__ void st_block(double *__restrict__ p, const double (&v)[BB]) {
   double2 *q = reinterpret_cast<double2 *>(p);
@@ -43,17 +55,42 @@ static __device__ __forceinline__ void st_block(double *__restrict__ p, const do
   for (int h = 0; h < ST / 2; h++) q[h] = make_double2(v[2 * h], 2 * h + 1 < BB ? v[2 * h + 1] : 0.0);
 }
 
-template <int BS>
-__global__ void __launch_bounds__(256)
+// One CTA takes tiles of blockDim.x consecutive target blocks (grid-stride over tiles).  With
+// STAGE, the tile's block rows (all their blocks, iterate s-1) are first copied to shared memory
+// when they fit in smem_blocks: the L blocks (I,K) every target of row I reads, the target's own
+// old block and the row's diagonal block then come from shared memory; only the pivots' U blocks
+// (K,J) and the divisor blocks of rows J are read from global memory.
+template <int BS, bool STAGE, int MINB>
+__global__ void __launch_bounds__(256, MINB)
 bsr_sweep_kernel(BsrDev B, const double *__restrict__ ahb, const double *__restrict__ old,
                  double *__restrict__ out, double omega, double *__restrict__ partials,
-                 ErrFlags *err) {
+                 ErrFlags *err, int smem_blocks) {
   constexpr int BB = BS * BS, ST = (BB + 1) & ~1;
+  extern __shared__ __align__(16) double sblk[];
   const bool damp = (omega != 1.0);
   const double om1 = 1.0 - omega;
   double r2 = 0.0;
-  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < B.nblk;
-       b += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t ntiles = (B.nblk + blockDim.x - 1) / blockDim.x;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t b = tile * blockDim.x + threadIdx.x;
+    int64_t s0 = 0;
+    bool staged = false;
+    if (STAGE) {
+      const int64_t bf = tile * blockDim.x;
+      const int64_t bl = min(bf + (int64_t)blockDim.x, B.nblk) - 1;
+      s0 = B.bptr[B.brow[bf]];
+      const int64_t s1 = B.bptr[B.brow[bl] + 1];
+      staged = (s1 - s0) <= smem_blocks;  // uniform over the CTA
+      __syncthreads();                    // the previous tile's readers are done
+      if (staged) {
+        const double2 *src = reinterpret_cast<const double2 *>(old + s0 * ST);
+        double2 *dst = reinterpret_cast<double2 *>(sblk);
+        for (int64_t q = threadIdx.x; q < (s1 - s0) * (ST / 2); q += blockDim.x) dst[q] = src[q];
+      }
+      __syncthreads();
+    }
+    if (b >= B.nblk) continue;
+    const double *lbase = staged ? sblk - s0 * ST : old;  // blocks of the tile's rows
     const int I = B.brow[b], J = B.bcol[b];
     double a[BB];
     ld_block<BB, ST>(ahb + b * ST, a);  // +0.0 for fill entries (R4)
@@ -61,7 +98,7 @@ bsr_sweep_kernel(BsrDev B, const double *__restrict__ ahb, const double *__restr
     for (int64_t t = B.tptr[b]; t < t1; t++) {  // pivot blocks K ascending
       const int2 pr = B.terms[t];
       double L[BB], U[BB];
-      ld_block<BB, ST>(old + (int64_t)pr.x * ST, L);
+      ld_block_any<BB, ST>(lbase + (int64_t)pr.x * ST, L);
       ld_block<BB, ST>(old + (int64_t)pr.y * ST, U);
 #pragma unroll
       for (int d = 0; d < BS; d++)
@@ -74,7 +111,7 @@ bsr_sweep_kernel(BsrDev B, const double *__restrict__ ahb, const double *__restr
         }
     }
     double o[BB], nv[BB];
-    ld_block<BB, ST>(old + b * ST, o);
+    ld_block_any<BB, ST>(lbase + b * ST, o);
     if (J < I) {  // L block: tail k = BS J + c, c < e; divide by u_jj of iterate s-1 (R1)
       double D[BB];
       ld_block<BB, ST>(old + (int64_t)B.bdiag[J] * ST, D);
@@ -119,7 +156,7 @@ bsr_sweep_kernel(BsrDev B, const double *__restrict__ ahb, const double *__restr
           atomicMin(&err->zero_pivot, (unsigned long long)I * BS + d);
     } else {  // U block: tail k = BS I + c, c < d, with the L part of the own diagonal block
       double D[BB];
-      ld_block<BB, ST>(old + (int64_t)B.bdiag[I] * ST, D);
+      ld_block_any<BB, ST>(lbase + (int64_t)B.bdiag[I] * ST, D);
 #pragma unroll
       for (int d = 0; d < BS; d++)
 #pragma unroll
@@ -194,18 +231,49 @@ __global__ void bsr_ahat_kernel(BsrDev B, const int64_t *__restrict__ arp,
     default: return cudaErrorInvalidValue;         \
   }
 
-cudaError_t bsr_sweep_occupancy(int bs, int threads, int *blocks_per_sm) {
-  FASTILU_BS_DISPATCH(bs, return cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                              blocks_per_sm, bsr_sweep_kernel<BS>, threads, 0))
+template <int BS, int MINB>
+static cudaError_t bsr_occ_t(int threads, size_t smem, int *bps) {
+  auto k = smem ? bsr_sweep_kernel<BS, true, MINB> : bsr_sweep_kernel<BS, false, MINB>;
+  if (smem) {
+    cudaError_t e = allow_dynamic_smem((const void *)k);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, k, threads, smem);
+}
+
+// MINB: resident-CTA hint (__launch_bounds__ min blocks): 1 = registers unconstrained, 4 = at
+// most 64 registers (4 x 256 threads per SM)
+cudaError_t bsr_sweep_occupancy(int bs, int threads, size_t smem, int minb, int *blocks_per_sm) {
+  if (minb >= 4) {
+    FASTILU_BS_DISPATCH(bs, return (bsr_occ_t<BS, 4>(threads, smem, blocks_per_sm)))
+  } else {
+    FASTILU_BS_DISPATCH(bs, return (bsr_occ_t<BS, 1>(threads, smem, blocks_per_sm)))
+  }
   return cudaSuccess;
+}
+
+int bsr_block_stride(int bs) { return (bs * bs + 1) & ~1; }
+
+template <int MINB>
+static cudaError_t launch_bsr_t(const BsrDev &B, const double *ahb, const double *old,
+                                double *out, double omega, double *partials, ErrFlags *err,
+                                int grid, int threads, size_t smem, cudaStream_t st) {
+  const int sb = smem ? (int)(smem / (8 * bsr_block_stride(B.bs))) : 0;
+  if (smem) {
+    FASTILU_BS_DISPATCH(B.bs, (bsr_sweep_kernel<BS, true, MINB><<<grid, threads, smem, st>>>(
+                                  B, ahb, old, out, omega, partials, err, sb)))
+  } else {
+    FASTILU_BS_DISPATCH(B.bs, (bsr_sweep_kernel<BS, false, MINB><<<grid, threads, 0, st>>>(
+                                  B, ahb, old, out, omega, partials, err, 0)))
+  }
+  return cudaGetLastError();
 }
 
 cudaError_t launch_bsr_sweep(const BsrDev &B, const double *ahb, const double *old, double *out,
                              double omega, double *partials, ErrFlags *err, int grid,
-                             int threads, cudaStream_t st) {
-  FASTILU_BS_DISPATCH(B.bs, (bsr_sweep_kernel<BS><<<grid, threads, 0, st>>>(
-                                B, ahb, old, out, omega, partials, err)))
-  return cudaGetLastError();
+                             int threads, size_t smem, int minb, cudaStream_t st) {
+  return minb >= 4 ? launch_bsr_t<4>(B, ahb, old, out, omega, partials, err, grid, threads, smem, st)
+                   : launch_bsr_t<1>(B, ahb, old, out, omega, partials, err, grid, threads, smem, st);
 }
 
 static unsigned conv_grid(int64_t nrows) {

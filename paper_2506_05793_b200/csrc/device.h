@@ -167,10 +167,13 @@ struct BsrDev {
   const int64_t *tptr;   // nblk + 1: term range of each target block
   const int2 *terms;     // (block (I,K), block (K,J)), K ascending, K < min(I, J)
 };
-cudaError_t bsr_sweep_occupancy(int bs, int threads, int *blocks_per_sm);
+// smem > 0: stage each tile's block rows in smem bytes of shared memory (when they fit)
+// minb: __launch_bounds__ resident-CTA hint (1 or 4)
+cudaError_t bsr_sweep_occupancy(int bs, int threads, size_t smem, int minb, int *blocks_per_sm);
 cudaError_t launch_bsr_sweep(const BsrDev &B, const double *ahb, const double *old, double *out,
                              double omega, double *partials, ErrFlags *err, int grid,
-                             int threads, cudaStream_t st);
+                             int threads, size_t smem, int minb, cudaStream_t st);
+int bsr_block_stride(int bs);
 cudaError_t launch_bsr_from_csr(const BsrDev &B, const int64_t *rp, const double *vals,
                                 double *vb, int64_t nrows, cudaStream_t st);
 cudaError_t launch_bsr_to_csr(const BsrDev &B, const int64_t *rp, const double *vb, double *vals,
@@ -179,5 +182,7 @@ cudaError_t launch_bsr_ahat(const BsrDev &B, const int64_t *arp, const int32_t *
                             const double *ahatA, double *ahb, int64_t nrows, cudaStream_t st);
 
 int sm_count(int device);
+// raise a kernel's dynamic shared memory limit to the device's opt-in maximum
+cudaError_t allow_dynamic_smem(const void *func);
 
 }  // namespace fastilu

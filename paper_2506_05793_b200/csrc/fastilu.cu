@@ -81,6 +81,8 @@ struct fastilu_handle_s {
   int2 *d_terms = nullptr;
   double *d_vb[2] = {nullptr, nullptr}, *d_ahb = nullptr;
   int bsr_grid = 0, bsr_threads = 256;
+  size_t bsr_smem = 0;
+  int bsr_minb = 1;
   int64_t bsr_nterms = 0;
   // fused multi-sweep compute (template path, single GPU): iterates 0..ns in pool buffers
   void *jit_fused = nullptr;
@@ -118,6 +120,7 @@ struct fastilu_handle_s {
   std::vector<double> resid;
   cudaEvent_t ev[5] = {};
   float t_init = 0.f, t_sweeps = 0.f, t_apply = 0.f;
+  bool apply_timed = false;  // ev[3] / ev[4] recorded by an apply
   Comm *comm = nullptr;
 };
 
@@ -577,11 +580,21 @@ static fastilu_status create_impl(fastilu_handle h, int64_t n, const int64_t *ro
   for (int64_t r = h->G; r < h->nloc; r++) nl_own += dloc[r];
   const double nl_avg = n ? (double)nl_own / n : 1.0;
   const double u_avg = n ? (double)(h->nnz_own - n - nl_own) / n : 1.0;
+  // block-dense patterns (3-dof elasticity type): block sweep with host-built term lists
+  // (single GPU; measured faster than the template layout on these patterns)
+  BlockPattern bp;
+  if (!multi && !std::getenv("FASTILU_NO_BSR")) {
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    const int64_t max_terms = (int64_t)(fr / 4 / 8);  // term list <= a quarter of free memory
+    h->bsr = build_blocks(rp, ci, h->nloc, nt, max_terms, bp);
+  }
   // template-SELL fast path for structured patterns (else the CSR kernels below)
   {
     std::vector<unsigned long long> tmask;
     std::vector<int32_t> tasrc;
-    bool ok = !std::getenv("FASTILU_NO_TSELL") && (!multi || (n % 32 == 0 && h->G % 32 == 0)) &&
+    bool ok = !h->bsr && !std::getenv("FASTILU_NO_TSELL") &&
+              (!multi || (n % 32 == 0 && h->G % 32 == 0)) &&
               jit_available(nullptr) &&
               build_template(rp, ci, h->nloc, arp, aci, nt, h->T, tmask, tasrc);
     if (multi) {  // all ranks must agree on the layout (and on the template itself)
@@ -608,14 +621,6 @@ static fastilu_status create_impl(fastilu_handle h, int64_t n, const int64_t *ro
         h->d_lmask.push_back(d);
       }
     }
-  }
-  // block-dense patterns (3-dof elasticity type): block sweep with host-built term lists
-  BlockPattern bp;
-  if (!h->tsell && !multi && !std::getenv("FASTILU_NO_BSR")) {
-    size_t fr = 0, tot = 0;
-    cudaMemGetInfo(&fr, &tot);
-    const int64_t max_terms = (int64_t)(fr / 4 / 8);  // term list <= a quarter of free memory
-    h->bsr = build_blocks(rp, ci, h->nloc, nt, max_terms, bp);
   }
   // structure classes for the class-program sweep (falls back to the hash kernel if absent)
   ClassProgram cp;
@@ -655,8 +660,16 @@ static fastilu_status create_impl(fastilu_handle h, int64_t n, const int64_t *ro
     h->bsr_nterms = bp.nterms;
     h->B = BsrDev{bp.bs,     bp.nb,      bp.nblk,     h->d_bptr, h->d_brow,
                   h->d_bcol, h->d_bdiag, h->d_tptr,   h->d_terms};
+    // options measured on the Table-6 problem and 3-dof 48^3 ILU(1/2): staging
+    // the tile's block rows in shared memory (FASTILU_BSR_SMEM_KB) costs L1 capacity and is
+    // slower, so off; 4 resident CTAs (64 registers, FASTILU_BSR_MINB) beat 3 (80 registers).
+    const char *sk = std::getenv("FASTILU_BSR_SMEM_KB");
+    h->bsr_smem = (size_t)(sk ? atoi(sk) : 0) * 1024;
+    const char *mb = std::getenv("FASTILU_BSR_MINB");
+    h->bsr_minb = mb ? atoi(mb) : 4;
     int bps = 0;
-    if (bsr_sweep_occupancy(bp.bs, h->bsr_threads, &bps) != cudaSuccess || bps < 1)
+    if (bsr_sweep_occupancy(bp.bs, h->bsr_threads, h->bsr_smem, h->bsr_minb, &bps) !=
+            cudaSuccess || bps < 1)
       return FASTILU_ERR_CUDA;
     h->bsr_grid = (int)std::max<int64_t>(
         1, std::min<int64_t>((int64_t)sm_count(h->device) * bps,
@@ -887,6 +900,7 @@ static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, i
   }
   if (!h->have_values || !h->d_aval) FAIL(FASTILU_ERR_STATE);
   cudaSetDevice(h->device);
+  (void)cudaGetLastError();  // clear a non-sticky error left by the caller's own CUDA work
   h->computed = false;
   h->err_index = -1;
   cudaStream_t st = h->stream;
@@ -997,7 +1011,8 @@ static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, i
     }
     if (h->bsr) {
       CU(launch_bsr_sweep(h->B, h->d_ahb, h->d_vb[ib], h->d_vb[ob], h->opt.omega, h->d_partials,
-                          h->d_err, h->bsr_grid, h->bsr_threads, st));
+                          h->d_err, h->bsr_grid, h->bsr_threads, h->bsr_smem, h->bsr_minb,
+                          st));
       CU(launch_reduce(h->d_partials, h->bsr_grid, h->d_r2 + (sw - 1), st));
       continue;
     }
@@ -1149,10 +1164,12 @@ extern "C" fastilu_status fastilu_apply(fastilu_handle h, const double *b, doubl
   if (!h || ntrisweeps < 1 || (h->n > 0 && (!b || !x))) FAIL(FASTILU_ERR_INVALID_ARG);
   if (!h->computed) FAIL(FASTILU_ERR_STATE);
   cudaSetDevice(h->device);
+  (void)cudaGetLastError();  // clear a non-sticky error left by the caller's own CUDA work
   CU(cudaEventRecord(h->ev[3], h->stream));
   fastilu_status s = apply_impl(h, b, x, ntrisweeps);
   if (s) return s;
   CU(cudaEventRecord(h->ev[4], h->stream));
+  h->apply_timed = true;
   return FASTILU_OK;
 }
 
@@ -1161,12 +1178,14 @@ extern "C" fastilu_status fastilu_apply_host(fastilu_handle h, const double *b, 
   if (!h || ntrisweeps < 1 || (h->n > 0 && (!b || !x))) FAIL(FASTILU_ERR_INVALID_ARG);
   if (!h->computed) FAIL(FASTILU_ERR_STATE);
   cudaSetDevice(h->device);
+  (void)cudaGetLastError();  // clear a non-sticky error left by the caller's own CUDA work
   if (!h->d_bx) CU(dalloc(&h->d_bx, 2 * h->n));
   CU(cudaMemcpyAsync(h->d_bx, b, sizeof(double) * h->n, cudaMemcpyHostToDevice, h->stream));
   CU(cudaEventRecord(h->ev[3], h->stream));
   fastilu_status s = apply_impl(h, h->d_bx, h->d_bx + h->n, ntrisweeps);
   if (s) return s;
   CU(cudaEventRecord(h->ev[4], h->stream));
+  h->apply_timed = true;
   CU(cudaMemcpyAsync(x, h->d_bx + h->n, sizeof(double) * h->n, cudaMemcpyDeviceToHost,
                      h->stream));
   CU(cudaStreamSynchronize(h->stream));
@@ -1187,6 +1206,7 @@ extern "C" fastilu_status fastilu_gmres(fastilu_handle h, const double *b, doubl
     FAIL(FASTILU_ERR_INVALID_ARG);
   if (!h->computed) FAIL(FASTILU_ERR_STATE);
   cudaSetDevice(h->device);
+  (void)cudaGetLastError();  // clear a non-sticky error left by the caller's own CUDA work
   cudaStream_t st = h->stream;
   const int64_t n = h->n;
   const int m = restart;
@@ -1306,6 +1326,7 @@ extern "C" fastilu_status fastilu_gmres(fastilu_handle h, const double *b, doubl
     if ((fs = nrm(r, &beta))) return fs;
   }
   CU(cudaEventRecord(h->ev[4], st));
+  h->apply_timed = true;
   CU(cudaStreamSynchronize(st));
   if (iters_out) *iters_out = total;
   if (relres_out) *relres_out = bnorm > 0.0 ? beta / bnorm : 0.0;
@@ -1343,6 +1364,7 @@ extern "C" fastilu_status fastilu_get_factors(fastilu_handle h, double *vals, do
   if (!h) FAIL(FASTILU_ERR_INVALID_ARG);
   if (!h->computed) FAIL(FASTILU_ERR_STATE);
   cudaSetDevice(h->device);
+  (void)cudaGetLastError();  // clear a non-sticky error left by the caller's own CUDA work
   CU(cudaStreamSynchronize(h->stream));
   if (vals && h->tsell) {  // gather the owned rows' S entries out of the template slots
     const Template &T = h->T;
@@ -1377,7 +1399,11 @@ extern "C" fastilu_status fastilu_get_timings(fastilu_handle h, double *t3) {
   if (!h || !t3) FAIL(FASTILU_ERR_INVALID_ARG);
   cudaSetDevice(h->device);
   float ta = 0.f;
-  if (cudaEventQuery(h->ev[4]) == cudaSuccess) cudaEventElapsedTime(&ta, h->ev[3], h->ev[4]);
+  if (h->apply_timed && cudaEventQuery(h->ev[4]) == cudaSuccess &&
+      cudaEventElapsedTime(&ta, h->ev[3], h->ev[4]) != cudaSuccess) {
+    (void)cudaGetLastError();  // never leave a non-sticky error behind for the next launch check
+    ta = 0.f;
+  }
   t3[0] = h->t_init;
   t3[1] = h->t_sweeps;
   t3[2] = ta;
@@ -1396,9 +1422,10 @@ extern "C" fastilu_status fastilu_get_info(fastilu_handle h, char *buf, int cap)
              h->t_spill, (long long)h->t_ntiles, h->t_sstride, (long long)h->G, (long long)h->H);
   else if (h->bsr)
     snprintf(tmp, sizeof(tmp),
-             "path=bsr%d blocks=%lld terms=%lld threads=%d grid=%d tri_lanes=%d G=%lld H=%lld",
+             "path=bsr%d blocks=%lld terms=%lld threads=%d grid=%d smem_kb=%d minb=%d "
+             "tri_lanes=%d G=%lld H=%lld",
              h->B.bs, (long long)h->B.nblk, (long long)h->bsr_nterms,
-             h->bsr_threads, h->bsr_grid, h->G_tri, (long long)h->G, (long long)h->H);
+             h->bsr_threads, h->bsr_grid, (int)(h->bsr_smem / 1024), h->bsr_minb, h->G_tri, (long long)h->G, (long long)h->H);
   else
     snprintf(tmp, sizeof(tmp),
              "path=%s G_lanes=%d E=%d threads=%d grid=%d classes=%lld tri_lanes=%d G=%lld H=%lld",

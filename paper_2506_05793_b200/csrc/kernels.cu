@@ -21,6 +21,21 @@ namespace cg = cooperative_groups;
 
 namespace fastilu {
 
+// The dynamic-smem limit is a property of the kernel function, shared by every handle: raise it
+// to the device's opt-in maximum (monotone) instead of the calling handle's need, so a handle
+// configured later with less shared memory cannot break the launches of an earlier one.
+cudaError_t allow_dynamic_smem(const void *func) {
+  int dev = 0, mx = 0;
+  cudaGetDevice(&dev);
+  cudaError_t e = cudaDeviceGetAttribute(&mx, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (e != cudaSuccess) return e;
+  cudaFuncAttributes fa{};
+  e = cudaFuncGetAttributes(&fa, func);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              mx - (int)fa.sharedSizeBytes);  // static + dynamic <= opt-in max
+}
+
 int sm_count(int device) {
   int v = 0;
   cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
@@ -283,9 +298,7 @@ static cudaError_t launch_sweep_t(const SweepArgs &a, const SweepCfg &c, cudaStr
 
 template <int G, bool HASH>
 static cudaError_t sweep_attr_t(const SweepCfg &c, int *blocks_per_sm) {
-  cudaError_t e = cudaFuncSetAttribute(sweep_kernel<G, HASH>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)(c.smem > 0 ? c.smem : 1));
+  cudaError_t e = allow_dynamic_smem((const void *)sweep_kernel<G, HASH>);
   if (e != cudaSuccess) return e;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, sweep_kernel<G, HASH>,
                                                        c.threads, c.smem);
@@ -462,9 +475,7 @@ static cudaError_t launch_prog_t(const SweepArgs &a, const ProgView &pv, const S
 
 template <int G, int E>
 static cudaError_t prog_attr_t(const SweepCfg &c, int *bps) {
-  cudaError_t e = cudaFuncSetAttribute(sweep_prog_kernel<G, E>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)(c.smem > 0 ? c.smem : 1));
+  cudaError_t e = allow_dynamic_smem((const void *)sweep_prog_kernel<G, E>);
   if (e != cudaSuccess) return e;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, sweep_prog_kernel<G, E>, c.threads,
                                                        c.smem);

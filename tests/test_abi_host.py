@@ -89,3 +89,14 @@ def test_create_without_gpu_fails_loudly():
     with pytest.raises(F.FastILUError) as ei:
         F.FastILU(a.row_ptr, a.col_idx, a.values, 0)
     assert ei.value.status == "CUDA"
+
+
+def test_bench_block_flop_count_matches_survey():
+    """bench.py's flop count for the block path reproduces SURVEY Sec. 8(d)'s independent count
+    for the Table-6 problem (3,537,519,556 terms per sweep) from the block-term total that the
+    library reports for it (129,330,412 pivot-block terms over 5,081,056 blocks)."""
+    import bench
+    info = "path=bsr3 blocks=5081056 terms=129330412 threads=256"
+    r = bench.bsr_roofline(info, 98304, 1.0)
+    assert r["terms_per_sweep"] == 3537519556
+    assert r["bound"] == "alu" and r["unit"] == "TFLOP/s"

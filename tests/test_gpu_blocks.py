@@ -78,3 +78,16 @@ def test_table6_problem_block_vs_scalar_kernel(monkeypatch):
     assert v1.size == 45729504
     assert np.array_equal(v1, v2)
     np.testing.assert_allclose(h1, g.residual_history(), rtol=1e-9)
+
+
+def test_handles_with_different_smem_configs(monkeypatch):
+    """The dynamic shared-memory limit is per kernel function: a handle configured later with
+    less shared memory must not break an earlier handle's launches (regression)."""
+    a = P.elasticity_pattern_3dof(6)
+    monkeypatch.setenv("FASTILU_BSR_SMEM_KB", "32")
+    f = F.FastILU(a.row_ptr, a.col_idx, a.values, 2)
+    monkeypatch.setenv("FASTILU_BSR_SMEM_KB", "8")
+    g = F.FastILU(a.row_ptr, a.col_idx, a.values, 2)
+    for h in (f, g, f):
+        h.compute(3)
+    assert np.array_equal(f.factors()[0], g.factors()[0])

@@ -214,6 +214,17 @@ def test_determinism_and_set_values():
     assert np.array_equal(f.factors()[0], v1)
 
 
+def test_timings_before_any_apply():
+    """fastilu_get_timings before the first apply must not leave a CUDA error behind that a
+    later launch check would report (regression)."""
+    a = P.laplace3d_27pt(6)
+    f = F.FastILU(a.row_ptr, a.col_idx, a.values, 1)
+    for _ in range(3):
+        f.compute(2)
+        t = f.timings()
+        assert t["apply_ms"] == 0.0 and t["sweeps_ms"] > 0.0
+
+
 def test_tiny_and_diagonal():
     full_check(P.Csr([0, 1], [0], [4.0]), 0, 2, 2)
     n = 37
