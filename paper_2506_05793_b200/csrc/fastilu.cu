@@ -99,6 +99,7 @@ struct fastilu_handle_s {
   int tri_cap = 0, tri_grid = 0;
   std::vector<unsigned long long *> d_lmask;  // warm-up: presence masks of levels 0..K-1
   void *jit_sweep = nullptr;
+  void *jit_sweep_first = nullptr;  // sweep 1 from iterate 0: A x A terms only
   void *jit_sweep_async = nullptr;  // compiled on the first asynchronous compute
   int t_parts = 1, t_minb = 0, t_sstride = 1;
   bool t_prefetch = true;
@@ -387,6 +388,11 @@ static fastilu_status setup_tsell(fastilu_handle h, const std::vector<unsigned l
   if (jit_get(src, "fastilu_tsell_sweep", h->device, &h->jit_sweep, &log)) {
     if (std::getenv("FASTILU_DEBUG")) fprintf(stderr, "fastilu: JIT failed: %s\n", log.c_str());
     FAIL(FASTILU_ERR_UNSUPPORTED);
+  }
+  if (!std::getenv("FASTILU_NO_FIRST_SWEEP")) {
+    const std::string s1 = sweep_source(T, threads, parts, minb, false, pf, false, true);
+    if (jit_get(s1, "fastilu_tsell_sweep_first", h->device, &h->jit_sweep_first, &log))
+      FAIL(FASTILU_ERR_UNSUPPORTED);
   }
   int bps = 0;
   jit_func_info(h->jit_sweep, &h->t_regs, &h->t_spill, threads, &bps);
@@ -1002,7 +1008,10 @@ static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, i
       unsigned int *ctr = h->d_counter;
       int sstr = h->t_sstride;
       void *args[] = {&old, &outp, &ahat, &mk, &udo, &udn, &a0, &a1, &om, &part, &zp, &ctr, &sstr};
-      if (jit_launch(async ? h->jit_sweep_async : h->jit_sweep, h->t_grid, h->t_threads, st,
+      void *fn = async ? h->jit_sweep_async
+                 : (sw == 1 && !warmup && h->jit_sweep_first) ? h->jit_sweep_first
+                                                              : h->jit_sweep;
+      if (jit_launch(fn, h->t_grid, h->t_threads, st,
                      args))
         return FASTILU_ERR_CUDA;
       CU(launch_reduce_reset(h->d_partials, (int)h->t_ntiles, h->d_r2 + (sw - 1), h->d_counter,

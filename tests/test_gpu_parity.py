@@ -305,3 +305,19 @@ def test_fused_wavefront_equals_per_sweep_kernels(kind, g, k, ns, nt, monkeypatc
     fo = oracle.compute(a, k, ns)
     assert np.array_equal(v1, fo.vals)
     assert np.array_equal(x1, oracle.apply(fo, b, nt))
+
+
+@pytest.mark.parametrize("kind,g,k,omega", [("27pt", 10, 1, 1.0), ("27pt", 9, 2, 0.7),
+                                             ("7pt", 12, 1, 1.0)])
+def test_first_sweep_kernel_equals_full_sweep(kind, g, k, omega, monkeypatch):
+    """Sweep 1 from iterate 0 runs a kernel restricted to the terms whose operands lie on A's
+    sub-template (fill entries of iterate 0 are exactly +0.0); it must equal the full sweep."""
+    a = P.make(kind, g)
+    f = F.FastILU(a.row_ptr, a.col_idx, a.values, k, omega=omega)
+    f.compute(2)
+    monkeypatch.setenv("FASTILU_NO_FIRST_SWEEP", "1")
+    h = F.FastILU(a.row_ptr, a.col_idx, a.values, k, omega=omega)
+    h.compute(2)
+    assert f.info().startswith("path=tsell") and h.info().startswith("path=tsell")
+    assert np.array_equal(f.factors()[0], h.factors()[0])
+    np.testing.assert_array_equal(f.residual_history(), h.residual_history())
