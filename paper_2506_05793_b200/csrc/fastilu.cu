@@ -101,6 +101,14 @@ struct fastilu_handle_s {
   void *jit_sweep = nullptr;
   void *jit_sweep_first = nullptr;  // sweep 1 from iterate 0: A x A terms only
   void *jit_sweep_async = nullptr;  // compiled on the first asynchronous compute
+  // staged sweep (tsell.h StagedCfg): pivot rows through shared memory by TMA
+  void *jit_st = nullptr, *jit_st_first = nullptr;
+  StagedCfg st{};
+  int st_grid = 0;
+  int64_t st_ntiles = 0;
+  struct alignas(64) TMapBuf {
+    unsigned char b[128];
+  } st_tmap[2];  // one tensor map per iterate buffer d_vals[0/1]
   int t_parts = 1, t_minb = 0, t_sstride = 1;
   bool t_prefetch = true;
   int t_threads = 128, t_grid = 1, t_regs = 0, t_spill = 0, t_rows_tile = 128;
@@ -394,6 +402,39 @@ static fastilu_status setup_tsell(fastilu_handle h, const std::vector<unsigned l
     if (jit_get(s1, "fastilu_tsell_sweep_first", h->device, &h->jit_sweep_first, &log))
       FAIL(FASTILU_ERR_UNSUPPORTED);
   }
+  // staged sweep: default for templates with more than one pivot row per line of pivots
+  // (27-pt ILU(k)); FASTILU_TSELL_STAGED=0/1 overrides
+  {
+    const char *ev = std::getenv("FASTILU_TSELL_STAGED");
+    const bool want = ev ? atoi(ev) != 0 : T.W > 16;
+    if (want) {
+      const char *ev_st = std::getenv("FASTILU_TSELL_STAGES");
+      const char *ev_sp = std::getenv("FASTILU_TSELL_ST_PARTS");
+      const int nst = ev_st ? std::max(2, atoi(ev_st)) : 2;
+      // ~32 targets per thread: 2 part-warps per slice for W = 63, 4 for W = 115
+      const int sparts = ev_sp ? std::max(1, atoi(ev_sp)) : std::max(1, (T.W + 31) / 32);
+      const int sthreads = 128 * sparts;  // 128-row tiles
+      const char *ev_smb = std::getenv("FASTILU_TSELL_ST_MINB");
+      const int sminb = ev_smb ? atoi(ev_smb) : 0;
+      StagedCfg c{};
+      const std::string s0 = sweep_source_staged(T, sthreads, sparts, nst, sminb, false, &c);
+      const std::string s1 = sweep_source_staged(T, sthreads, sparts, nst, sminb, true, nullptr);
+      int sbps = 0;
+      if (!jit_get(s0, "fastilu_tsell_sweep_st", h->device, &h->jit_st, &log) &&
+          !jit_get(s1, "fastilu_tsell_sweep_st_first", h->device, &h->jit_st_first, &log) &&
+          !jit_set_smem(h->jit_st, c.smem) && !jit_set_smem(h->jit_st_first, c.smem) &&
+          !jit_occupancy(h->jit_st, c.threads, c.smem, &sbps) && sbps > 0) {
+        h->st = c;
+        const int64_t nsl_own = (h->n + 31) / 32, spt = c.rows / 32;
+        h->st_ntiles = std::max<int64_t>(1, (nsl_own + spt - 1) / spt);
+        h->st_grid = (int)std::min<int64_t>((int64_t)sm_count(h->device) * sbps, h->st_ntiles);
+      } else {
+        if (std::getenv("FASTILU_DEBUG"))
+          fprintf(stderr, "fastilu: staged sweep unavailable: %s\n", log.c_str());
+        h->jit_st = h->jit_st_first = nullptr;
+      }
+    }
+  }
   int bps = 0;
   jit_func_info(h->jit_sweep, &h->t_regs, &h->t_spill, threads, &bps);
   if (std::getenv("FASTILU_DEBUG"))
@@ -430,7 +471,15 @@ static fastilu_status setup_tsell(fastilu_handle h, const std::vector<unsigned l
   CU(dalloc(&h->d_toffA, T.WA));
   CU(dalloc(&h->d_tw2a, T.W));
   CU(dalloc(&h->d_counter, 1));
-  CU(dalloc(&h->d_partials, std::max<int64_t>(h->t_ntiles, kSumsqBlocks)));
+  CU(dalloc(&h->d_partials,
+            std::max<int64_t>(std::max(h->t_ntiles, h->st_ntiles), kSumsqBlocks)));
+  if (h->jit_st)
+    for (int b = 0; b < 2; b++)
+      if (jit_tmap_sell(h->st_tmap[b].b, h->d_vals[b], T.W, h->nsl, h->st.box_cols,
+                        h->st.box_slices)) {
+        if (std::getenv("FASTILU_DEBUG")) fprintf(stderr, "fastilu: tensor map failed\n");
+        h->jit_st = h->jit_st_first = nullptr;
+      }
   CU(cudaMemset(h->d_counter, 0, sizeof(unsigned int)));
   CU(cudaMemcpy(h->d_tmask, mask.data(), 8 * mask.size(), cudaMemcpyHostToDevice));
   CU(cudaMemcpy(h->d_tasrc, asrc.data(), 4 * asrc.size(), cudaMemcpyHostToDevice));
@@ -1007,6 +1056,16 @@ static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, i
       unsigned long long *zp = &h->d_err->zero_pivot;
       unsigned int *ctr = h->d_counter;
       int sstr = h->t_sstride;
+      if (h->jit_st && !async) {
+        void *sargs[] = {&old, &outp, &ahat, &mk, &udn, &a0, &a1, &om, &part, &zp, &ctr,
+                         h->st_tmap[ib].b};
+        void *fn = (sw == 1 && !warmup && h->jit_st_first) ? h->jit_st_first : h->jit_st;
+        if (jit_launch_smem(fn, h->st_grid, h->st.threads, h->st.smem, st, sargs))
+          return FASTILU_ERR_CUDA;
+        CU(launch_reduce_reset(h->d_partials, (int)h->st_ntiles, h->d_r2 + (sw - 1),
+                               h->d_counter, st));
+        continue;
+      }
       void *args[] = {&old, &outp, &ahat, &mk, &udo, &udn, &a0, &a1, &om, &part, &zp, &ctr, &sstr};
       void *fn = async ? h->jit_sweep_async
                  : (sw == 1 && !warmup && h->jit_sweep_first) ? h->jit_sweep_first
@@ -1429,7 +1488,16 @@ extern "C" fastilu_status fastilu_get_info(fastilu_handle h, char *buf, int cap)
              h->T.W, h->T.c0, h->T.WA, h->T.terms.size(), h->t_threads, h->t_rows_tile,
              h->t_grid, h->t_regs,
              h->t_spill, (long long)h->t_ntiles, h->t_sstride, (long long)h->G, (long long)h->H);
-  else if (h->bsr)
+  if (h->tsell && h->jit_st) {
+    const size_t L = strlen(tmp);
+    snprintf(tmp + L, sizeof(tmp) - L,
+             " staged=1 st_threads=%d st_parts=%d st_rows=%d st_groups=%d st_box=32x%dx%d "
+             "st_stages=%d st_smem_kb=%d st_grid=%d",
+             h->st.threads, h->st.parts, h->st.rows, h->st.ngroups, h->st.box_cols,
+             h->st.box_slices, h->st.stages, h->st.smem / 1024, h->st_grid);
+  }
+  if (h->tsell) {
+  } else if (h->bsr)
     snprintf(tmp, sizeof(tmp),
              "path=bsr%d blocks=%lld terms=%lld threads=%d grid=%d smem_kb=%d minb=%d "
              "tri_lanes=%d G=%lld H=%lld",

@@ -38,6 +38,12 @@ struct Api {
   CUresult (*FuncGetAttribute)(int *, CUfunction_attribute, CUfunction) = nullptr;
   CUresult (*OccupancyMaxActiveBlocksPerMultiprocessor)(int *, CUfunction, int,
                                                         size_t) = nullptr;
+  CUresult (*FuncSetAttribute)(CUfunction, CUfunction_attribute, int) = nullptr;
+  CUresult (*TensorMapEncodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                   const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                   const cuuint32_t *, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                   CUtensorMapFloatOOBfill) = nullptr;
 };
 
 Api &api() {
@@ -75,6 +81,8 @@ Api &api() {
     DR(LaunchKernel);
     DR(FuncGetAttribute);
     DR(OccupancyMaxActiveBlocksPerMultiprocessor);
+    DR(FuncSetAttribute);
+    DR(TensorMapEncodeTiled);
 #undef DR
     a.ok = a.CreateProgram && a.CompileProgram && a.GetCUBINSize && a.GetCUBIN &&
            a.DestroyProgram && a.ModuleLoadData && a.ModuleGetFunction && a.LaunchKernel &&
@@ -148,6 +156,51 @@ int jit_launch(void *fn, int grid, int block, void *stream, void **args) {
                         nullptr) == CUDA_SUCCESS
              ? 0
              : 1;
+}
+
+int jit_set_smem(void *fn, int bytes) {
+  Api &a = api();
+  if (!a.FuncSetAttribute) return 1;
+  return a.FuncSetAttribute((CUfunction)fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
+                            bytes) == CUDA_SUCCESS
+             ? 0
+             : 2;
+}
+
+int jit_launch_smem(void *fn, int grid, int block, int smem, void *stream, void **args) {
+  Api &a = api();
+  return a.LaunchKernel((CUfunction)fn, grid, 1, 1, block, 1, 1, (unsigned)smem,
+                        (CUstream)stream, args, nullptr) == CUDA_SUCCESS
+             ? 0
+             : 1;
+}
+
+int jit_occupancy(void *fn, int block, int smem, int *blocks_per_sm) {
+  Api &a = api();
+  *blocks_per_sm = 0;
+  return a.OccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, (CUfunction)fn, block,
+                                                     (size_t)smem) == CUDA_SUCCESS
+             ? 0
+             : 1;
+}
+
+int jit_tmap_sell(void *out, const double *base, int W, long long nsl, int box_cols,
+                  int box_slices) {
+  Api &a = api();
+  if (!a.TensorMapEncodeTiled) return 1;
+  if ((reinterpret_cast<uintptr_t>(out) & 63) || (reinterpret_cast<uintptr_t>(base) & 15))
+    return 2;
+  const cuuint64_t dims[3] = {32, (cuuint64_t)W, (cuuint64_t)nsl};
+  const cuuint64_t strides[2] = {256, (cuuint64_t)W * 256};
+  const cuuint32_t box[3] = {32, (cuuint32_t)box_cols, (cuuint32_t)box_slices};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return a.TensorMapEncodeTiled(reinterpret_cast<CUtensorMap *>(out),
+                                CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void *)base, dims, strides,
+                                box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS
+             ? 0
+             : 3;
 }
 
 int jit_func_info(void *fn, int *regs, int *local_bytes, int block, int *blocks_per_sm) {

@@ -10,5 +10,15 @@ bool jit_available(std::string *why);
 int jit_get(const std::string &src, const char *name, int device, void **fn, std::string *log);
 int jit_launch(void *fn, int grid, int block, void *stream, void **args);
 int jit_func_info(void *fn, int *regs, int *local_bytes, int block, int *blocks_per_sm);
+// Dynamic shared memory: raise the function's limit to `bytes`, launch with `smem` bytes and
+// query the resident blocks per SM at that size.
+int jit_set_smem(void *fn, int bytes);
+int jit_launch_smem(void *fn, int grid, int block, int smem, void *stream, void **args);
+int jit_occupancy(void *fn, int block, int smem, int *blocks_per_sm);
+// 3D TMA tensor map (128 bytes, 64-byte aligned `out`) over a template-SELL array of fp64:
+// dims {32 rows of a slice, W columns, nsl slices}, strides {256 B, W * 256 B}, box
+// {32, box_cols, box_slices}; out-of-range boxes are zero-filled.  0 on success.
+int jit_tmap_sell(void *out, const double *base, int W, long long nsl, int box_cols,
+                  int box_slices);
 
 }  // namespace fastilu
