@@ -413,12 +413,23 @@ static fastilu_status setup_tsell(fastilu_handle h, const std::vector<unsigned l
       const int nst = ev_st ? std::max(2, atoi(ev_st)) : 2;
       // ~32 targets per thread: 2 part-warps per slice for W = 63, 4 for W = 115
       const int sparts = ev_sp ? std::max(1, atoi(ev_sp)) : std::max(1, (T.W + 31) / 32);
-      const int sthreads = 128 * sparts;  // 128-row tiles
+      const char *ev_sth = std::getenv("FASTILU_TSELL_ST_THREADS");
+      // 256-row tiles (one 512-thread block per SM) for 2 parts, 128-row tiles for more
+      // (shared memory: the stage box grows with the template's upper width); measured
+      // 15.9 vs 16.8 ms (c4, 3 sweeps) and equal for ILU(2)
+      const int sthreads =
+          ev_sth ? std::max(32 * sparts, atoi(ev_sth) / (32 * sparts) * 32 * sparts)
+                 : (sparts <= 2 ? 256 * sparts : 128 * sparts);
+      const char *ev_so = std::getenv("FASTILU_TSELL_ST_OPTS");
+      const unsigned sopts = (ev_so ? (unsigned)atoi(ev_so) : 0u) |
+                             (h->opt.omega != 1.0 ? kStagedDamp : 0u);
       const char *ev_smb = std::getenv("FASTILU_TSELL_ST_MINB");
       const int sminb = ev_smb ? atoi(ev_smb) : 0;
       StagedCfg c{};
-      const std::string s0 = sweep_source_staged(T, sthreads, sparts, nst, sminb, false, &c);
-      const std::string s1 = sweep_source_staged(T, sthreads, sparts, nst, sminb, true, nullptr);
+      const std::string s0 =
+          sweep_source_staged(T, sthreads, sparts, nst, sminb, false, &c, sopts);
+      const std::string s1 =
+          sweep_source_staged(T, sthreads, sparts, nst, sminb, true, nullptr, sopts);
       int sbps = 0;
       if (!jit_get(s0, "fastilu_tsell_sweep_st", h->device, &h->jit_st, &log) &&
           !jit_get(s1, "fastilu_tsell_sweep_st_first", h->device, &h->jit_st_first, &log) &&
