@@ -436,8 +436,7 @@ static fastilu_status setup_tsell(fastilu_handle h, const std::vector<unsigned l
           !jit_set_smem(h->jit_st, c.smem) && !jit_set_smem(h->jit_st_first, c.smem) &&
           !jit_occupancy(h->jit_st, c.threads, c.smem, &sbps) && sbps > 0) {
         h->st = c;
-        const int64_t nsl_own = (h->n + 31) / 32, spt = c.rows / 32;
-        h->st_ntiles = std::max<int64_t>(1, (nsl_own + spt - 1) / spt);
+        h->st_ntiles = std::max<int64_t>(1, (h->n + c.shift + c.rows - 1) / c.rows);
         h->st_grid = (int)std::min<int64_t>((int64_t)sm_count(h->device) * sbps, h->st_ntiles);
       } else {
         if (std::getenv("FASTILU_DEBUG"))
@@ -1502,9 +1501,9 @@ extern "C" fastilu_status fastilu_get_info(fastilu_handle h, char *buf, int cap)
   if (h->tsell && h->jit_st) {
     const size_t L = strlen(tmp);
     snprintf(tmp + L, sizeof(tmp) - L,
-             " staged=1 st_threads=%d st_parts=%d st_rows=%d st_groups=%d st_box=32x%dx%d "
-             "st_stages=%d st_smem_kb=%d st_grid=%d",
-             h->st.threads, h->st.parts, h->st.rows, h->st.ngroups, h->st.box_cols,
+             " staged=1 st_threads=%d st_parts=%d st_rows=%d st_shift=%d st_groups=%d "
+             "st_box=32x%dx%d st_stages=%d st_smem_kb=%d st_grid=%d",
+             h->st.threads, h->st.parts, h->st.rows, h->st.shift, h->st.ngroups, h->st.box_cols,
              h->st.box_slices, h->st.stages, h->st.smem / 1024, h->st_grid);
   }
   if (h->tsell) {
