@@ -111,7 +111,7 @@ cudaError_t launch_tsell_gather_a(const TDev &t, const double *aval, int64_t nro
 cudaError_t launch_tsell_init(const TDev &t, const double *aT, const double *s,
                               const double *ad, int64_t r0, int64_t r1, double *ahatT,
                               double *vals, double *udiag, ErrFlags *err, double shift,
-                              cudaStream_t st);
+                              cudaStream_t st, bool iter0 = true);
 cudaError_t launch_tsell_jacobi(const TDev &t, bool lower, const double *vals,
                                 const double *udiag, const double *rhs, const double *xo,
                                 double *xn, double *xfinal, const double *s, int64_t r0,

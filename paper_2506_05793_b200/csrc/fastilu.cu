@@ -103,12 +103,15 @@ struct fastilu_handle_s {
   void *jit_sweep_async = nullptr;  // compiled on the first asynchronous compute
   // staged sweep (tsell.h StagedCfg): pivot rows through shared memory by TMA
   void *jit_st = nullptr, *jit_st_first = nullptr;
-  StagedCfg st{};
+  void *jit_st_init = nullptr;  // sweep 1 with iterate 0 computed from ahat (single GPU)
+  void *jit_tri[2] = {nullptr, nullptr};  // wavefront trisolve L / U (single GPU)
+  int tri_jgrid = 0;
+  StagedCfg st{}, st_init{};
   int st_grid = 0;
   int64_t st_ntiles = 0;
   struct alignas(64) TMapBuf {
     unsigned char b[128];
-  } st_tmap[2];  // one tensor map per iterate buffer d_vals[0/1]
+  } st_tmap[2], st_tmap_ahat;  // per iterate buffer d_vals[0/1]; over d_ahat
   int t_parts = 1, t_minb = 0, t_sstride = 1;
   bool t_prefetch = true;
   int t_threads = 128, t_grid = 1, t_regs = 0, t_spill = 0, t_rows_tile = 128;
@@ -437,6 +440,16 @@ static fastilu_status setup_tsell(fastilu_handle h, const std::vector<unsigned l
           !jit_occupancy(h->jit_st, c.threads, c.smem, &sbps) && sbps > 0) {
         h->st = c;
         h->st_ntiles = std::max<int64_t>(1, (h->n + c.shift + c.rows - 1) / c.rows);
+        // the first sweep with the init fused in (single GPU: ghost rows would need ahat)
+        StagedCfg ci{};
+        const std::string s2 = sweep_source_staged(T, sthreads, sparts, nst, sminb, true, &ci,
+                                                   sopts | kStagedFromAhat);
+        if (h->opt.nranks <= 1 && !std::getenv("FASTILU_NO_FUSED_INIT") &&
+            !jit_get(s2, "fastilu_tsell_sweep_st_init", h->device, &h->jit_st_init, &log) &&
+            !jit_set_smem(h->jit_st_init, ci.smem) && ci.rows == c.rows && ci.shift == c.shift)
+          h->st_init = ci;
+        else
+          h->jit_st_init = nullptr;
         h->st_grid = (int)std::min<int64_t>((int64_t)sm_count(h->device) * sbps, h->st_ntiles);
       } else {
         if (std::getenv("FASTILU_DEBUG"))
@@ -444,6 +457,22 @@ static fastilu_status setup_tsell(fastilu_handle h, const std::vector<unsigned l
         h->jit_st = h->jit_st_first = nullptr;
       }
     }
+  }
+  // wavefront trisolve kernels (factor rows in registers across sweeps): single GPU, up to 40
+  // entries per triangular row (27-pt ILU(1) has 31).  Opt-in (FASTILU_JIT_TRISOLVE=1): it
+  // reads the factor once per apply but each tile's sweeps are latency-bound and wait on their
+  // neighbours -- measured 18.3 ms vs 6.7 ms for the streaming per-sweep kernels (c4, 5+5).
+  if (h->opt.nranks <= 1 && T.c0 <= 40 && T.W - T.c0 - 1 <= 40 &&
+      std::getenv("FASTILU_JIT_TRISOLVE") && atoi(std::getenv("FASTILU_JIT_TRISOLVE")) != 0) {
+    int tb = 0, ub = 0;
+    const std::string sl = trisolve_source(T, true, 256), su = trisolve_source(T, false, 256);
+    if (!jit_get(sl, "fastilu_tsell_tri_L", h->device, &h->jit_tri[0], &log) &&
+        !jit_get(su, "fastilu_tsell_tri_U", h->device, &h->jit_tri[1], &log) &&
+        !jit_occupancy(h->jit_tri[0], 256, 0, &tb) && !jit_occupancy(h->jit_tri[1], 256, 0, &ub) &&
+        tb > 0 && ub > 0)
+      h->tri_jgrid = sm_count(h->device) * std::min(tb, ub);
+    else
+      h->jit_tri[0] = h->jit_tri[1] = nullptr;
   }
   int bps = 0;
   jit_func_info(h->jit_sweep, &h->t_regs, &h->t_spill, threads, &bps);
@@ -488,8 +517,11 @@ static fastilu_status setup_tsell(fastilu_handle h, const std::vector<unsigned l
       if (jit_tmap_sell(h->st_tmap[b].b, h->d_vals[b], T.W, h->nsl, h->st.box_cols,
                         h->st.box_slices)) {
         if (std::getenv("FASTILU_DEBUG")) fprintf(stderr, "fastilu: tensor map failed\n");
-        h->jit_st = h->jit_st_first = nullptr;
+        h->jit_st = h->jit_st_first = h->jit_st_init = nullptr;
       }
+  if (h->jit_st_init && jit_tmap_sell(h->st_tmap_ahat.b, h->d_ahat, T.WA, h->nsl,
+                                      h->st_init.box_cols, h->st_init.box_slices))
+    h->jit_st_init = nullptr;
   CU(cudaMemset(h->d_counter, 0, sizeof(unsigned int)));
   CU(cudaMemcpy(h->d_tmask, mask.data(), 8 * mask.size(), cudaMemcpyHostToDevice));
   CU(cudaMemcpy(h->d_tasrc, asrc.data(), 4 * asrc.size(), cudaMemcpyHostToDevice));
@@ -989,10 +1021,14 @@ static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, i
     fastilu_status cs = comm_vector_halo(h->comm, h->d_s, st, false, true);
     if (cs) return cs;
   }
-  // a3: ahat and the initial guess (iterate 0) for the owned rows
+  // a3: ahat and the initial guess (iterate 0) for the owned rows.  With the fused first
+  // sweep, iterate 0 is computed from ahat inside sweep 1 and never stored.
+  const bool fuse_init = h->tsell && h->jit_st_init && h->jit_st && !h->comm && !warmup &&
+                         !async && nsweeps >= 1 && h->opt.omega == 1.0 &&
+                         !fused_enabled("FASTILU_NO_FUSED_SWEEPS");
   if (h->tsell)
     CU(launch_tsell_init(tdev(h), h->d_aT, h->d_s, h->d_ad, r0, r1, h->d_ahat, h->d_vals[0],
-                         h->d_ud[0], h->d_err, h->opt.shift, st));
+                         h->d_ud[0], h->d_err, h->opt.shift, st, !fuse_init));
   else
     CU(launch_init(P, h->d_arp, h->d_aci, h->d_apos, h->d_aval, h->d_s, h->d_ad, r0, r1,
                    h->d_ahat, h->d_vals[0], h->d_ud[0], h->d_err, h->G_init, h->opt.shift, st));
@@ -1070,7 +1106,13 @@ static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, i
         void *sargs[] = {&old, &outp, &ahat, &mk, &udn, &a0, &a1, &om, &part, &zp, &ctr,
                          h->st_tmap[ib].b};
         void *fn = (sw == 1 && !warmup && h->jit_st_first) ? h->jit_st_first : h->jit_st;
-        if (jit_launch_smem(fn, h->st_grid, h->st.threads, h->st.smem, st, sargs))
+        int smem = h->st.smem;
+        if (sw == 1 && fuse_init) {
+          fn = h->jit_st_init;
+          smem = h->st_init.smem;
+          sargs[11] = h->st_tmap_ahat.b;
+        }
+        if (jit_launch_smem(fn, h->st_grid, h->st.threads, smem, st, sargs))
           return FASTILU_ERR_CUDA;
         CU(launch_reduce_reset(h->d_partials, (int)h->st_ntiles, h->d_r2 + (sw - 1),
                                h->d_counter, st));
@@ -1196,8 +1238,50 @@ static fastilu_status apply_fused(fastilu_handle h, const double *b, double *x, 
   return FASTILU_OK;
 }
 
+// a8 + a9 as two wavefront kernels (tsell.h trisolve_source): all ntri sweeps of a triangle in
+// one launch, the factor read once.
+static fastilu_status apply_jit(fastilu_handle h, const double *b, double *x, int ntri) {
+  cudaStream_t st = h->stream;
+  const int64_t R = 256, ntiles = (h->n + R - 1) / R;
+  const size_t ws = 128 + (size_t)ntri * ntiles;
+  if (ntri > h->tri_cap || !h->d_tribuf) {
+    if (h->d_tribuf) cudaFree(h->d_tribuf);
+    if (h->d_triws) cudaFree(h->d_triws);
+    h->d_tribuf = nullptr;
+    h->d_triws = nullptr;
+    CU(dalloc(&h->d_tribuf, (int64_t)2 * ntri * h->E));
+    CU(cudaMemset(h->d_tribuf, 0, sizeof(double) * 2 * ntri * h->E));
+    CU(cudaMalloc((void **)&h->d_triws, std::max(ws, tsell_trisolve_ws_bytes(ntri, h->n))));
+    h->tri_cap = ntri;
+  }
+  long long r0 = h->G, r1 = h->G + h->n, E = h->E, Gh = h->G, nt = ntiles;
+  double om = h->opt.omega_tri;
+  const double *vals = h->vals_cur, *ud = h->ud_cur, *sv = h->d_s;
+  const unsigned long long *mk = h->d_tmask;
+  const int grid = (int)std::min<int64_t>(h->tri_jgrid, ntiles);
+  int nts = ntri;
+  for (int tri = 0; tri < 2; tri++) {
+    const bool lower = tri == 0;
+    double *bufp = h->d_tribuf + (lower ? 0 : (int64_t)ntri * h->E);
+    const double *rhs = lower ? b : h->d_tribuf + (int64_t)(ntri - 1) * h->E;
+    double *xo = x;
+    unsigned int *ctr = h->d_triws;
+    unsigned char *flags = reinterpret_cast<unsigned char *>(h->d_triws) + 128;
+    const int64_t bw = lower ? -(int64_t)h->T.off[0] : (int64_t)h->T.off[h->T.W - 1];
+    int dep = (int)std::min<int64_t>(ntiles, (bw + R - 1) / R + 1);
+    int fx = lower ? 0 : 1;
+    CU(cudaMemsetAsync(h->d_triws, 0, ws, st));
+    void *args[] = {&vals, &ud, &mk, &rhs, &sv, &bufp, &xo, &r0, &r1, &E, &Gh, &nts, &om,
+                    &ctr, &flags, &nt, &dep, &fx};
+    if (jit_launch(h->jit_tri[tri], grid, 256, st, args)) return FASTILU_ERR_CUDA;
+  }
+  return FASTILU_OK;
+}
+
 static fastilu_status apply_impl(fastilu_handle h, const double *b, double *x, int ntri) {
   cudaStream_t st = h->stream;
+  if (h->tsell && !h->comm && h->jit_tri[0] && h->jit_tri[1] && ntri >= 1)
+    return apply_jit(h, b, x, ntri);
   if (h->tsell && !h->comm && fused_enabled("FASTILU_NO_FUSED_TRISOLVE"))
     return apply_fused(h, b, x, ntri);
   DevPattern P{h->d_rp, h->d_ci, h->d_dloc};

@@ -682,12 +682,13 @@ __global__ void __launch_bounds__(256)
 tsell_init_kernel(TDev t, const double *__restrict__ aT, const double *__restrict__ s,
                   const double *__restrict__ ad, int64_t r0, int64_t r1,
                   double *__restrict__ ahatT, double *__restrict__ vals,
-                  double *__restrict__ udiag, ErrFlags *err, double shift) {
+                  double *__restrict__ udiag, ErrFlags *err, double shift, bool iter0) {
   __shared__ int32_t soff[128], soffA[128];
-  __shared__ int8_t sw2a[128];
+  __shared__ int8_t sw2a[128], sa2w[128];
   for (int q = threadIdx.x; q < t.W; q += blockDim.x) {
     soff[q] = t.off[q];
     sw2a[q] = t.w2a[q];
+    if (t.w2a[q] >= 0) sa2w[t.w2a[q]] = (int8_t)q;
   }
   for (int q = threadIdx.x; q < t.WA; q += blockDim.x) soffA[q] = t.offA[q];
   __syncthreads();
@@ -699,6 +700,17 @@ tsell_init_kernel(TDev t, const double *__restrict__ aT, const double *__restric
   const double si = s[i];
   const double *arow = aT + sl * t.WA * 32 + ln;
   double *hrow = ahatT + sl * t.WA * 32 + ln;
+  if (!iter0) {  // ahat only (the fused first sweep derives iterate 0 from it): A's columns
+    for (int a = 0; a < t.WA; a++) {
+      const int w = sa2w[a];
+      double av = arow[a * 32];
+      if (w == t.c0) av = __dadd_rn(av, __dmul_rn(shift, fabs(av)));
+      const double ah = tbit(m, w) ? __dmul_rn(__dmul_rn(av, si), s[i + soffA[a]]) : 0.0;
+      hrow[a * 32] = ah;
+      if (w == t.c0 && bad_pivot(ah)) atomicMin(&err->zero_pivot, (unsigned long long)i);
+    }
+    return;
+  }
   for (int w = 0; w < t.W; w++) {
     const int a = sw2a[w];
     double v = 0.0;  // fill entries and slots outside S: +0.0
@@ -710,9 +722,9 @@ tsell_init_kernel(TDev t, const double *__restrict__ aT, const double *__restric
       hrow[a * 32] = ah;
       if (tbit(m, w)) v = (w < t.c0) ? __ddiv_rn(ah, ad[i + soff[w]]) : ah;
     }
-    vals[(sl * t.W + w) * 32 + ln] = v;
+    if (iter0) vals[(sl * t.W + w) * 32 + ln] = v;
     if (w == t.c0) {
-      udiag[i] = v;
+      if (iter0) udiag[i] = v;
       if (bad_pivot(v)) atomicMin(&err->zero_pivot, (unsigned long long)i);
     }
   }
@@ -721,10 +733,10 @@ tsell_init_kernel(TDev t, const double *__restrict__ aT, const double *__restric
 cudaError_t launch_tsell_init(const TDev &t, const double *aT, const double *s,
                               const double *ad, int64_t r0, int64_t r1, double *ahatT,
                               double *vals, double *udiag, ErrFlags *err, double shift,
-                              cudaStream_t st) {
+                              cudaStream_t st, bool iter0) {
   if (r1 <= r0) return cudaSuccess;
   tsell_init_kernel<<<(unsigned)((r1 - r0 + 255) / 256), 256, 0, st>>>(
-      t, aT, s, ad, r0, r1, ahatT, vals, udiag, err, shift);
+      t, aT, s, ad, r0, r1, ahatT, vals, udiag, err, shift, iter0);
   return cudaGetLastError();
 }
 

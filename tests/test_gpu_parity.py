@@ -321,3 +321,37 @@ def test_first_sweep_kernel_equals_full_sweep(kind, g, k, omega, monkeypatch):
     assert f.info().startswith("path=tsell") and h.info().startswith("path=tsell")
     assert np.array_equal(f.factors()[0], h.factors()[0])
     np.testing.assert_array_equal(f.residual_history(), h.residual_history())
+
+
+# every template-path kernel variant computes exactly the oracle's factors and x
+_VARIANTS = [
+    ("register-pivot sweep", {"FASTILU_TSELL_STAGED": "0"}, None),
+    ("staged sweep forced on", {"FASTILU_TSELL_STAGED": "1"}, "staged=1"),
+    ("iterate 0 stored by the init", {"FASTILU_NO_FUSED_INIT": "1"}, None),
+    ("shifted tiles (smaller TMA box)", {"FASTILU_TSELL_STAGED": "1", "FASTILU_TSELL_ST_OPTS": "64"},
+     "staged=1"),
+    ("3-stage ring", {"FASTILU_TSELL_STAGED": "1", "FASTILU_TSELL_STAGES": "3"}, "st_stages=3"),
+    ("128-row tiles", {"FASTILU_TSELL_STAGED": "1", "FASTILU_TSELL_ST_THREADS": "256"}, None),
+    ("wavefront trisolve", {"FASTILU_JIT_TRISOLVE": "1"}, None),
+]
+
+
+@pytest.mark.parametrize("name,env,marker", _VARIANTS, ids=[v[0] for v in _VARIANTS])
+@pytest.mark.parametrize("kind,g,gz,k,ns,nt", [("27pt", 12, 11, 1, 3, 5), ("27pt", 9, 10, 2, 2, 3),
+                                               ("7pt", 20, 17, 0, 3, 4), ("27pt", 11, 9, 0, 1, 1)])
+def test_template_kernel_variants(name, env, marker, kind, g, gz, k, ns, nt, monkeypatch):
+    """Ragged grids (n not a multiple of the tile): factors, residual history and x of each
+    kernel variant are bitwise the oracle's."""
+    for key, val in env.items():
+        monkeypatch.setenv(key, val)
+    a = P.make(kind, g, gz)
+    b = P.rhs_positive(a.n)
+    f, vals, _, x = gpu_run(a, k, ns, nt, b)
+    assert f.info().startswith("path=tsell")
+    if marker and not (k == 2 and "FASTILU_TSELL_STAGES" in env):  # 3 x 87 KB > 227 KB:
+        assert marker in f.info(), f.info()  # ILU(2) then keeps the register-pivot kernel
+    fo = oracle.compute(a, k, ns)
+    assert np.array_equal(vals, fo.vals)
+    np.testing.assert_allclose(f.residual_history(), fo.resid,
+                               rtol=max(1e-12, (fo.pattern.nnz + 64) * np.finfo(float).eps))
+    assert np.array_equal(x, oracle.apply(fo, b, nt))
