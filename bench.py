@@ -265,7 +265,7 @@ def run_ours(args, wl):
     if world > 1:
         dist.barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    t_sweeps, t_apply, t_init = [], [], []
+    t_sweeps, t_apply, t_init, t_first, t_rest = [], [], [], [], []
     torch.cuda.synchronize()
     clocks.mark_start()
     ev0.record(stream)
@@ -273,6 +273,8 @@ def run_ours(args, wl):
         step()
         tm = f.timings()  # library CUDA events on this stream (compute synchronised)
         t_sweeps.append(tm["sweeps_ms"])
+        t_first.append(tm["sweep1_ms"])
+        t_rest.append(tm["sweeps_rest_ms"])
         t_init.append(tm["init_ms"])
     ev1.record(stream)
     torch.cuda.synchronize()
@@ -289,7 +291,10 @@ def run_ours(args, wl):
     sweep_ms = float(np.mean(t_sweeps))
     value = nnz_S_total * ns / (ms * 1e-3)
     peak, peak_src = peaks()
-    per_launch_ms = sweep_ms / max(ns, 1)
+    # the dominant kernel is the full sweep (sweeps 2..ns); sweep 1 is a different kernel (the
+    # initial guess fused in, A x A terms only), reported separately
+    rest_ms = float(np.mean(t_rest)) if ns >= 2 else 0.0
+    per_launch_ms = rest_ms / (ns - 1) if ns >= 2 and rest_ms > 0 else sweep_ms / max(ns, 1)
     achieved = bm["B_f"] / (per_launch_ms * 1e-3) / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -351,7 +356,8 @@ def run_ours(args, wl):
                        "global_grid": [g, g, g * world],
                        "l2": "working set >> 126 MB L2 (no flush needed)"},
             "sweep_nnz_updates_per_s": nnz_S * ns / (sweep_ms * 1e-3),
-            "sweep_ms": sweep_ms, "init_ms": float(np.mean(t_init)), "apply_ms": t_apply,
+            "sweep_ms": sweep_ms, "sweep1_ms": float(np.mean(t_first)),
+            "sweep_launch_ms": per_launch_ms, "init_ms": float(np.mean(t_init)), "apply_ms": t_apply,
             "trisolve_gbs": bm["B_apply"] / (t_apply * 1e-3) / 1e9 if t_apply > 0 else None,
             "composite_gbs": (bm["B_init"] + ns * bm["B_f"] + bm["B_apply"]) / (ms * 1e-3) / 1e9,
             "roofline": roof,

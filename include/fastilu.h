@@ -179,6 +179,10 @@ fastilu_status fastilu_get_residual_history(fastilu_handle h, double *hist, int 
 /* Device-time breakdown of the last compute/apply in milliseconds (CUDA events):
  * t[0] = scale+init, t[1] = all sweeps, t[2] = apply (last call).  */
 fastilu_status fastilu_get_timings(fastilu_handle h, double *t3);
+/* Split of t[1] of fastilu_get_timings (milliseconds, CUDA events on the handle's stream):
+ * t2[0] = sweep 1 (for the template path: the kernel with the initial guess fused in, plus its
+ * residual reduction), t2[1] = sweeps 2..nsweeps (0 if nsweeps < 2).  Host-only; no sync. */
+fastilu_status fastilu_get_sweep_split(fastilu_handle h, double *t2);
 /* One-line description of the handle's kernel configuration (path "tsell" = template-SELL
  * with the JIT-specialised sweep, "csr-classes" / "csr-hash" / "csr-bsearch" = CSR kernels),
  * written NUL-terminated into buf (at most cap bytes). */

@@ -69,6 +69,7 @@ _SIGS = {
     "fastilu_get_factors": (C.c_int, [H, F64P, F64P]),
     "fastilu_get_residual_history": (C.c_int, [H, F64P, C.c_int, C.POINTER(C.c_int)]),
     "fastilu_get_timings": (C.c_int, [H, F64P]),
+    "fastilu_get_sweep_split": (C.c_int, [H, F64P]),
     "fastilu_get_info": (C.c_int, [H, C.c_char_p, C.c_int]),
     "fastilu_status_string": (C.c_char_p, [C.c_int]),
     "fastilu_error_index": (C.c_int64, [H]),
@@ -320,7 +321,11 @@ class FastILU:
     def timings(self):
         t = np.zeros(3)
         _check(lib().fastilu_get_timings(self._h, _p(t, F64P)), "fastilu_get_timings", self._h)
-        return {"init_ms": t[0], "sweeps_ms": t[1], "apply_ms": t[2]}
+        u = np.zeros(2)
+        _check(lib().fastilu_get_sweep_split(self._h, _p(u, F64P)), "fastilu_get_sweep_split",
+               self._h)
+        return {"init_ms": t[0], "sweeps_ms": t[1], "apply_ms": t[2], "sweep1_ms": u[0],
+                "sweeps_rest_ms": u[1]}
 
     def info(self) -> str:
         """Kernel configuration of this handle (fastilu_get_info)."""

@@ -130,7 +130,9 @@ struct fastilu_handle_s {
   bool have_values = false, computed = false;
   int cur = 0;
   std::vector<double> resid;
-  cudaEvent_t ev[5] = {};
+  cudaEvent_t ev[6] = {};  // ev[5]: after sweep 1
+  float t_sweep1 = 0.f;
+  int last_ns = 0;
   float t_init = 0.f, t_sweeps = 0.f, t_apply = 0.f;
   bool apply_timed = false;  // ev[3] / ev[4] recorded by an apply
   Comm *comm = nullptr;
@@ -836,7 +838,7 @@ static fastilu_status create_impl(fastilu_handle h, int64_t n, const int64_t *ro
     CU(cudaMemset(h->d_z[b], 0, sizeof(double) * h->E));
     CU(cudaMemset(h->d_w[b], 0, sizeof(double) * h->E));
   }
-  for (int i = 0; i < 5; i++) CU(cudaEventCreate(&h->ev[i]));
+  for (int i = 0; i < 6; i++) CU(cudaEventCreate(&h->ev[i]));
   if (multi) {
     int64_t nl_global = 0;
     fastilu_status cs = comm_layout(h->comm, h->row_begin, h->n, h->G, h->H, rp.data(), nl_own,
@@ -1063,6 +1065,7 @@ static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, i
   }
   // a4/a5: nsweeps synchronous sweeps, ping-pong buffers
   for (int sw = 1; sw <= nsweeps && !fused; sw++) {
+    if (sw == 2) CU(cudaEventRecord(h->ev[5], st));  // sweep 1 / the rest split
     executed = sw;
     const int ib_async = 0;  // asynchronous sweeps stay in buffer 0 (in place)
     if (thr2 >= 0.0 && sw > 1) {  // r(sw-2) of the previous sweep decides whether to go on
@@ -1156,6 +1159,9 @@ static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, i
   CU(cudaStreamSynchronize(st));
   CU(cudaEventElapsedTime(&h->t_init, h->ev[0], h->ev[1]));
   CU(cudaEventElapsedTime(&h->t_sweeps, h->ev[1], h->ev[2]));
+  h->t_sweep1 = h->t_sweeps;
+  h->last_ns = fused ? 0 : executed;
+  if (!fused && executed >= 2) CU(cudaEventElapsedTime(&h->t_sweep1, h->ev[1], h->ev[5]));
   h->resid.assign(nsweeps, 0.0);
   std::vector<double> r2(h->h_r2, h->h_r2 + nsweeps);
   ErrFlags ef = *h->h_err;  // local rows -> global rows
@@ -1572,6 +1578,13 @@ extern "C" fastilu_status fastilu_get_timings(fastilu_handle h, double *t3) {
   return FASTILU_OK;
 }
 
+extern "C" fastilu_status fastilu_get_sweep_split(fastilu_handle h, double *t2) {
+  if (!h || !t2) FAIL(FASTILU_ERR_INVALID_ARG);
+  t2[0] = h->t_sweep1;
+  t2[1] = h->last_ns >= 2 ? (double)h->t_sweeps - (double)h->t_sweep1 : 0.0;
+  return FASTILU_OK;
+}
+
 extern "C" fastilu_status fastilu_get_info(fastilu_handle h, char *buf, int cap) {
   if (!h || !buf || cap < 1) FAIL(FASTILU_ERR_INVALID_ARG);
   char tmp[512];
@@ -1630,7 +1643,7 @@ extern "C" fastilu_status fastilu_destroy(fastilu_handle h) {
   for (auto *p : h->d_lmask) cudaFree(p);
   for (auto *p : h->fpool_v) cudaFree(p);
   for (auto *p : h->fpool_u) cudaFree(p);
-  for (int i = 0; i < 5; i++)
+  for (int i = 0; i < 6; i++)
     if (h->ev[i]) cudaEventDestroy(h->ev[i]);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
   delete h;

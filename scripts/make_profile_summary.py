@@ -112,7 +112,9 @@ def main():
                 for k, v in met.get(i, {}).items():
                     f.write(f"- {k}: {v}\n")
                 f.write("\n")
-        sweeps = [d for name, d in kern.values() if "sweep" in name]
+        # the dominant (full) sweep kernel, not sweep 1's variants (_init / _first)
+        sweeps = [d for name, d in kern.values()
+                  if "sweep" in name and not name.endswith(("_init", "_first"))]
         if sweeps:
             tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
             cur = json.load(open(tp)) if os.path.exists(tp) else {}
