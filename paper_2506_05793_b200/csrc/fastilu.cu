@@ -106,6 +106,8 @@ struct fastilu_handle_s {
   void *jit_st_init = nullptr;  // sweep 1 with iterate 0 computed from ahat (single GPU)
   void *jit_tri[2] = {nullptr, nullptr};  // wavefront trisolve L / U (single GPU)
   int tri_jgrid = 0;
+  void *jit_lag[2] = {nullptr, nullptr};  // lagged multi-sweep trisolve L / U (single GPU)
+  int lag_grid = 0;
   StagedCfg st{}, st_init{};
   int st_grid = 0;
   int64_t st_ntiles = 0;
@@ -426,7 +428,7 @@ static fastilu_status setup_tsell(fastilu_handle h, const std::vector<unsigned l
           ev_sth ? std::max(32 * sparts, atoi(ev_sth) / (32 * sparts) * 32 * sparts)
                  : (sparts <= 2 ? 256 * sparts : 128 * sparts);
       const char *ev_so = std::getenv("FASTILU_TSELL_ST_OPTS");
-      const unsigned sopts = (ev_so ? (unsigned)atoi(ev_so) : 0u) |
+      const unsigned sopts = (ev_so ? (unsigned)atoi(ev_so) : kStagedFastDiv) |
                              (h->opt.omega != 1.0 ? kStagedDamp : 0u);
       const char *ev_smb = std::getenv("FASTILU_TSELL_ST_MINB");
       const int sminb = ev_smb ? atoi(ev_smb) : 0;
@@ -475,6 +477,23 @@ static fastilu_status setup_tsell(fastilu_handle h, const std::vector<unsigned l
       h->tri_jgrid = sm_count(h->device) * std::min(tb, ub);
     else
       h->jit_tri[0] = h->jit_tri[1] = nullptr;
+  }
+  // lagged multi-sweep trisolve: opt-in (FASTILU_TRILAG=1), measured slower than the streaming
+  // per-sweep kernels (c4 5+5: 9.2-16 ms vs 6.7 ms)
+  if (h->opt.nranks <= 1 && std::getenv("FASTILU_TRILAG") && atoi(std::getenv("FASTILU_TRILAG"))) {
+    int lb = 0, ub = 0;
+    const std::string sl = trisolve_lag_source(T, true, 256), su = trisolve_lag_source(T, false, 256);
+    if (!jit_get(sl, "fastilu_tsell_trilag_L", h->device, &h->jit_lag[0], &log) &&
+        !jit_get(su, "fastilu_tsell_trilag_U", h->device, &h->jit_lag[1], &log) &&
+        !jit_occupancy(h->jit_lag[0], 256, 0, &lb) && !jit_occupancy(h->jit_lag[1], 256, 0, &ub) &&
+        lb > 0 && ub > 0)
+    {  // resident blocks bound the lag and so the L2 footprint of the re-read factor rows
+      const char *eb = std::getenv("FASTILU_TRILAG_BPS");
+      const int cap = eb ? std::max(1, atoi(eb)) : 3;
+      h->lag_grid = sm_count(h->device) * std::min(cap, std::min(lb, ub));
+    }
+    else
+      h->jit_lag[0] = h->jit_lag[1] = nullptr;
   }
   int bps = 0;
   jit_func_info(h->jit_sweep, &h->t_regs, &h->t_spill, threads, &bps);
@@ -1284,8 +1303,58 @@ static fastilu_status apply_jit(fastilu_handle h, const double *b, double *x, in
   return FASTILU_OK;
 }
 
+// a8 + a9 with the lagged multi-sweep kernels (tsell.h trisolve_lag_source): launches of up to
+// S sweeps (FASTILU_TRILAG_S, default 3) in which a tile's factor rows are re-read from L2.
+static fastilu_status apply_lag(fastilu_handle h, const double *b, double *x, int ntri) {
+  cudaStream_t st = h->stream;
+  const int64_t R = 256, ntiles = (h->n + R - 1) / R;
+  const size_t ws = 128 + (size_t)ntri * ntiles;
+  if (ntri > h->tri_cap || !h->d_tribuf) {
+    if (h->d_tribuf) cudaFree(h->d_tribuf);
+    if (h->d_triws) cudaFree(h->d_triws);
+    h->d_tribuf = nullptr;
+    h->d_triws = nullptr;
+    CU(dalloc(&h->d_tribuf, (int64_t)2 * ntri * h->E));
+    CU(cudaMemset(h->d_tribuf, 0, sizeof(double) * 2 * ntri * h->E));
+    CU(cudaMalloc((void **)&h->d_triws, std::max(ws, tsell_trisolve_ws_bytes(ntri, h->n))));
+    h->tri_cap = ntri;
+  }
+  const char *ev = std::getenv("FASTILU_TRILAG_S");
+  const int smax = ev ? std::max(1, atoi(ev)) : 3;
+  long long r0 = h->G, r1 = h->G + h->n, E = h->E, Gh = h->G, nt = ntiles;
+  double om = h->opt.omega_tri;
+  const double *vals = h->vals_cur, *ud = h->ud_cur, *sv = h->d_s;
+  const unsigned long long *mk = h->d_tmask;
+  const int grid = (int)std::min<int64_t>(h->lag_grid, ntiles + 2 * (int64_t)h->lag_grid);
+  int lag = h->lag_grid + 32, nts = ntri;
+  unsigned int *ctr = h->d_triws;
+  unsigned char *flags = reinterpret_cast<unsigned char *>(h->d_triws) + 128;
+  for (int tri = 0; tri < 2; tri++) {
+    const bool lower = tri == 0;
+    double *bufp = h->d_tribuf + (lower ? 0 : (int64_t)ntri * h->E);
+    const double *rhs = lower ? b : h->d_tribuf + (int64_t)(ntri - 1) * h->E;
+    double *xo = x;
+    const int64_t bw = lower ? -(int64_t)h->T.off[0] : (int64_t)h->T.off[h->T.W - 1];
+    int dep = (int)std::min<int64_t>(ntiles, (bw + R - 1) / R + 1);
+    int fx = lower ? 0 : 1;
+    CU(cudaMemsetAsync(h->d_triws, 0, ws, st));
+    for (int t0 = 1; t0 <= ntri;) {
+      int S = std::min(smax, ntri - t0 + 1);
+      if (t0 > 1) CU(cudaMemsetAsync(ctr, 0, sizeof(unsigned int), st));
+      void *args[] = {&vals, &ud, &mk, &rhs, &sv, &bufp, &xo, &r0, &r1, &E, &Gh, &nts, &t0,
+                      &S, &lag, &om, &ctr, &flags, &nt, &dep, &fx};
+      if (jit_launch(h->jit_lag[tri], grid, 256, st, args)) return FASTILU_ERR_CUDA;
+      t0 += S;
+    }
+  }
+  return FASTILU_OK;
+}
+
 static fastilu_status apply_impl(fastilu_handle h, const double *b, double *x, int ntri) {
   cudaStream_t st = h->stream;
+  if (h->tsell && !h->comm && h->jit_lag[0] && h->jit_lag[1] && ntri >= 1 &&
+      !(h->jit_tri[0] && h->jit_tri[1]))
+    return apply_lag(h, b, x, ntri);
   if (h->tsell && !h->comm && h->jit_tri[0] && h->jit_tri[1] && ntri >= 1)
     return apply_jit(h, b, x, ntri);
   if (h->tsell && !h->comm && fused_enabled("FASTILU_NO_FUSED_TRISOLVE"))

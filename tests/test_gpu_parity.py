@@ -333,6 +333,10 @@ _VARIANTS = [
     ("3-stage ring", {"FASTILU_TSELL_STAGED": "1", "FASTILU_TSELL_STAGES": "3"}, "st_stages=3"),
     ("128-row tiles", {"FASTILU_TSELL_STAGED": "1", "FASTILU_TSELL_ST_THREADS": "256"}, None),
     ("wavefront trisolve", {"FASTILU_JIT_TRISOLVE": "1"}, None),
+    ("lagged 3-sweep trisolve", {"FASTILU_TRILAG": "1", "FASTILU_TRILAG_S": "3"}, None),
+    ("lagged 5-sweep trisolve", {"FASTILU_TRILAG": "1", "FASTILU_TRILAG_S": "5"}, None),
+    ("divisions through __ddiv_rn", {"FASTILU_TSELL_STAGED": "1", "FASTILU_TSELL_ST_OPTS": "0"},
+     "staged=1"),
 ]
 
 
