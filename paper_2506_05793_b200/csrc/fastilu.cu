@@ -114,6 +114,7 @@ struct fastilu_handle_s {
   struct alignas(64) TMapBuf {
     unsigned char b[128];
   } st_tmap[2], st_tmap_ahat;  // per iterate buffer d_vals[0/1]; over d_ahat
+  TMapBuf st_tmap_own[2], st_tmap_own_ahat;  // own-row boxes (kStagedOwnL)
   int t_parts = 1, t_minb = 0, t_sstride = 1;
   bool t_prefetch = true;
   int t_threads = 128, t_grid = 1, t_regs = 0, t_spill = 0, t_rows_tile = 128;
@@ -428,7 +429,7 @@ static fastilu_status setup_tsell(fastilu_handle h, const std::vector<unsigned l
           ev_sth ? std::max(32 * sparts, atoi(ev_sth) / (32 * sparts) * 32 * sparts)
                  : (sparts <= 2 ? 256 * sparts : 128 * sparts);
       const char *ev_so = std::getenv("FASTILU_TSELL_ST_OPTS");
-      const unsigned sopts = (ev_so ? (unsigned)atoi(ev_so) : kStagedFastDiv) |
+      const unsigned sopts = (ev_so ? (unsigned)atoi(ev_so) : (kStagedFastDiv | kStagedOwnL | kStagedLastIssues)) |
                              (h->opt.omega != 1.0 ? kStagedDamp : 0u);
       const char *ev_smb = std::getenv("FASTILU_TSELL_ST_MINB");
       const int sminb = ev_smb ? atoi(ev_smb) : 0;
@@ -542,6 +543,15 @@ static fastilu_status setup_tsell(fastilu_handle h, const std::vector<unsigned l
       }
   if (h->jit_st_init && jit_tmap_sell(h->st_tmap_ahat.b, h->d_ahat, T.WA, h->nsl,
                                       h->st_init.box_cols, h->st_init.box_slices))
+    h->jit_st_init = nullptr;
+  // own-row boxes: {32, own_cols, rows/32} (any valid map when the kernel does not use them)
+  if (h->jit_st)
+    for (int b = 0; b < 2; b++)
+      if (jit_tmap_sell(h->st_tmap_own[b].b, h->d_vals[b], T.W, h->nsl,
+                        std::max(1, h->st.own_cols), h->st.rows / 32))
+        h->jit_st = h->jit_st_first = h->jit_st_init = nullptr;
+  if (h->jit_st_init && jit_tmap_sell(h->st_tmap_own_ahat.b, h->d_ahat, T.WA, h->nsl,
+                                      std::max(1, h->st_init.own_cols), h->st_init.rows / 32))
     h->jit_st_init = nullptr;
   CU(cudaMemset(h->d_counter, 0, sizeof(unsigned int)));
   CU(cudaMemcpy(h->d_tmask, mask.data(), 8 * mask.size(), cudaMemcpyHostToDevice));
@@ -1126,13 +1136,14 @@ static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, i
       int sstr = h->t_sstride;
       if (h->jit_st && !async) {
         void *sargs[] = {&old, &outp, &ahat, &mk, &udn, &a0, &a1, &om, &part, &zp, &ctr,
-                         h->st_tmap[ib].b};
+                         h->st_tmap[ib].b, h->st_tmap_own[ib].b};
         void *fn = (sw == 1 && !warmup && h->jit_st_first) ? h->jit_st_first : h->jit_st;
         int smem = h->st.smem;
         if (sw == 1 && fuse_init) {
           fn = h->jit_st_init;
           smem = h->st_init.smem;
           sargs[11] = h->st_tmap_ahat.b;
+          sargs[12] = h->st_tmap_own_ahat.b;
         }
         if (jit_launch_smem(fn, h->st_grid, h->st.threads, smem, st, sargs))
           return FASTILU_ERR_CUDA;

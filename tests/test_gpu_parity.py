@@ -330,7 +330,12 @@ _VARIANTS = [
     ("iterate 0 stored by the init", {"FASTILU_NO_FUSED_INIT": "1"}, None),
     ("shifted tiles (smaller TMA box)", {"FASTILU_TSELL_STAGED": "1", "FASTILU_TSELL_ST_OPTS": "64"},
      "staged=1"),
-    ("3-stage ring", {"FASTILU_TSELL_STAGED": "1", "FASTILU_TSELL_STAGES": "3"}, "st_stages=3"),
+    ("3-stage ring", {"FASTILU_TSELL_STAGED": "1", "FASTILU_TSELL_STAGES": "3",
+                      "FASTILU_TSELL_ST_OPTS": "256"}, "st_stages=3"),
+    ("3-stage ring, 192-row tiles, last-arriver producer",
+     {"FASTILU_TSELL_STAGED": "1", "FASTILU_TSELL_STAGES": "3", "FASTILU_TSELL_ST_THREADS": "384",
+      "FASTILU_TSELL_ST_OPTS": "1792"}, None),
+    ("thread-0 producer", {"FASTILU_TSELL_STAGED": "1", "FASTILU_TSELL_ST_OPTS": "768"}, "staged=1"),
     ("128-row tiles", {"FASTILU_TSELL_STAGED": "1", "FASTILU_TSELL_ST_THREADS": "256"}, None),
     ("wavefront trisolve", {"FASTILU_JIT_TRISOLVE": "1"}, None),
     ("lagged 3-sweep trisolve", {"FASTILU_TRILAG": "1", "FASTILU_TRILAG_S": "3"}, None),
