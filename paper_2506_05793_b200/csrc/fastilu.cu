@@ -108,6 +108,7 @@ struct fastilu_handle_s {
   int tri_jgrid = 0;
   void *jit_lag[2] = {nullptr, nullptr};  // lagged multi-sweep trisolve L / U (single GPU)
   int lag_grid = 0;
+  void *jit_scale = nullptr, *jit_ahat = nullptr;  // template-specialised a2 / a3 (tsell)
   StagedCfg st{}, st_init{};
   int st_grid = 0;
   int64_t st_ntiles = 0;
@@ -478,6 +479,13 @@ static fastilu_status setup_tsell(fastilu_handle h, const std::vector<unsigned l
       h->tri_jgrid = sm_count(h->device) * std::min(tb, ub);
     else
       h->jit_tri[0] = h->jit_tri[1] = nullptr;
+  }
+  // template-specialised scale / ahat kernels (FASTILU_NO_JIT_PREP=1 keeps the generic ones)
+  if (!std::getenv("FASTILU_NO_JIT_PREP") && T.c0 >= 0 && T.w2a[T.c0] >= 0) {
+    const std::string sp = prep_source(T);
+    if (jit_get(sp, "fastilu_tsell_scale", h->device, &h->jit_scale, &log) ||
+        jit_get(sp, "fastilu_tsell_ahat", h->device, &h->jit_ahat, &log))
+      h->jit_scale = h->jit_ahat = nullptr;
   }
   // lagged multi-sweep trisolve: opt-in (FASTILU_TRILAG=1), measured slower than the streaming
   // per-sweep kernels (c4 5+5: 9.2-16 ms vs 6.7 ms)
@@ -1046,8 +1054,18 @@ static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, i
   const int64_t r0 = h->G, r1 = h->G + h->n;
   CU(cudaEventRecord(h->ev[0], st));
   // a2: scaling for every local row (lower ghosts included), then the upper ghosts' s / ad
-  CU(launch_scale(h->d_arp, h->d_adiag, h->d_aval, 0, h->nloc, h->d_s, h->d_ad, h->d_err,
-                  h->opt.shift, st));
+  if (h->tsell && h->jit_scale) {  // from the diagonal column of A's template copy
+    const double *aT = h->d_aT;
+    long long nl = h->nloc;
+    double *sp = h->d_s, *adp = h->d_ad, sh = h->opt.shift;
+    ErrFlags *ep = h->d_err;
+    void *args[] = {&aT, &nl, &sp, &adp, &ep, &sh};
+    if (jit_launch(h->jit_scale, (int)((h->nloc + 255) / 256), 256, st, args))
+      FAIL(FASTILU_ERR_CUDA);
+  } else {
+    CU(launch_scale(h->d_arp, h->d_adiag, h->d_aval, 0, h->nloc, h->d_s, h->d_ad, h->d_err,
+                    h->opt.shift, st));
+  }
   if (h->comm) {  // lower ghosts' s / ahat_ii are computed locally from the lead rows of A
     fastilu_status cs = comm_vector_halo(h->comm, h->d_s, st, false, true);
     if (cs) return cs;
@@ -1057,9 +1075,19 @@ static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, i
   const bool fuse_init = h->tsell && h->jit_st_init && h->jit_st && !h->comm && !warmup &&
                          !async && nsweeps >= 1 && h->opt.omega == 1.0 &&
                          !fused_enabled("FASTILU_NO_FUSED_SWEEPS");
-  if (h->tsell)
+  if (h->tsell && fuse_init && h->jit_ahat) {
+    const double *aT = h->d_aT, *sv = h->d_s;
+    const unsigned long long *mk = h->d_tmask;
+    long long a0 = r0, a1 = r1;
+    double *hp = h->d_ahat, sh = h->opt.shift;
+    ErrFlags *ep = h->d_err;
+    void *args[] = {&aT, &sv, &mk, &a0, &a1, &hp, &ep, &sh};
+    if (h->n > 0 && jit_launch(h->jit_ahat, (int)((h->n + 255) / 256), 256, st, args))
+      FAIL(FASTILU_ERR_CUDA);
+  } else if (h->tsell) {
     CU(launch_tsell_init(tdev(h), h->d_aT, h->d_s, h->d_ad, r0, r1, h->d_ahat, h->d_vals[0],
                          h->d_ud[0], h->d_err, h->opt.shift, st, !fuse_init));
+  }
   else
     CU(launch_init(P, h->d_arp, h->d_aci, h->d_apos, h->d_aval, h->d_s, h->d_ad, r0, r1,
                    h->d_ahat, h->d_vals[0], h->d_ud[0], h->d_err, h->G_init, h->opt.shift, st));

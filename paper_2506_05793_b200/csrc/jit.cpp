@@ -110,7 +110,8 @@ int jit_get(const std::string &src, const char *name, int device, void **fn, std
     return 1;
   }
   std::lock_guard<std::mutex> lk(g_mu);
-  auto key = std::make_pair(device, src);
+  auto key = std::make_pair(device, std::string(name) + '\n' + src);  // a source may hold
+                                                                         // several kernels
   auto it = g_cache.find(key);
   if (it != g_cache.end()) {
     *fn = (void *)it->second;
