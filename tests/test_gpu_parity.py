@@ -337,6 +337,8 @@ _VARIANTS = [
       "FASTILU_TSELL_ST_OPTS": "1792"}, None),
     ("thread-0 producer", {"FASTILU_TSELL_STAGED": "1", "FASTILU_TSELL_ST_OPTS": "768"}, "staged=1"),
     ("generic scale / init kernels", {"FASTILU_NO_JIT_PREP": "1"}, None),
+    ("generic Jacobi kernels", {"FASTILU_NO_JIT_JACOBI": "1"}, None),
+    ("loads-first Jacobi kernels", {"FASTILU_JIT_JACOBI_MODE": "1"}, None),
     ("128-row tiles", {"FASTILU_TSELL_STAGED": "1", "FASTILU_TSELL_ST_THREADS": "256"}, None),
     ("wavefront trisolve", {"FASTILU_JIT_TRISOLVE": "1"}, None),
     ("lagged 3-sweep trisolve", {"FASTILU_TRILAG": "1", "FASTILU_TRILAG_S": "3"}, None),
