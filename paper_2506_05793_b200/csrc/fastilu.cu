@@ -449,7 +449,10 @@ static fastilu_status setup_tsell(fastilu_handle h, const std::vector<unsigned l
         h->st_ntiles = std::max<int64_t>(1, (h->n + c.shift + c.rows - 1) / c.rows);
         // the first sweep with the init fused in (single GPU: ghost rows would need ahat)
         StagedCfg ci{};
-        const std::string s2 = sweep_source_staged(T, sthreads, sparts, nst, sminb, true, &ci,
+        // its stage (A's columns only) is small: FASTILU_TSELL_STAGES_INIT more ring slots
+        const char *ev_si = std::getenv("FASTILU_TSELL_STAGES_INIT");
+        const int nsi = ev_si ? std::max(2, atoi(ev_si)) : nst;
+        const std::string s2 = sweep_source_staged(T, sthreads, sparts, nsi, sminb, true, &ci,
                                                    sopts | kStagedFromAhat);
         if (h->opt.nranks <= 1 && !std::getenv("FASTILU_NO_FUSED_INIT") &&
             !jit_get(s2, "fastilu_tsell_sweep_st_init", h->device, &h->jit_st_init, &log) &&
