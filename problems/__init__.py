@@ -184,6 +184,26 @@ def tridiagonal(n: int, seed: int = SEED) -> Csr:
     return Csr(rp, ci, vals)
 
 
+def banded(n: int, offsets, seed: int = SEED) -> Csr:
+    """Diagonally dominant matrix with the given column offsets j - i (0 included; entries
+    outside [0, n) dropped), off-diagonal values -U[0.1, 1.0) (seeded): a template pattern whose
+    pivots need not lie next to the row (edge cases of the template-SELL kernels)."""
+    offs = sorted(set(int(o) for o in offsets) | {0})
+    rng = np.random.default_rng(seed)
+    rp = [0]
+    ci = []
+    for i in range(n):
+        ci.extend(i + o for o in offs if 0 <= i + o < n)
+        rp.append(len(ci))
+    rp = np.array(rp, dtype=np.int64)
+    ci = np.array(ci, dtype=np.int32)
+    vals = -rng.uniform(0.1, 1.0, size=ci.size)
+    for i in range(n):
+        s, e = rp[i], rp[i + 1]
+        vals[s + int(np.searchsorted(ci[s:e], i))] = float(len(offs)) + rng.uniform(0.0, 1.0)
+    return Csr(rp, ci, vals)
+
+
 def random_sparse(n: int, density: float, seed: int = SEED, dominant: bool = True) -> Csr:
     """Random sparse matrix with a full diagonal; M-matrix-like when dominant."""
     rng = np.random.default_rng(seed)

@@ -367,3 +367,22 @@ def test_template_kernel_variants(name, env, marker, kind, g, gz, k, ns, nt, mon
     np.testing.assert_allclose(f.residual_history(), fo.resid,
                                rtol=max(1e-12, (fo.pattern.nnz + 64) * np.finfo(float).eps))
     assert np.array_equal(x, oracle.apply(fo, b, nt))
+
+
+@pytest.mark.parametrize("offsets,k", [((-40, -33, 33, 40), 1), ((-70, -3, 2, 65), 0),
+                                       ((-100, -64, 64, 100), 0), ((-100, -64, 64, 100), 1),
+                                       ((-100, -64, -1, 1, 64, 100), 1)])
+@pytest.mark.parametrize("staged", ["0", "1"])
+def test_banded_templates(offsets, k, staged, monkeypatch):
+    """Template patterns whose pivot groups lie away from the row (the last group's TMA box then
+    misses the tile's own rows, and pivots span several slices): both sweep kernels, factors and
+    x bitwise the oracle's."""
+    monkeypatch.setenv("FASTILU_TSELL_STAGED", staged)
+    a = P.banded(3001, offsets)
+    b = P.rhs_positive(a.n)
+    f, vals, _, x = gpu_run(a, k, 3, 4, b)
+    assert f.info().startswith("path=tsell"), f.info()
+    assert ("staged=1" in f.info()) == (staged == "1"), f.info()
+    fo = oracle.compute(a, k, 3)
+    assert np.array_equal(vals, fo.vals)
+    assert np.array_equal(x, oracle.apply(fo, b, 4))
