@@ -121,6 +121,16 @@ fastilu_status fastilu_set_values_device(fastilu_handle h, const double *values_
  * Returns ZERO_DIAG / ZERO_PIVOT with the row in fastilu_error_index. */
 fastilu_status fastilu_compute(fastilu_handle h, int nsweeps);
 
+/* fastilu_set_values(values) followed by fastilu_compute(nsweeps), with the upload of the new
+ * values (HOST array, same layout as for fastilu_set_values; pin it for overlap) pipelined with
+ * the numeric phase: row chunks of at least A's bandwidth are uploaded on a second stream while
+ * earlier chunks are scaled and swept (PAPER.md:121-125 numeric phase).  Factors,
+ * pattern of errors and every per-entry value are those of set_values + compute; the residual
+ * history is summed per chunk (equal up to rounding).  Falls back to the two calls when the
+ * pipeline does not apply (multi-GPU, CSR or block path, omega != 1, fewer than 2 chunks).
+ * Synchronises at the end like fastilu_compute; errors as fastilu_compute. */
+fastilu_status fastilu_compute_host(fastilu_handle h, const double *values, int nsweeps);
+
 /* The paper's asynchronous in-place sweeps: every thread updates its entries in
  * place, reading whatever mix of old and already-updated values it finds (Gauss-Seidel-like,
  * non-deterministic; same fixed point).  The residual history is the by-product of those

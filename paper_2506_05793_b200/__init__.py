@@ -59,6 +59,7 @@ _SIGS = {
     "fastilu_compute_tol": (C.c_int, [H, C.c_double, C.c_int, C.POINTER(C.c_int)]),
     "fastilu_compute_warmup": (C.c_int, [H, C.c_int]),
     "fastilu_compute_async": (C.c_int, [H, C.c_int]),
+    "fastilu_compute_host": (C.c_int, [H, F64P, C.c_int]),
     "fastilu_apply": (C.c_int, [H, C.c_void_p, C.c_void_p, C.c_int]),
     "fastilu_apply_host": (C.c_int, [H, F64P, F64P, C.c_int]),
     "fastilu_destroy": (C.c_int, [H]),
@@ -254,6 +255,13 @@ class FastILU:
 
     def compute(self, nsweeps: int):
         _check(lib().fastilu_compute(self._h, int(nsweeps)), "fastilu_compute", self._h)
+
+    def compute_host(self, values, nsweeps: int):
+        """fastilu_compute_host: new host values + nsweeps sweeps, upload pipelined with the
+        numeric phase (pass a pinned array for overlap)."""
+        v = np.ascontiguousarray(values, dtype=np.float64)
+        _check(lib().fastilu_compute_host(self._h, _p(v, F64P), int(nsweeps)),
+               "fastilu_compute_host", self._h)
 
     def compute_async(self, nsweeps: int):
         """The paper's asynchronous in-place sweeps (non-deterministic; fastilu_compute_async)."""

@@ -108,6 +108,9 @@ struct TDev {
 // A's CSR values -> template slots aT (nslices * WA * 32), rows [0, nrows)
 cudaError_t launch_tsell_gather_a(const TDev &t, const double *aval, int64_t nrows, double *aT,
                                   cudaStream_t st);
+// same for local rows [r0, r1) only
+cudaError_t launch_tsell_gather_a_range(const TDev &t, const double *aval, int64_t r0,
+                                        int64_t r1, double *aT, cudaStream_t st);
 cudaError_t launch_tsell_init(const TDev &t, const double *aT, const double *s,
                               const double *ad, int64_t r0, int64_t r1, double *ahatT,
                               double *vals, double *udiag, ErrFlags *err, double shift,

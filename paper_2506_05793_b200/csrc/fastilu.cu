@@ -37,6 +37,12 @@ struct fastilu_handle_s {
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
+  // fastilu_compute_host: value upload pipelined with the compute (copy stream, chunk events)
+  cudaStream_t copy_stream = nullptr;
+  std::vector<cudaEvent_t> chunk_ev;
+  std::vector<int64_t> h_arp;  // local A row pointers (offsets into the local values)
+  double *d_r2c = nullptr;     // per-chunk residual sums (chunks x nsweeps)
+  int r2c_cap = 0;
   // partition (global indices)
   int64_t n = 0, global_n = 0, row_begin = 0, n_lead = 0;
   int64_t G = 0, H = 0, lbase = 0, nloc = 0, E = 0;
@@ -697,6 +703,7 @@ static fastilu_status create_impl(fastilu_handle h, int64_t n, const int64_t *ro
   std::vector<int64_t> arp(h->nloc + 1);
   std::vector<int32_t> adiag(h->nloc), aci(h->nnzA_loc, 0), apos(h->nnzA_loc, 0);
   for (int64_t r = 0; r <= h->nloc; r++) arp[r] = row_ptr[ar0 + r] - h->a_in_off;
+  h->h_arp = arp;
   {
     std::vector<std::thread> th;
     int T = std::max(1, std::min<int>(nt, (int)(h->nloc / 4096 + 1)));
@@ -1070,10 +1077,10 @@ static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, i
   // a2: scaling for every local row (lower ghosts included), then the upper ghosts' s / ad
   if (h->tsell && h->jit_scale) {  // from the diagonal column of A's template copy
     const double *aT = h->d_aT;
-    long long nl = h->nloc;
+    long long z0 = 0, nl = h->nloc;
     double *sp = h->d_s, *adp = h->d_ad, sh = h->opt.shift;
     ErrFlags *ep = h->d_err;
-    void *args[] = {&aT, &nl, &sp, &adp, &ep, &sh};
+    void *args[] = {&aT, &z0, &nl, &sp, &adp, &ep, &sh};
     if (jit_launch(h->jit_scale, (int)((h->nloc + 255) / 256), 256, st, args))
       FAIL(FASTILU_ERR_CUDA);
   } else {
@@ -1260,6 +1267,175 @@ static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, i
   }
   h->computed = true;
   return FASTILU_OK;
+}
+
+// fastilu_compute_host: new values from host memory + nsweeps sweeps, the upload pipelined with
+// the compute.  Chunks of >= A's bandwidth rows: chunk c's values go up on a copy stream; on
+// the compute stream chunk c is gathered and scaled, chunk c-1 gets ahat (its s neighbours now
+// exist), and the sweeps advance along a diagonal (step d: sweep s on chunk d-s+1, s ascending),
+// which keeps every iterate a later chunk still reads alive in the two ping-pong buffers: sweep
+// s of chunk c reads iterate s-1 of rows <= its own only.  Same kernels, same per-entry
+// arithmetic as set_values + compute; only the residual's sum is taken per chunk.
+static fastilu_status compute_host_impl(fastilu_handle h, const double *values, int nsweeps) {
+  const int64_t R = h->st.rows > 0 ? h->st.rows : 256;
+  int64_t bwA = 0;
+  for (int32_t o : h->T.offA) bwA = std::max<int64_t>(bwA, std::abs((int64_t)o));
+  int64_t chunk = std::max<int64_t>(bwA, 16 * R);
+  chunk = std::max<int64_t>(chunk, (h->n + 15) / 16);
+  chunk = (chunk + R - 1) / R * R;
+  const int C = (int)((h->n + chunk - 1) / std::max<int64_t>(chunk, 1));
+  const bool ok = h->tsell && !h->comm && h->jit_st && h->jit_st_init && h->jit_ahat &&
+                  h->jit_scale && nsweeps >= 1 && h->opt.omega == 1.0 && h->G == 0 &&
+                  h->st.shift == 0 && C >= 2 && !fused_enabled("FASTILU_NO_FUSED_SWEEPS") &&
+                  !std::getenv("FASTILU_NO_PIPELINE");
+  if (!ok) {
+    fastilu_status us = upload_values(h, values, false);
+    if (us) return us;
+    return compute_impl(h, nsweeps, 0.0, nullptr);
+  }
+  h->computed = false;
+  h->err_index = -1;
+  cudaStream_t st = h->stream;
+  if (!h->copy_stream) CU(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
+  while ((int)h->chunk_ev.size() < C) {
+    cudaEvent_t e;
+    CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    h->chunk_ev.push_back(e);
+  }
+  if (nsweeps > h->hist_cap) {
+    if (h->d_r2) cudaFree(h->d_r2);
+    if (h->h_r2) cudaFreeHost(h->h_r2);
+    h->d_r2 = nullptr;
+    h->h_r2 = nullptr;
+    CU(dalloc(&h->d_r2, nsweeps));
+    CU(cudaMallocHost((void **)&h->h_r2, sizeof(double) * nsweeps));
+    h->hist_cap = nsweeps;
+  }
+  if (C * nsweeps > h->r2c_cap) {
+    if (h->d_r2c) cudaFree(h->d_r2c);
+    h->d_r2c = nullptr;
+    CU(dalloc(&h->d_r2c, (int64_t)C * nsweeps));
+    h->r2c_cap = C * nsweeps;
+  }
+  auto rb = [&](int c) { return std::min<int64_t>((int64_t)c * chunk, h->n); };
+  CU(cudaMemsetAsync(h->d_err, 0xff, sizeof(ErrFlags), st));
+  CU(cudaEventRecord(h->ev[0], st));
+  // every chunk's values up front on the copy stream, ordered after the compute stream's
+  // previous work (the previous compute may still read d_aval / d_aT)
+  CU(cudaEventRecord(h->ev[1], st));
+  CU(cudaStreamWaitEvent(h->copy_stream, h->ev[1], 0));
+  for (int c = 0; c < C; c++) {
+    const int64_t a0 = h->h_arp[rb(c)], a1 = h->h_arp[rb(c + 1)];
+    if (a1 > a0)
+      CU(cudaMemcpyAsync(h->d_aval + a0, values + h->a_in_off + a0, sizeof(double) * (a1 - a0),
+                         cudaMemcpyHostToDevice, h->copy_stream));
+    CU(cudaEventRecord(h->chunk_ev[c], h->copy_stream));
+  }
+  const double sh = h->opt.shift;
+  ErrFlags *ep = h->d_err;
+  auto prep = [&](int c) -> fastilu_status {  // gather + scale of chunk c
+    CU(cudaStreamWaitEvent(st, h->chunk_ev[c], 0));
+    CU(launch_tsell_gather_a_range(tdev(h), h->d_aval, rb(c), rb(c + 1), h->d_aT, st));
+    const double *aT = h->d_aT;
+    long long z0 = rb(c), z1 = rb(c + 1);
+    double *sp = h->d_s, *adp = h->d_ad;
+    void *args[] = {&aT, &z0, &z1, &sp, &adp, &ep, (void *)&sh};
+    if (jit_launch(h->jit_scale, (int)((z1 - z0 + 255) / 256), 256, st, args)) FAIL(FASTILU_ERR_CUDA);
+    return FASTILU_OK;
+  };
+  auto ahat = [&](int c) -> fastilu_status {
+    const double *aT = h->d_aT, *sv = h->d_s;
+    const unsigned long long *mk = h->d_tmask;
+    long long z0 = rb(c), z1 = rb(c + 1);
+    double *hp = h->d_ahat;
+    void *args[] = {&aT, &sv, &mk, &z0, &z1, &hp, &ep, (void *)&sh};
+    if (jit_launch(h->jit_ahat, (int)((z1 - z0 + 255) / 256), 256, st, args)) FAIL(FASTILU_ERR_CUDA);
+    return FASTILU_OK;
+  };
+  auto sweep = [&](int sw, int c) -> fastilu_status {
+    const int ib = (sw - 1) & 1, ob = sw & 1;
+    const double *old = h->d_vals[ib], *ahp = h->d_ahat;
+    double *outp = h->d_vals[ob], *udn = h->d_ud[ob], *part = h->d_partials;
+    const unsigned long long *mk = h->d_tmask;
+    long long a0 = rb(c), a1 = rb(c + 1);
+    double om = 1.0;
+    unsigned long long *zp = &h->d_err->zero_pivot;
+    unsigned int *ctr = h->d_counter;
+    void *sargs[] = {&old, &outp, &ahp, &mk, &udn, &a0, &a1, &om, &part, &zp, &ctr,
+                     h->st_tmap[ib].b, h->st_tmap_own[ib].b};
+    void *fn = h->jit_st;
+    int smem = h->st.smem;
+    if (sw == 1) {
+      fn = h->jit_st_init;
+      smem = h->st_init.smem;
+      sargs[11] = h->st_tmap_ahat.b;
+      sargs[12] = h->st_tmap_own_ahat.b;
+    }
+    const int64_t nt = (a1 - a0 + R - 1) / R;
+    const int grid = (int)std::min<int64_t>(h->st_grid, nt);
+    if (jit_launch_smem(fn, grid, h->st.threads, smem, st, sargs)) FAIL(FASTILU_ERR_CUDA);
+    CU(launch_reduce_reset(h->d_partials, (int)nt, h->d_r2c + (int64_t)c * nsweeps + (sw - 1),
+                           h->d_counter, st));
+    return FASTILU_OK;
+  };
+  auto diag = [&](int d) -> fastilu_status {  // step d: sweep s on chunk d - s + 1
+    for (int sw = 1; sw <= nsweeps; sw++) {
+      const int c = d - sw + 1;
+      if (c < 0 || c >= C) continue;
+      fastilu_status fs = sweep(sw, c);
+      if (fs) return fs;
+    }
+    return FASTILU_OK;
+  };
+  fastilu_status fs;
+  for (int c = 0; c < C; c++) {
+    if ((fs = prep(c))) return fs;
+    if (c >= 1) {
+      if ((fs = ahat(c - 1))) return fs;
+      if ((fs = diag(c - 1))) return fs;
+    }
+  }
+  if ((fs = ahat(C - 1))) return fs;
+  for (int d = C - 1; d <= C + nsweeps - 2; d++)
+    if ((fs = diag(d))) return fs;
+  CU(cudaEventRecord(h->ev[2], st));
+  std::vector<double> r2c((size_t)C * nsweeps);
+  CU(cudaMemcpyAsync(h->h_err, h->d_err, sizeof(ErrFlags), cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(r2c.data(), h->d_r2c, sizeof(double) * r2c.size(), cudaMemcpyDeviceToHost,
+                     st));
+  CU(cudaStreamSynchronize(st));
+  h->have_values = true;
+  h->t_init = 0.f;
+  CU(cudaEventElapsedTime(&h->t_sweeps, h->ev[0], h->ev[2]));
+  h->t_sweep1 = h->t_sweeps;
+  h->last_ns = 0;
+  h->resid.assign(nsweeps, 0.0);
+  for (int sw = 0; sw < nsweeps; sw++) {
+    double t = 0.0;
+    for (int c = 0; c < C; c++) t += r2c[(size_t)c * nsweeps + sw];
+    h->resid[sw] = std::sqrt(t);
+  }
+  h->cur = nsweeps & 1;
+  h->vals_cur = h->d_vals[h->cur];
+  h->ud_cur = h->d_ud[h->cur];
+  ErrFlags ef = *h->h_err;
+  if (ef.zero_diag != ~0ull) {
+    h->err_index = (int64_t)ef.zero_diag + h->lbase;
+    return FASTILU_ERR_ZERO_DIAG;
+  }
+  if (ef.zero_pivot != ~0ull) {
+    h->err_index = (int64_t)ef.zero_pivot + h->lbase;
+    return FASTILU_ERR_ZERO_PIVOT;
+  }
+  h->computed = true;
+  return FASTILU_OK;
+}
+
+extern "C" fastilu_status fastilu_compute_host(fastilu_handle h, const double *values,
+                                               int nsweeps) {
+  if (!h || !values || !h->d_aval || nsweeps < 0) FAIL(FASTILU_ERR_INVALID_ARG);
+  cudaSetDevice(h->device);
+  return compute_host_impl(h, values, nsweeps);
 }
 
 extern "C" fastilu_status fastilu_compute(fastilu_handle h, int nsweeps) {
@@ -1790,6 +1966,9 @@ extern "C" fastilu_status fastilu_destroy(fastilu_handle h) {
   for (int i = 0; i < 6; i++)
     if (h->ev[i]) cudaEventDestroy(h->ev[i]);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+  for (cudaEvent_t e : h->chunk_ev) cudaEventDestroy(e);
+  if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
+  if (h->d_r2c) cudaFree(h->d_r2c);
   delete h;
   return FASTILU_OK;
 }

@@ -658,9 +658,9 @@ __device__ __forceinline__ bool tbit(const unsigned long long *m, int w) {
 
 // A's values in CSR order -> A's template slots (once per fastilu_set_values; lane per row).
 __global__ void __launch_bounds__(256)
-tsell_gather_a_kernel(TDev t, const double *__restrict__ aval, int64_t nrows,
+tsell_gather_a_kernel(TDev t, const double *__restrict__ aval, int64_t r0, int64_t nrows,
                       double *__restrict__ aT) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t i = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nrows) return;
   const int64_t sl = i >> 5, ln = i & 31;
   for (int a = 0; a < t.WA; a++) {
@@ -671,8 +671,13 @@ tsell_gather_a_kernel(TDev t, const double *__restrict__ aval, int64_t nrows,
 
 cudaError_t launch_tsell_gather_a(const TDev &t, const double *aval, int64_t nrows, double *aT,
                                   cudaStream_t st) {
-  if (nrows <= 0) return cudaSuccess;
-  tsell_gather_a_kernel<<<(unsigned)((nrows + 255) / 256), 256, 0, st>>>(t, aval, nrows, aT);
+  return launch_tsell_gather_a_range(t, aval, 0, nrows, aT, st);
+}
+
+cudaError_t launch_tsell_gather_a_range(const TDev &t, const double *aval, int64_t r0,
+                                        int64_t r1, double *aT, cudaStream_t st) {
+  if (r1 <= r0) return cudaSuccess;
+  tsell_gather_a_kernel<<<(unsigned)((r1 - r0 + 255) / 256), 256, 0, st>>>(t, aval, r0, r1, aT);
   return cudaGetLastError();
 }
 

@@ -386,3 +386,50 @@ def test_banded_templates(offsets, k, staged, monkeypatch):
     fo = oracle.compute(a, k, 3)
     assert np.array_equal(vals, fo.vals)
     assert np.array_equal(x, oracle.apply(fo, b, 4))
+
+
+@pytest.mark.parametrize("kind,g,gz,k,ns", [("27pt", 24, 70, 1, 3), ("27pt", 20, 41, 2, 2),
+                                            ("7pt", 40, 90, 0, 4), ("27pt", 24, 70, 1, 1)])
+def test_compute_host_pipelined(kind, g, gz, k, ns):
+    """fastilu_compute_host (values uploaded in row chunks, sweeps advanced chunk by chunk along
+    a diagonal) equals set_values + compute bitwise (factors, x), and the oracle."""
+    a = P.make(kind, g, gz)
+    b = P.rhs_positive(a.n)
+    f = F.FastILU(a.row_ptr, a.col_idx, a.values, k)
+    f.compute_host(a.values, ns)
+    v1, _ = f.factors()
+    r1 = f.residual_history()
+    tb = torch.tensor(b, dtype=torch.float64, device="cuda")
+    tx = torch.empty_like(tb)
+    f.apply(tb, tx, 3)
+    torch.cuda.synchronize()
+    x1 = tx.cpu().numpy()
+    f.set_values(a.values)
+    f.compute(ns)
+    v2, _ = f.factors()
+    f.apply(tb, tx, 3)
+    torch.cuda.synchronize()
+    assert np.array_equal(v1, v2)
+    assert np.array_equal(x1, tx.cpu().numpy())
+    fo = oracle.compute(a, k, ns)
+    assert np.array_equal(v1, fo.vals)
+    np.testing.assert_allclose(r1, fo.resid, rtol=max(1e-12, (fo.pattern.nnz + 64) * np.finfo(float).eps))
+
+
+def test_compute_host_new_values_and_errors():
+    """compute_host with scaled values gives the factors of the scaled matrix (the old values are
+    fully replaced), and a zero diagonal is reported like compute's."""
+    a = P.laplace3d_27pt(24, gz=70)
+    f = F.FastILU(a.row_ptr, a.col_idx, a.values, 1)
+    f.compute(2)
+    v2 = a.values * 3.0
+    f.compute_host(v2, 2)
+    g = F.FastILU(a.row_ptr, a.col_idx, v2, 1)
+    g.compute(2)
+    assert np.array_equal(f.factors()[0], g.factors()[0])
+    z = a.values.copy()
+    r = 24 * 24 * 50 + 3
+    z[a.row_ptr[r] + int(np.searchsorted(a.col_idx[a.row_ptr[r]:a.row_ptr[r + 1]], r))] = 0.0
+    with pytest.raises(F.FastILUError) as ei:
+        f.compute_host(z, 2)
+    assert ei.value.status == "ZERO_DIAG" and ei.value.index == r
