@@ -130,6 +130,11 @@ fastilu_status fastilu_compute(fastilu_handle h, int nsweeps);
  * pipeline does not apply (multi-GPU, CSR or block path, omega != 1, fewer than 2 chunks).
  * Synchronises at the end like fastilu_compute; errors as fastilu_compute. */
 fastilu_status fastilu_compute_host(fastilu_handle h, const double *values, int nsweeps);
+/* fastilu_compute_host(values, nsweeps) followed by fastilu_apply_host(b, x, ntrisweeps): the
+ * one-call host-to-host solve step (e2e); b's upload is queued behind the values so it lands
+ * during the compute.  b, x: HOST arrays of n (pinned for overlap).  Synchronises. */
+fastilu_status fastilu_solve_host(fastilu_handle h, const double *values, int nsweeps,
+                                  const double *b, double *x, int ntrisweeps);
 
 /* The paper's asynchronous in-place sweeps: every thread updates its entries in
  * place, reading whatever mix of old and already-updated values it finds (Gauss-Seidel-like,

@@ -60,6 +60,7 @@ _SIGS = {
     "fastilu_compute_warmup": (C.c_int, [H, C.c_int]),
     "fastilu_compute_async": (C.c_int, [H, C.c_int]),
     "fastilu_compute_host": (C.c_int, [H, F64P, C.c_int]),
+    "fastilu_solve_host": (C.c_int, [H, F64P, C.c_int, F64P, F64P, C.c_int]),
     "fastilu_apply": (C.c_int, [H, C.c_void_p, C.c_void_p, C.c_int]),
     "fastilu_apply_host": (C.c_int, [H, F64P, F64P, C.c_int]),
     "fastilu_destroy": (C.c_int, [H]),
@@ -262,6 +263,16 @@ class FastILU:
         v = np.ascontiguousarray(values, dtype=np.float64)
         _check(lib().fastilu_compute_host(self._h, _p(v, F64P), int(nsweeps)),
                "fastilu_compute_host", self._h)
+
+    def solve_host(self, values, nsweeps: int, b, ntrisweeps: int, out=None):
+        """fastilu_solve_host: new host values, nsweeps sweeps, x = M^-1 b (host arrays)."""
+        v = np.ascontiguousarray(values, dtype=np.float64)
+        bb = np.ascontiguousarray(b, dtype=np.float64)
+        x = out if out is not None else np.empty(self.n, dtype=np.float64)
+        _check(lib().fastilu_solve_host(self._h, _p(v, F64P), int(nsweeps), _p(bb, F64P),
+                                        _p(x, F64P), int(ntrisweeps)), "fastilu_solve_host",
+               self._h)
+        return x
 
     def compute_async(self, nsweeps: int):
         """The paper's asynchronous in-place sweeps (non-deterministic; fastilu_compute_async)."""

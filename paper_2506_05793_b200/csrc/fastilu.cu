@@ -40,6 +40,7 @@ struct fastilu_handle_s {
   // fastilu_compute_host: value upload pipelined with the compute (copy stream, chunk events)
   cudaStream_t copy_stream = nullptr;
   std::vector<cudaEvent_t> chunk_ev;
+  int chunk_b = 0;  // index of the event after the right-hand side's upload (solve_host)
   std::vector<int64_t> h_arp;  // local A row pointers (offsets into the local values)
   double *d_r2c = nullptr;     // per-chunk residual sums (chunks x nsweeps)
   int r2c_cap = 0;
@@ -1269,6 +1270,8 @@ static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, i
   return FASTILU_OK;
 }
 
+static fastilu_status apply_impl(fastilu_handle h, const double *b, double *x, int ntri);
+
 // fastilu_compute_host: new values from host memory + nsweeps sweeps, the upload pipelined with
 // the compute.  Chunks of >= A's bandwidth rows: chunk c's values go up on a copy stream; on
 // the compute stream chunk c is gathered and scaled, chunk c-1 gets ahat (its s neighbours now
@@ -1276,7 +1279,10 @@ static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, i
 // which keeps every iterate a later chunk still reads alive in the two ping-pong buffers: sweep
 // s of chunk c reads iterate s-1 of rows <= its own only.  Same kernels, same per-entry
 // arithmetic as set_values + compute; only the residual's sum is taken per chunk.
-static fastilu_status compute_host_impl(fastilu_handle h, const double *values, int nsweeps) {
+static fastilu_status compute_host_impl(fastilu_handle h, const double *values, int nsweeps,
+                                        const double *b_host = nullptr,
+                                        bool *b_queued = nullptr) {
+  if (b_queued) *b_queued = false;
   const int64_t R = h->st.rows > 0 ? h->st.rows : 256;
   int64_t bwA = 0;
   for (int32_t o : h->T.offA) bwA = std::max<int64_t>(bwA, std::abs((int64_t)o));
@@ -1297,7 +1303,7 @@ static fastilu_status compute_host_impl(fastilu_handle h, const double *values, 
   h->err_index = -1;
   cudaStream_t st = h->stream;
   if (!h->copy_stream) CU(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
-  while ((int)h->chunk_ev.size() < C) {
+  while ((int)h->chunk_ev.size() < C + 1) {
     cudaEvent_t e;
     CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     h->chunk_ev.push_back(e);
@@ -1330,6 +1336,14 @@ static fastilu_status compute_host_impl(fastilu_handle h, const double *values, 
       CU(cudaMemcpyAsync(h->d_aval + a0, values + h->a_in_off + a0, sizeof(double) * (a1 - a0),
                          cudaMemcpyHostToDevice, h->copy_stream));
     CU(cudaEventRecord(h->chunk_ev[c], h->copy_stream));
+  }
+  if (b_host) {  // solve_host: the right-hand side follows the values on the copy stream
+    if (!h->d_bx) CU(dalloc(&h->d_bx, 2 * h->n));
+    CU(cudaMemcpyAsync(h->d_bx, b_host, sizeof(double) * h->n, cudaMemcpyHostToDevice,
+                       h->copy_stream));
+    CU(cudaEventRecord(h->chunk_ev[C], h->copy_stream));
+    h->chunk_b = C;
+    *b_queued = true;
   }
   const double sh = h->opt.shift;
   ErrFlags *ep = h->d_err;
@@ -1436,6 +1450,30 @@ extern "C" fastilu_status fastilu_compute_host(fastilu_handle h, const double *v
   if (!h || !values || !h->d_aval || nsweeps < 0) FAIL(FASTILU_ERR_INVALID_ARG);
   cudaSetDevice(h->device);
   return compute_host_impl(h, values, nsweeps);
+}
+
+// fastilu_solve_host: compute_host(values, nsweeps) + apply_host(b, x, ntri), b's upload queued
+// behind the values so that it lands during the compute's tail
+extern "C" fastilu_status fastilu_solve_host(fastilu_handle h, const double *values, int nsweeps,
+                                             const double *b, double *x, int ntrisweeps) {
+  if (!h || !values || !h->d_aval || nsweeps < 0 || ntrisweeps < 1 ||
+      (h->n > 0 && (!b || !x)))
+    FAIL(FASTILU_ERR_INVALID_ARG);
+  cudaSetDevice(h->device);
+  bool queued = false;
+  fastilu_status s = compute_host_impl(h, values, nsweeps, b, &queued);
+  if (s) return s;
+  if (!queued) return fastilu_apply_host(h, b, x, ntrisweeps);
+  CU(cudaStreamWaitEvent(h->stream, h->chunk_ev[h->chunk_b], 0));
+  CU(cudaEventRecord(h->ev[3], h->stream));
+  s = apply_impl(h, h->d_bx, h->d_bx + h->n, ntrisweeps);
+  if (s) return s;
+  CU(cudaEventRecord(h->ev[4], h->stream));
+  h->apply_timed = true;
+  CU(cudaMemcpyAsync(x, h->d_bx + h->n, sizeof(double) * h->n, cudaMemcpyDeviceToHost,
+                     h->stream));
+  CU(cudaStreamSynchronize(h->stream));
+  return FASTILU_OK;
 }
 
 extern "C" fastilu_status fastilu_compute(fastilu_handle h, int nsweeps) {

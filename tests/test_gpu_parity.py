@@ -433,3 +433,16 @@ def test_compute_host_new_values_and_errors():
     with pytest.raises(F.FastILUError) as ei:
         f.compute_host(z, 2)
     assert ei.value.status == "ZERO_DIAG" and ei.value.index == r
+
+
+def test_solve_host_equals_compute_and_apply():
+    """fastilu_solve_host (values + b uploaded on the copy stream) = compute + apply, bitwise."""
+    a = P.laplace3d_27pt(24, gz=70)
+    b = P.rhs_positive(a.n)
+    f = F.FastILU(a.row_ptr, a.col_idx, a.values, 1)
+    x1 = f.solve_host(a.values, 3, b, 4)
+    f.compute(3)
+    x2 = f.apply_host(b, 4)
+    assert np.array_equal(x1, x2)
+    fo = oracle.compute(a, 1, 3)
+    assert np.array_equal(x1, oracle.apply(fo, b, 4))
