@@ -117,6 +117,10 @@ struct fastilu_handle_s {
   int lag_grid = 0;
   void *jit_scale = nullptr, *jit_ahat = nullptr;  // template-specialised a2 / a3 (tsell)
   void *jit_jac[2] = {nullptr, nullptr};            // template-specialised a8 / a9 sweeps
+  void *jit_jac2[2] = {nullptr, nullptr};  // two lagged sweeps per launch (single GPU)
+  double *d_z3 = nullptr, *d_w3 = nullptr;  // third iterate buffers of the paired sweeps
+  unsigned int *d_j2ws = nullptr;           // counter + per-tile flags of a paired launch
+  int j2_grid = 0, j2_lag = 0;
   StagedCfg st{}, st_init{};
   int st_grid = 0;
   int64_t st_ntiles = 0;
@@ -468,6 +472,13 @@ static fastilu_status setup_tsell(fastilu_handle h, const std::vector<unsigned l
         else
           h->jit_st_init = nullptr;
         h->st_grid = (int)std::min<int64_t>((int64_t)sm_count(h->device) * sbps, h->st_ntiles);
+        if (std::getenv("FASTILU_DEBUG")) {
+          int sregs = 0, sloc = 0, dummy = 0;
+          jit_func_info(h->jit_st, &sregs, &sloc, c.threads, &dummy);
+          fprintf(stderr, "fastilu: staged threads=%d parts=%d rows=%d smem=%d regs=%d local=%d "
+                  "blocks/SM=%d grid=%d\n", c.threads, c.parts, c.rows, c.smem, sregs, sloc, sbps,
+                  h->st_grid);
+        }
       } else {
         if (std::getenv("FASTILU_DEBUG"))
           fprintf(stderr, "fastilu: staged sweep unavailable: %s\n", log.c_str());
@@ -507,6 +518,29 @@ static fastilu_status setup_tsell(fastilu_handle h, const std::vector<unsigned l
     if (jit_get(jl, "fastilu_tsell_jac_L", h->device, &h->jit_jac[0], &log) ||
         jit_get(ju, "fastilu_tsell_jac_U", h->device, &h->jit_jac[1], &log))
       h->jit_jac[0] = h->jit_jac[1] = nullptr;
+  }
+  // two lagged Jacobi sweeps per launch: opt-in (FASTILU_JAC2=1), measured
+  // slower than the streaming sweeps (c4 apply 6.3-7.2 ms vs 5.8 ms)
+  if (h->opt.nranks <= 1 && h->jit_jac[0] && h->jit_jac[1] && std::getenv("FASTILU_JAC2") &&
+      atoi(std::getenv("FASTILU_JAC2")) != 0) {
+    int lb = 0, ub = 0;
+    const char *em = std::getenv("FASTILU_JAC2_MODE");
+    const unsigned j2m = em ? (unsigned)atoi(em) : 0u;
+    if (!jit_get(jacobi_pair_source(T, true, j2m), "fastilu_tsell_jac2_L", h->device,
+                 &h->jit_jac2[0], &log) &&
+        !jit_get(jacobi_pair_source(T, false, j2m), "fastilu_tsell_jac2_U", h->device,
+                 &h->jit_jac2[1], &log) &&
+        !jit_occupancy(h->jit_jac2[0], 256, 0, &lb) && !jit_occupancy(h->jit_jac2[1], 256, 0, &ub) &&
+        lb > 0 && ub > 0) {
+      const char *eb = std::getenv("FASTILU_JAC2_BPS"), *el = std::getenv("FASTILU_JAC2_LAG");
+      const int bps = std::min(eb ? std::max(1, atoi(eb)) : 8, std::min(lb, ub));
+      h->j2_grid = sm_count(h->device) * bps;
+      // lag in tiles: above the steps in flight (one per resident block), so item B's
+      // dependencies are done when it starts
+      h->j2_lag = el ? std::max(1, atoi(el)) : h->j2_grid + 64;
+    } else {
+      h->jit_jac2[0] = h->jit_jac2[1] = nullptr;
+    }
   }
   // lagged multi-sweep trisolve: opt-in (FASTILU_TRILAG=1), measured slower than the streaming
   // per-sweep kernels (c4 5+5: 9.2-16 ms vs 6.7 ms)
@@ -1631,8 +1665,78 @@ static int jit_jacobi(fastilu_handle h, bool lower, const double *vals, const do
                     args);
 }
 
+// a8 + a9 with two sweeps per launch (tsell.h jacobi_pair_source): z^t lives in zb[t % 3] so a
+// launch's input, middle and output iterates are distinct buffers; an odd sweep left over runs
+// the streaming kernel.  The last U sweep writes x = s o w.
+static fastilu_status apply_jac2(fastilu_handle h, const double *b, double *x, int ntri) {
+  cudaStream_t st = h->stream;
+  const int64_t R = 256, ntiles = (h->n + R - 1) / R;
+  const size_t ws = 128 + (size_t)ntiles;
+  if (!h->d_z3) {
+    CU(dalloc(&h->d_z3, h->E));
+    CU(dalloc(&h->d_w3, h->E));
+    CU(cudaMemset(h->d_z3, 0, sizeof(double) * h->E));
+    CU(cudaMemset(h->d_w3, 0, sizeof(double) * h->E));
+    CU(cudaMalloc((void **)&h->d_j2ws, ws));
+  }
+  const int64_t r0 = h->G, r1 = h->G + h->n;
+  const double om = h->opt.omega_tri;
+  const double *vals = h->vals_cur, *ud = h->ud_cur;
+  double *zb[3] = {h->d_z[0], h->d_z[1], h->d_z3}, *wb[3] = {h->d_w[0], h->d_w[1], h->d_w3};
+  unsigned int *ctr = h->d_j2ws;
+  unsigned char *flags = reinterpret_cast<unsigned char *>(h->d_j2ws) + 128;
+  auto pair = [&](bool lower, const double *rhs, double **vb, int t, bool final_x) -> int {
+    if (cudaMemsetAsync(h->d_j2ws, 0, ws, st) != cudaSuccess) return 1;
+    const double *xa = vb[(t - 1) % 3];
+    double *xb = vb[t % 3], *xc = vb[(t + 1) % 3], *xf = x;
+    const unsigned long long *mk = h->d_tmask;
+    const double *sv = h->d_s;
+    long long a0 = r0, a1 = r1, g = h->G, nt = ntiles;
+    double omv = om;
+    int fx = final_x ? 1 : 0, lag = h->j2_lag;
+    const int64_t bw = lower ? -(int64_t)h->T.off[0] : (int64_t)h->T.off[h->T.W - 1];
+    int dep = (int)std::min<int64_t>(ntiles, (bw + R - 1) / R + 1);
+    const int grid = (int)std::min<int64_t>(h->j2_grid, ntiles + lag);
+    void *args[] = {&vals, &ud, &mk, &rhs, &xa, &xb, &xc, &xf, &sv, &a0, &a1, &g, &omv, &fx,
+                    &ctr, &flags, &nt, &lag, &dep};
+    return jit_launch(h->jit_jac2[lower ? 0 : 1], grid, 256, st, args);
+  };
+  // a8: t = 1: z1 = w y, y = s o b (z0 = 0)
+  CU(launch_trisolve_first_L(b, h->d_s, h->d_y, zb[1], r0, r1, h->G, om, st));
+  for (int t = 2; t <= ntri;) {
+    if (t + 1 <= ntri) {
+      if (pair(true, h->d_y, zb, t, false)) FAIL(FASTILU_ERR_CUDA);
+      t += 2;
+    } else {
+      if (jit_jacobi(h, true, vals, nullptr, h->d_y, zb[(t - 1) % 3], zb[t % 3], nullptr, r0, r1,
+                     0, om, false))
+        FAIL(FASTILU_ERR_CUDA);
+      t += 1;
+    }
+  }
+  const double *zf = zb[ntri % 3];
+  // a9: t = 1: w1 = w z / u_ii; the last sweep writes x = s o w
+  CU(launch_trisolve_first_U(zf, ud, h->d_s, wb[1], x, r0, r1, h->G, om, ntri == 1, st));
+  for (int t = 2; t <= ntri;) {
+    if (t + 1 <= ntri) {
+      if (pair(false, zf, wb, t, t + 1 == ntri)) FAIL(FASTILU_ERR_CUDA);
+      t += 2;
+    } else {
+      if (jit_jacobi(h, false, vals, ud, zf, wb[(t - 1) % 3], wb[t % 3], x, r0, r1, h->G, om,
+                     t == ntri))
+        FAIL(FASTILU_ERR_CUDA);
+      t += 1;
+    }
+  }
+  return FASTILU_OK;
+}
+
 static fastilu_status apply_impl(fastilu_handle h, const double *b, double *x, int ntri) {
   cudaStream_t st = h->stream;
+  if (h->tsell && !h->comm && h->jit_jac2[0] && h->jit_jac2[1] && ntri >= 3 &&
+      !(h->jit_lag[0] && h->jit_lag[1]) && !(h->jit_tri[0] && h->jit_tri[1]) &&
+      !fused_enabled("FASTILU_NO_FUSED_TRISOLVE"))
+    return apply_jac2(h, b, x, ntri);
   if (h->tsell && !h->comm && h->jit_lag[0] && h->jit_lag[1] && ntri >= 1 &&
       !(h->jit_tri[0] && h->jit_tri[1]))
     return apply_lag(h, b, x, ntri);
@@ -1990,7 +2094,7 @@ extern "C" fastilu_status fastilu_destroy(fastilu_handle h) {
                   h->d_rclass, h->d_coff, h->d_caoff, h->d_prog, h->d_toff, h->d_toffA,
                   h->d_tasrc, h->d_tw2a, h->d_tmask, h->d_counter, h->gm_V, h->gm_w,
                   h->gm_ext, h->gm_u, h->gm_r, h->gm_part, h->gm_c, h->d_aT, h->d_tribuf,
-                  h->d_triws, h->d_fptr_v, h->d_fptr_u, h->d_fpart, h->d_fws,
+                  h->d_triws, h->d_z3, h->d_w3, h->d_j2ws, h->d_fptr_v, h->d_fptr_u, h->d_fpart, h->d_fws,
                   h->d_bptr, h->d_tptr, h->d_brow, h->d_bcol, h->d_bdiag, h->d_terms,
                   h->d_vb[0], h->d_vb[1], h->d_ahb};
   for (void *p : ptrs)

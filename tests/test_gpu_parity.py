@@ -341,6 +341,13 @@ _VARIANTS = [
     ("loads-first Jacobi kernels", {"FASTILU_JIT_JACOBI_MODE": "1"}, None),
     ("128-row tiles", {"FASTILU_TSELL_STAGED": "1", "FASTILU_TSELL_ST_THREADS": "256"}, None),
     ("wavefront trisolve", {"FASTILU_JIT_TRISOLVE": "1"}, None),
+    ("paired Jacobi sweeps", {"FASTILU_JAC2": "1"}, None),
+    ("paired Jacobi sweeps, L1 gathers + L2 hints", {"FASTILU_JAC2": "1",
+                                                     "FASTILU_JAC2_MODE": "3"}, None),
+    ("paired Jacobi sweeps, lag 1 (flag waits taken)", {"FASTILU_JAC2": "1", "FASTILU_JAC2_LAG": "1",
+                                                        "FASTILU_JAC2_BPS": "2"}, None),
+    ("paired Jacobi sweeps, lag 5, one block per SM", {"FASTILU_JAC2": "1", "FASTILU_JAC2_LAG": "5",
+                                                       "FASTILU_JAC2_BPS": "1"}, None),
     ("lagged 3-sweep trisolve", {"FASTILU_TRILAG": "1", "FASTILU_TRILAG_S": "3"}, None),
     ("lagged 5-sweep trisolve", {"FASTILU_TRILAG": "1", "FASTILU_TRILAG_S": "5"}, None),
     ("divisions through __ddiv_rn", {"FASTILU_TSELL_STAGED": "1", "FASTILU_TSELL_ST_OPTS": "0"},
