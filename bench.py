@@ -60,6 +60,28 @@ def bsr_roofline(info, n, sweep_ms):
                            "per lane-cycle (no FMA)", "traffic": None, "terms_per_sweep": terms}
 
 
+def smem_port(info, n, launch_ms, sm_mhz, sms=148):
+    """Staged template sweep: shared-memory port bytes per launch, a lower
+    bound -- one 8-byte LDS per term and row (the pivot value u_kj) plus the TMA pivot-box
+    writes (groups x box bytes per tile) -- against 128 B/clk/SM (B300_MICROARCH.md LDS/STS
+    table) x SMs x the SM clock measured in the timed region."""
+    import re
+    kv = dict(re.findall(r"(\w+)=(\S+)", info))
+    if kv.get("staged") != "1" or launch_ms <= 0:
+        return None
+    terms, rows = int(kv["terms"]), int(kv["st_rows"])
+    bx, by, bz = (int(v) for v in kv["st_box"].split("x"))
+    tiles = -(-n // rows)
+    lds = n * terms * 8
+    tma = tiles * int(kv["st_groups"]) * bx * by * bz * 8
+    mhz = sm_mhz or 1965.0
+    peak = 128 * sms * mhz * 1e6 / 1e9
+    ach = (lds + tma) / (launch_ms * 1e-3) / 1e9
+    return {"achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+            "bytes_per_launch": lds + tma, "lds_bytes": lds, "tma_bytes": tma,
+            "peak_source": f"128 B/clk/SM x {sms} SMs x {mhz:.0f} MHz (median SM clock, timed region)"}
+
+
 def byte_model(n, nnz_A, nnz_S, nnz_Ls, ns, nt):
     """Algorithmic bytes."""
     sp = 4 if nnz_S < 2**31 else 8
@@ -348,6 +370,9 @@ def run_ours(args, wl):
             "algorithmic_bytes_per_launch": bm["B_f"]}
     if info.startswith("path=bsr"):
         roof = bsr_roofline(info, n, sweep_ms / max(ns, 1))
+    else:  # the secondary bound of the staged sweep (its shared-memory port)
+        roof["smem_port"] = smem_port(info, n, per_launch_ms, clk.get("sm_mhz"),
+                                      torch.cuda.get_device_properties(dev).multi_processor_count)
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

@@ -232,6 +232,23 @@ def test_tiny_and_diagonal():
     full_check(P.tridiagonal(300), 1, 5, 5)
 
 
+def test_empty_matrix():
+    """n = 0 (degenerate case): create, compute and apply succeed and do nothing; the oracle
+    agrees (empty pattern, empty x)."""
+    a = P.Csr(np.zeros(1), np.zeros(0), np.zeros(0))
+    fo = oracle.compute(a, 1, 3)
+    assert fo.pattern.nnz == 0 and len(oracle.apply(fo, np.zeros(0), 5)) == 0
+    f = F.FastILU(a.row_ptr, a.col_idx, a.values, 1)
+    f.compute(3)
+    b = torch.empty(0, dtype=torch.float64, device="cuda")
+    x = torch.empty_like(b)
+    f.apply(b, x, 5)
+    torch.cuda.synchronize()
+    rp, ci, _ = f.pattern()
+    assert list(rp) == [0] and len(ci) == 0
+    f.close()
+
+
 def test_errors():
     a = P.laplace3d_7pt(4)
     v = a.values.copy()
