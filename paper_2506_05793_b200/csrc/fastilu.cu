@@ -465,7 +465,7 @@ static fastilu_status setup_tsell(fastilu_handle h, const std::vector<unsigned l
         const int nsi = ev_si ? std::max(2, atoi(ev_si)) : nst;
         const std::string s2 = sweep_source_staged(T, sthreads, sparts, nsi, sminb, true, &ci,
                                                    sopts | kStagedFromAhat);
-        if (h->opt.nranks <= 1 && !std::getenv("FASTILU_NO_FUSED_INIT") &&
+        if (!std::getenv("FASTILU_NO_FUSED_INIT") &&
             !jit_get(s2, "fastilu_tsell_sweep_st_init", h->device, &h->jit_st_init, &log) &&
             !jit_set_smem(h->jit_st_init, ci.smem) && ci.rows == c.rows && ci.shift == c.shift)
           h->st_init = ci;
@@ -504,7 +504,7 @@ static fastilu_status setup_tsell(fastilu_handle h, const std::vector<unsigned l
   }
   // template-specialised scale / ahat kernels (FASTILU_NO_JIT_PREP=1 keeps the generic ones)
   if (!std::getenv("FASTILU_NO_JIT_PREP") && T.c0 >= 0 && T.w2a[T.c0] >= 0) {
-    const std::string sp = prep_source(T);
+    const std::string sp = prep_source(T, h->opt.nranks > 1);
     if (jit_get(sp, "fastilu_tsell_scale", h->device, &h->jit_scale, &log) ||
         jit_get(sp, "fastilu_tsell_ahat", h->device, &h->jit_ahat, &log))
       h->jit_scale = h->jit_ahat = nullptr;
@@ -1128,17 +1128,20 @@ static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, i
   }
   // a3: ahat and the initial guess (iterate 0) for the owned rows.  With the fused first
   // sweep, iterate 0 is computed from ahat inside sweep 1 and never stored.
-  const bool fuse_init = h->tsell && h->jit_st_init && h->jit_st && !h->comm && !warmup &&
+  // Multi-GPU: the lower ghost rows' diagonal and upper ahat are computed locally (their A
+  // rows and scales are local), so sweep 1 stages them like owned rows and iterate 0 needs no
+  // halo.
+  const bool fuse_init = h->tsell && h->jit_st_init && h->jit_st && h->jit_ahat && !warmup &&
                          !async && nsweeps >= 1 && h->opt.omega == 1.0 &&
                          !fused_enabled("FASTILU_NO_FUSED_SWEEPS");
-  if (h->tsell && fuse_init && h->jit_ahat) {
+  if (h->tsell && fuse_init) {
     const double *aT = h->d_aT, *sv = h->d_s;
     const unsigned long long *mk = h->d_tmask;
-    long long a0 = r0, a1 = r1;
+    long long a0 = 0, a1 = r1, aown = r0;
     double *hp = h->d_ahat, sh = h->opt.shift;
     ErrFlags *ep = h->d_err;
-    void *args[] = {&aT, &sv, &mk, &a0, &a1, &hp, &ep, &sh};
-    if (h->n > 0 && jit_launch(h->jit_ahat, (int)((h->n + 255) / 256), 256, st, args))
+    void *args[] = {&aT, &sv, &mk, &a0, &a1, &hp, &ep, &sh, &aown};
+    if (r1 > 0 && jit_launch(h->jit_ahat, (int)((r1 + 255) / 256), 256, st, args))
       FAIL(FASTILU_ERR_CUDA);
   } else if (h->tsell) {
     CU(launch_tsell_init(tdev(h), h->d_aT, h->d_s, h->d_ad, r0, r1, h->d_ahat, h->d_vals[0],
@@ -1155,8 +1158,11 @@ static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, i
   double thr2 = -1.0;  // (rtol ||Ahat|_S||_F)^2, tolerance mode only
   std::vector<double> r2tol;
   if (rtol > 0.0) {
-    const int64_t na = h->tsell ? h->nsl * h->T.WA * 32 : h->nnzA_loc;
-    CU(launch_sumsq(h->d_ahat, na, h->d_partials, h->d_r2, st));
+    // owned rows only (with the fused first sweep the lower ghosts' ahat is stored too; G is
+    // a whole number of slices on the template path)
+    const int64_t a_off = h->tsell ? (h->G / 32) * h->T.WA * 32 : 0;
+    const int64_t na = h->tsell ? h->nsl * h->T.WA * 32 - a_off : h->nnzA_loc;
+    CU(launch_sumsq(h->d_ahat + a_off, na, h->d_partials, h->d_r2, st));
     double a2 = 0.0;
     CU(cudaMemcpyAsync(h->h_r2, h->d_r2, sizeof(double), cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
@@ -1198,7 +1204,7 @@ static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, i
       }
     }
     const int ib = async ? ib_async : (sw - 1) & 1, ob = async ? ib_async : sw & 1;
-    if (h->comm) {
+    if (h->comm && !(sw == 1 && fuse_init)) {  // fused sweep 1 reads no stored iterate 0
       fastilu_status cs = comm_factor_halo(h->comm, h->d_vals[ib], h->d_rp, h->d_ud[ib], st);
       if (cs) return cs;
     }
@@ -1396,7 +1402,8 @@ static fastilu_status compute_host_impl(fastilu_handle h, const double *values, 
     const unsigned long long *mk = h->d_tmask;
     long long z0 = rb(c), z1 = rb(c + 1);
     double *hp = h->d_ahat;
-    void *args[] = {&aT, &sv, &mk, &z0, &z1, &hp, &ep, (void *)&sh};
+    long long zown = 0;
+    void *args[] = {&aT, &sv, &mk, &z0, &z1, &hp, &ep, (void *)&sh, &zown};
     if (jit_launch(h->jit_ahat, (int)((z1 - z0 + 255) / 256), 256, st, args)) FAIL(FASTILU_ERR_CUDA);
     return FASTILU_OK;
   };
@@ -2061,9 +2068,10 @@ extern "C" fastilu_status fastilu_get_info(fastilu_handle h, char *buf, int cap)
     const size_t L = strlen(tmp);
     snprintf(tmp + L, sizeof(tmp) - L,
              " staged=1 st_threads=%d st_parts=%d st_rows=%d st_shift=%d st_groups=%d "
-             "st_box=32x%dx%d st_stages=%d st_smem_kb=%d st_grid=%d",
+             "st_box=32x%dx%d st_stages=%d st_smem_kb=%d st_grid=%d st_init=%d",
              h->st.threads, h->st.parts, h->st.rows, h->st.shift, h->st.ngroups, h->st.box_cols,
-             h->st.box_slices, h->st.stages, h->st.smem / 1024, h->st_grid);
+             h->st.box_slices, h->st.stages, h->st.smem / 1024, h->st_grid,
+             h->jit_st_init ? 1 : 0);
   }
   if (h->tsell) {
   } else if (h->bsr)

@@ -20,7 +20,7 @@ def split_planes(gz, world):
     return [(gz * r // world, gz * (r + 1) // world) for r in range(world)]
 
 
-def run_partitioned(kind, g, gz, k, ns, nt, world, omega=1.0, omega_tri=1.0):
+def run_partitioned(kind, g, gz, k, ns, nt, world, omega=1.0, omega_tri=1.0, tol=None, info=None):
     plane = g * g
     global_n = plane * gz
     b = P.rhs_positive(global_n)
@@ -39,13 +39,21 @@ def run_partitioned(kind, g, gz, k, ns, nt, world, omega=1.0, omega_tri=1.0):
                           omega_tri=omega_tri, rank=r, nranks=world, comm_kind=F.COMM_LOCAL,
                           group=grp, global_n=global_n, row_begin=z0 * plane,
                           n_lead=lp * plane, n=(z1 - z0) * plane)
-            f.compute(ns)
+            if tol is not None:
+                assert f.compute_tol(tol, 100) > 0
+            else:
+                f.compute(ns)
+            if info is not None:
+                info[r] = f.info()
             vals, s = f.factors()
             tb = torch.tensor(b[z0 * plane:z1 * plane], device="cuda")
             tx = torch.empty_like(tb)
             f.apply(tb, tx, nt)
             torch.cuda.synchronize()
-            out[r] = (vals, s, tx.cpu().numpy(), f.residual_history(), f.pattern())
+            # the end-to-end entry bench.py times at N > 1 (host values + b in, x out)
+            xh = (f.solve_host(blk.values, ns, b[z0 * plane:z1 * plane], nt)
+                  if tol is None else None)
+            out[r] = (vals, s, tx.cpu().numpy(), f.residual_history(), f.pattern(), xh)
             f.close()
         except Exception as e:  # surfaced below
             errs[r] = e
@@ -88,6 +96,7 @@ def test_partition_bitwise_equal_single_gpu(kind, g, gz, k, ns, nt, world):
     assert np.array_equal(sP, s1)
     assert np.array_equal(vP, v1), "partitioned factors differ from the single-GPU run"
     assert np.array_equal(xP, x1), "partitioned x differs from the single-GPU run"
+    assert np.array_equal(np.concatenate([o[5] for o in out]), x1), "solve_host on P ranks"
     for o in out:  # residual: rank-ordered sum of the same per-row terms
         np.testing.assert_allclose(o[3], f1.residual_history(), rtol=1e-12)
     fo = oracle.compute(a, k, ns)
@@ -104,3 +113,21 @@ def test_partition_damped():
     xo = oracle.apply(fo, b, nt, 0.9)
     xP = np.concatenate([o[2] for o in out])
     assert np.all(np.abs(xP - xo) <= 1e-12 * np.abs(xo))
+
+
+def test_partition_fused_first_sweep_and_tolerance():
+    """Template path on 2 ranks: sweep 1 runs the init-fused staged kernel on every rank (the
+    lower ghost rows' ahat is computed locally), and the stopping sweep of compute_tol (norm of
+    ahat over owned rows, residual summed over ranks) equals the single-GPU one."""
+    kind, g, gz, k, nt = "27pt", 16, 16, 1, 3
+    a = P.make(kind, g, gz)
+    f1 = F.FastILU(a.row_ptr, a.col_idx, a.values, k)
+    s1 = f1.compute_tol(1e-10, 100)
+    v1 = f1.factors()[0]
+    info = [None, None]
+    out, _ = run_partitioned(kind, g, gz, k, 0, nt, 2, tol=1e-10, info=info)
+    assert all("staged=1" in i and "st_init=1" in i for i in info), info
+    for o in out:
+        assert len(o[3]) == s1
+        np.testing.assert_allclose(o[3], f1.residual_history(), rtol=1e-12)
+    assert np.array_equal(np.concatenate([o[0] for o in out]), v1)
