@@ -130,6 +130,13 @@ class Clocks:
         for line in self.p.stdout:
             self.rows.append((time.time(), line.strip()))
 
+    def wait_ready(self, timeout=5.0):
+        """Block until nvidia-smi delivered its first sample (its start-up takes ~0.3-1 s, longer
+        than a short timed region)."""
+        t = time.time()
+        while self.p is not None and not self.rows and time.time() - t < timeout:
+            time.sleep(0.02)
+
     def mark_start(self):
         self.t0 = time.time()
 
@@ -286,6 +293,7 @@ def run_ours(args, wl):
         f.apply(b, x, nt)
 
     clocks = Clocks(local)
+    clocks.wait_ready()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
