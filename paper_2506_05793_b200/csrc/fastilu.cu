@@ -122,8 +122,8 @@ struct fastilu_handle_s {
   unsigned int *d_j2ws = nullptr;           // counter + per-tile flags of a paired launch
   int j2_grid = 0, j2_lag = 0;
   StagedCfg st{}, st_init{};
-  int st_grid = 0;
-  int64_t st_ntiles = 0;
+  int st_grid = 0, st_init_grid = 0;
+  int64_t st_ntiles = 0, st_init_ntiles = 0;
   struct alignas(64) TMapBuf {
     unsigned char b[128];
   } st_tmap[2], st_tmap_ahat;  // per iterate buffer d_vals[0/1]; over d_ahat
@@ -458,19 +458,34 @@ static fastilu_status setup_tsell(fastilu_handle h, const std::vector<unsigned l
           !jit_occupancy(h->jit_st, c.threads, c.smem, &sbps) && sbps > 0) {
         h->st = c;
         h->st_ntiles = std::max<int64_t>(1, (h->n + c.shift + c.rows - 1) / c.rows);
-        // the first sweep with the init fused in (single GPU: ghost rows would need ahat)
+        // the first sweep with the init fused in
         StagedCfg ci{};
         // its stage (A's columns only) is small: FASTILU_TSELL_STAGES_INIT more ring slots
         const char *ev_si = std::getenv("FASTILU_TSELL_STAGES_INIT");
         const int nsi = ev_si ? std::max(2, atoi(ev_si)) : nst;
-        const std::string s2 = sweep_source_staged(T, sthreads, sparts, nsi, sminb, true, &ci,
+        // its own block shape: for 2-part templates (27-pt ILU(1)) one part-warp per slice and
+        // 320-row tiles (the A x A terms fit one thread; less box overhang): c4 sweep 1
+        // 3.46 -> 3.08 ms (profiles/r1j_*).  FASTILU_TSELL_INIT_PARTS / _THREADS override.
+        const char *ev_ip = std::getenv("FASTILU_TSELL_INIT_PARTS");
+        const char *ev_it = std::getenv("FASTILU_TSELL_INIT_THREADS");
+        const int iparts = ev_ip ? std::max(1, atoi(ev_ip)) : (sparts == 2 ? 1 : sparts);
+        const int ithreads =
+            ev_it ? std::max(32 * iparts, atoi(ev_it) / (32 * iparts) * 32 * iparts)
+                  : (sparts == 2 && !ev_ip ? 320 : sthreads);
+        const std::string s2 = sweep_source_staged(T, ithreads, iparts, nsi, sminb, true, &ci,
                                                    sopts | kStagedFromAhat);
+        int ibps = 0;
         if (!std::getenv("FASTILU_NO_FUSED_INIT") &&
             !jit_get(s2, "fastilu_tsell_sweep_st_init", h->device, &h->jit_st_init, &log) &&
-            !jit_set_smem(h->jit_st_init, ci.smem) && ci.rows == c.rows && ci.shift == c.shift)
+            !jit_set_smem(h->jit_st_init, ci.smem) && ci.shift == c.shift &&
+            !jit_occupancy(h->jit_st_init, ci.threads, ci.smem, &ibps) && ibps > 0) {
           h->st_init = ci;
-        else
+          h->st_init_ntiles = std::max<int64_t>(1, (h->n + ci.shift + ci.rows - 1) / ci.rows);
+          h->st_init_grid =
+              (int)std::min<int64_t>((int64_t)sm_count(h->device) * ibps, h->st_init_ntiles);
+        } else {
           h->jit_st_init = nullptr;
+        }
         h->st_grid = (int)std::min<int64_t>((int64_t)sm_count(h->device) * sbps, h->st_ntiles);
         if (std::getenv("FASTILU_DEBUG")) {
           int sregs = 0, sloc = 0, dummy = 0;
@@ -596,7 +611,8 @@ static fastilu_status setup_tsell(fastilu_handle h, const std::vector<unsigned l
   CU(dalloc(&h->d_tw2a, T.W));
   CU(dalloc(&h->d_counter, 1));
   CU(dalloc(&h->d_partials,
-            std::max<int64_t>(std::max(h->t_ntiles, h->st_ntiles), kSumsqBlocks)));
+            std::max<int64_t>(std::max(std::max(h->t_ntiles, h->st_ntiles), h->st_init_ntiles),
+                              kSumsqBlocks)));
   if (h->jit_st)
     for (int b = 0; b < 2; b++)
       if (jit_tmap_sell(h->st_tmap[b].b, h->d_vals[b], T.W, h->nsl, h->st.box_cols,
@@ -1228,17 +1244,19 @@ static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, i
         void *sargs[] = {&old, &outp, &ahat, &mk, &udn, &a0, &a1, &om, &part, &zp, &ctr,
                          h->st_tmap[ib].b, h->st_tmap_own[ib].b};
         void *fn = (sw == 1 && !warmup && h->jit_st_first) ? h->jit_st_first : h->jit_st;
-        int smem = h->st.smem;
+        int smem = h->st.smem, grid = h->st_grid, thr = h->st.threads;
+        int64_t ntl = h->st_ntiles;
         if (sw == 1 && fuse_init) {
           fn = h->jit_st_init;
           smem = h->st_init.smem;
+          grid = h->st_init_grid;
+          thr = h->st_init.threads;
+          ntl = h->st_init_ntiles;
           sargs[11] = h->st_tmap_ahat.b;
           sargs[12] = h->st_tmap_own_ahat.b;
         }
-        if (jit_launch_smem(fn, h->st_grid, h->st.threads, smem, st, sargs))
-          return FASTILU_ERR_CUDA;
-        CU(launch_reduce_reset(h->d_partials, (int)h->st_ntiles, h->d_r2 + (sw - 1),
-                               h->d_counter, st));
+        if (jit_launch_smem(fn, grid, thr, smem, st, sargs)) return FASTILU_ERR_CUDA;
+        CU(launch_reduce_reset(h->d_partials, (int)ntl, h->d_r2 + (sw - 1), h->d_counter, st));
         continue;
       }
       void *args[] = {&old, &outp, &ahat, &mk, &udo, &udn, &a0, &a1, &om, &part, &zp, &ctr, &sstr};
@@ -1419,16 +1437,20 @@ static fastilu_status compute_host_impl(fastilu_handle h, const double *values, 
     void *sargs[] = {&old, &outp, &ahp, &mk, &udn, &a0, &a1, &om, &part, &zp, &ctr,
                      h->st_tmap[ib].b, h->st_tmap_own[ib].b};
     void *fn = h->jit_st;
-    int smem = h->st.smem;
+    int smem = h->st.smem, thr = h->st.threads, gmax = h->st_grid;
+    int64_t Rk = R;
     if (sw == 1) {
       fn = h->jit_st_init;
       smem = h->st_init.smem;
+      thr = h->st_init.threads;
+      gmax = h->st_init_grid;
+      Rk = h->st_init.rows;
       sargs[11] = h->st_tmap_ahat.b;
       sargs[12] = h->st_tmap_own_ahat.b;
     }
-    const int64_t nt = (a1 - a0 + R - 1) / R;
-    const int grid = (int)std::min<int64_t>(h->st_grid, nt);
-    if (jit_launch_smem(fn, grid, h->st.threads, smem, st, sargs)) FAIL(FASTILU_ERR_CUDA);
+    const int64_t nt = (a1 - a0 + Rk - 1) / Rk;
+    const int grid = (int)std::min<int64_t>(gmax, nt);
+    if (jit_launch_smem(fn, grid, thr, smem, st, sargs)) FAIL(FASTILU_ERR_CUDA);
     CU(launch_reduce_reset(h->d_partials, (int)nt, h->d_r2c + (int64_t)c * nsweeps + (sw - 1),
                            h->d_counter, st));
     return FASTILU_OK;
@@ -2068,10 +2090,11 @@ extern "C" fastilu_status fastilu_get_info(fastilu_handle h, char *buf, int cap)
     const size_t L = strlen(tmp);
     snprintf(tmp + L, sizeof(tmp) - L,
              " staged=1 st_threads=%d st_parts=%d st_rows=%d st_shift=%d st_groups=%d "
-             "st_box=32x%dx%d st_stages=%d st_smem_kb=%d st_grid=%d st_init=%d",
+             "st_box=32x%dx%d st_stages=%d st_smem_kb=%d st_grid=%d st_init=%d "
+             "st_init_parts=%d st_init_rows=%d",
              h->st.threads, h->st.parts, h->st.rows, h->st.shift, h->st.ngroups, h->st.box_cols,
              h->st.box_slices, h->st.stages, h->st.smem / 1024, h->st_grid,
-             h->jit_st_init ? 1 : 0);
+             h->jit_st_init ? 1 : 0, h->st_init.parts, h->st_init.rows);
   }
   if (h->tsell) {
   } else if (h->bsr)

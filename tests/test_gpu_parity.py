@@ -357,6 +357,16 @@ _VARIANTS = [
     ("generic Jacobi kernels", {"FASTILU_NO_JIT_JACOBI": "1"}, None),
     ("loads-first Jacobi kernels", {"FASTILU_JIT_JACOBI_MODE": "1"}, None),
     ("128-row tiles", {"FASTILU_TSELL_STAGED": "1", "FASTILU_TSELL_ST_THREADS": "256"}, None),
+    ("one part-warp per slice, 320-row tiles",
+     {"FASTILU_TSELL_STAGED": "1", "FASTILU_TSELL_ST_PARTS": "1", "FASTILU_TSELL_ST_THREADS": "320"},
+     None),
+    ("init-fused sweep 1 with the full sweep's block shape",
+     {"FASTILU_TSELL_INIT_PARTS": "2", "FASTILU_TSELL_INIT_THREADS": "512"}, None),
+    ("init-fused sweep 1 with 128-row tiles (more tiles than the full sweep)",
+     {"FASTILU_TSELL_INIT_PARTS": "1", "FASTILU_TSELL_INIT_THREADS": "128"}, None),
+    ("two part-warps per slice, 256-row tiles",
+     {"FASTILU_TSELL_STAGED": "1", "FASTILU_TSELL_ST_PARTS": "2", "FASTILU_TSELL_ST_THREADS": "512"},
+     None),
     ("wavefront trisolve", {"FASTILU_JIT_TRISOLVE": "1"}, None),
     ("paired Jacobi sweeps", {"FASTILU_JAC2": "1"}, None),
     ("paired Jacobi sweeps, L1 gathers + L2 hints", {"FASTILU_JAC2": "1",
