@@ -463,15 +463,21 @@ static fastilu_status setup_tsell(fastilu_handle h, const std::vector<unsigned l
         // its stage (A's columns only) is small: FASTILU_TSELL_STAGES_INIT more ring slots
         const char *ev_si = std::getenv("FASTILU_TSELL_STAGES_INIT");
         const int nsi = ev_si ? std::max(2, atoi(ev_si)) : nst;
-        // its own block shape: for 2-part templates (27-pt ILU(1)) one part-warp per slice and
-        // 320-row tiles (the A x A terms fit one thread; less box overhang): c4 sweep 1
-        // 3.46 -> 3.08 ms (profiles/r1j_*).  FASTILU_TSELL_INIT_PARTS / _THREADS override.
+        // its own block shape (its A x A terms need half the full sweep's accumulators): for
+        // 2-part templates (27-pt ILU(1)) one part-warp per slice and 384-row tiles (less box
+        // overhang): c4 sweep 1 3.46 -> 2.93 ms; for 4-part templates (ILU(2)) two part-warps
+        // and 256-row tiles: c3b 1.12 -> 0.84 ms (profiles/r1j_*, r1l_*).
+        // FASTILU_TSELL_INIT_PARTS / _THREADS override.
         const char *ev_ip = std::getenv("FASTILU_TSELL_INIT_PARTS");
         const char *ev_it = std::getenv("FASTILU_TSELL_INIT_THREADS");
-        const int iparts = ev_ip ? std::max(1, atoi(ev_ip)) : (sparts == 2 ? 1 : sparts);
+        const int iparts = ev_ip ? std::max(1, atoi(ev_ip))
+                                 : (sparts == 2 ? 1 : sparts >= 4 ? 2 : sparts);
         const int ithreads =
             ev_it ? std::max(32 * iparts, atoi(ev_it) / (32 * iparts) * 32 * iparts)
-                  : (sparts == 2 && !ev_ip ? 320 : sthreads);
+            : ev_ip ? sthreads
+            : sparts == 2 ? 384
+            : sparts >= 4 ? 512
+                          : sthreads;
         const std::string s2 = sweep_source_staged(T, ithreads, iparts, nsi, sminb, true, &ci,
                                                    sopts | kStagedFromAhat);
         int ibps = 0;

@@ -357,7 +357,7 @@ _VARIANTS = [
     ("generic Jacobi kernels", {"FASTILU_NO_JIT_JACOBI": "1"}, None),
     ("loads-first Jacobi kernels", {"FASTILU_JIT_JACOBI_MODE": "1"}, None),
     ("128-row tiles", {"FASTILU_TSELL_STAGED": "1", "FASTILU_TSELL_ST_THREADS": "256"}, None),
-    ("one part-warp per slice, 320-row tiles",
+    ("one part-warp per slice, 320-row tiles (full sweep)",
      {"FASTILU_TSELL_STAGED": "1", "FASTILU_TSELL_ST_PARTS": "1", "FASTILU_TSELL_ST_THREADS": "320"},
      None),
     ("init-fused sweep 1 with the full sweep's block shape",
