@@ -100,3 +100,19 @@ def test_bench_block_flop_count_matches_survey():
     r = bench.bsr_roofline(info, 98304, 1.0)
     assert r["terms_per_sweep"] == 3537519556
     assert r["bound"] == "alu" and r["unit"] == "TFLOP/s"
+
+
+def test_bench_smem_port_bytes():
+    """bench.py's shared-memory-port figure of the staged sweep: one 8-byte
+    LDS per term and row plus the TMA box writes, counted from the kernel configuration the
+    library reports (c4: 587 terms, 65,536 tiles of 256 rows, 7 boxes of 32 x 32 x 10 doubles)."""
+    import bench
+    info = ("path=tsell W=63 c0=31 WA=27 terms=587 staged=1 st_threads=512 st_parts=2 "
+            "st_rows=256 st_shift=0 st_groups=7 st_box=32x32x10 st_stages=2")
+    n = 256 ** 3
+    r = bench.smem_port(info, n, 1.0, 1000.0, 100)
+    assert r["lds_bytes"] == n * 587 * 8
+    assert r["tma_bytes"] == (n // 256) * 7 * 32 * 32 * 10 * 8
+    assert abs(r["peak"] - 128 * 100 * 1000e6 / 1e9) < 1e-9
+    assert abs(r["achieved"] - (r["lds_bytes"] + r["tma_bytes"]) / 1e-3 / 1e9) < 1e-6
+    assert bench.smem_port("path=tsell W=7 terms=3", n, 1.0, 1000.0) is None
