@@ -6,7 +6,9 @@ parity of the CUDA path.  Only tests/, __graft_entry__.smoke() and bench.py's
 cpu_baseline / `--impl reference` legs may import this package; the product
 package (paper_2506_05793_b200) never does, and this package never imports
 the product.  Arithmetic lives in fastilu_oracle.c (compiled -O2
--ffp-contract=off, single thread); this file only marshals arrays.
+-ffp-contract=off; single thread by default, `set_threads(T)` runs its per-row
+loops with OpenMP, bitwise equal to one thread); this file only marshals arrays
+(and, for the warm-up, places level L-1's values into S_L).
 
 Pins (tests/test_oracle_*.py, `-m "not gpu"`):
   * symbolic ILU(k): the ten nnz/n values printed in tab:fastilu_nx16/32
@@ -15,7 +17,14 @@ Pins (tests/test_oracle_*.py, `-m "not gpu"`):
   * exact ILU: tridiagonal ILU(0) == Thomas LU bitwise; dense KIJ elimination
     with dropping == IKJ bitwise; k >= n => LAPACK getrf within 1e-14.
   * sweeps: reach the exact ILU bitwise within the dependency-DAG depth;
-    residual non-increasing above the roundoff floor; diagonal A immediate.
+    residual non-increasing above the roundoff floor; diagonal A immediate;
+    the residual's exact sum == math.fsum bitwise.
+  * damped sweeps / Jacobi (omega < 1, reading R1 of PAPER.md:546-548): hand-derived
+    iterates of a 3x3 tridiagonal example (tests/golden/damped_3x3.json), a 2x2
+    closed form, omega = 0 is the identity, the update is affine in omega.
+  * warm-up (R10, PAPER.md:721): an independent dense embedding of S_{L-1} into S_L;
+    a pattern with no fill (S_0 = S_1) makes FastILU(0) then FastILU(1) equal to
+    one FastILU(0) run of twice the sweeps.
   * trisolve: == substitution after nlevels sweeps (bitwise), T = I, 1 sweep
     = D^-1 b; substitution == scipy solve_triangular.
   * gmres (NEXT row f1): A = I converges in one iteration; an exact LU preconditioner in at
@@ -53,7 +62,7 @@ def build(force: bool = False) -> str:
         os.makedirs(os.path.dirname(_LIB), exist_ok=True)
         tmp = _LIB + f".tmp{os.getpid()}"
         subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c11",
-                               "-fPIC", "-shared", "-o", tmp, _SRC, "-lm"])
+                               "-fopenmp", "-fPIC", "-shared", "-o", tmp, _SRC, "-lm"])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -73,6 +82,10 @@ def lib():
         L.orc_symbolic.argtypes = [C.c_int64, I64P, I32P, C.c_int, C.POINTER(I64P),
                                    C.POINTER(I32P), C.POINTER(I32P), I64P]
         L.orc_free.argtypes = [C.c_void_p]
+        L.orc_set_threads.argtypes = [C.c_int]
+        L.orc_set_threads.restype = C.c_int
+        L.orc_fsum.argtypes = [C.c_int64, F64P]
+        L.orc_fsum.restype = C.c_double
         L.orc_scale_init.argtypes = [C.c_int64, I64P, I32P, F64P, I64P, I32P, C.c_double, F64P,
                                      F64P, F64P, I64P]
         L.orc_bad_diagonal.argtypes = [C.c_int64, I64P, I32P, F64P]
@@ -119,6 +132,18 @@ class Pattern:
     @property
     def nnz(self):
         return int(self.row_ptr[-1])
+
+
+def set_threads(t: int) -> int:
+    """OpenMP threads for the oracle's per-row loops (1 = sequential, the default).  Results are
+    bitwise independent of t (per-entry arithmetic is sequential; the residual sum is exact)."""
+    return int(lib().orc_set_threads(int(t)))
+
+
+def fsum(x) -> float:
+    """Exactly rounded sum (the oracle's residual accumulator; pinned against math.fsum)."""
+    x = _f64(x)
+    return float(lib().orc_fsum(x.shape[0], _p(x, F64P)))
 
 
 def validate(row_ptr, col_idx):

@@ -8,8 +8,17 @@
  * library under paper_2506_05793_b200/) shares no code with this file.
  *
  * Arithmetic: IEEE binary64, compiled with -O2 -ffp-contract=off so that no
- * multiply-subtract is fused; every sum is accumulated left to right in the
- * order stated next to it.  Single threaded.
+ * multiply-subtract is fused; every per-entry sum is accumulated left to right
+ * in the order stated next to it.  The residual r(s-1) (a sum of nnz(S)
+ * squares) is summed EXACTLY and rounded once (orc_fsum_*, Shewchuk's
+ * partials, the algorithm of Python's math.fsum), so its value does not
+ * depend on any summation order.
+ *
+ * Threads: orc_set_threads(T) runs the per-row loops (scale/init, sweep,
+ * Jacobi sweeps) with OpenMP over rows.  Every row/entry is computed by one
+ * thread with the sequential arithmetic above and the exact residual sum is
+ * order independent, so T threads give results bitwise equal to 1 thread
+ * (tests/test_oracle_numeric.py::test_threads_bitwise).  Default: 1 thread.
  *
  * Readings of the paper (listed in DESIGN.md, "Readings"):
  *   R1 (Fig. algo:fastILU_comp line 3): the printed l-update
@@ -39,6 +48,9 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 
 /* status codes mirror include/fastilu.h by VALUE only (no shared header) */
 enum {
@@ -52,6 +64,73 @@ enum {
 };
 
 void orc_free(void *p) { free(p); }
+
+static int g_threads = 1;
+/* number of OpenMP threads for the per-row loops (1 = sequential); returns the value in use */
+int orc_set_threads(int t) {
+#ifdef _OPENMP
+  g_threads = t > 0 ? t : 1;
+#else
+  (void)t;
+  g_threads = 1;
+#endif
+  return g_threads;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Exactly rounded summation (Shewchuk, "Adaptive precision floating-point   */
+/* arithmetic", 1997; the algorithm of Python's math.fsum).  The running sum */
+/* is held as a list of non-overlapping partials whose exact sum is the exact */
+/* sum of every term added so far (each two-sum below is error free).         */
+/* Finite terms only (squares of finite defects here).                        */
+/* ------------------------------------------------------------------------ */
+typedef struct { double p[80]; int n; } orc_fsum_t;
+
+static void orc_fsum_add(orc_fsum_t *s, double x) {
+  int i = 0;
+  for (int j = 0; j < s->n; j++) {
+    double y = s->p[j];
+    if (fabs(x) < fabs(y)) { double t = x; x = y; y = t; }
+    double hi = x + y;           /* two-sum with |x| >= |y|: hi + lo == x + y exactly */
+    double lo = y - (hi - x);
+    if (lo != 0.0) s->p[i++] = lo;
+    x = hi;
+  }
+  s->p[i++] = x;
+  s->n = i;
+}
+
+/* the exact sum rounded to nearest (ties to even), from the partials */
+static double orc_fsum_result(const orc_fsum_t *s) {
+  int n = s->n;
+  if (n == 0) return 0.0;
+  double hi = s->p[--n], lo = 0.0;
+  while (n > 0) {               /* add partials from the largest down until inexact */
+    double x = hi, y = s->p[--n];
+    hi = x + y;
+    double yr = hi - x;
+    lo = y - yr;
+    if (lo != 0.0) break;
+  }
+  /* half-way case: the remaining partials decide the rounding direction */
+  if (n > 0 && ((lo < 0.0 && s->p[n - 1] < 0.0) || (lo > 0.0 && s->p[n - 1] > 0.0))) {
+    double y = lo * 2.0, x = hi + y;
+    if (y == x - hi) hi = x;
+  }
+  return hi;
+}
+
+/* exposed for its pin (tests: == math.fsum bitwise on adversarial inputs) */
+double orc_fsum(int64_t n, const double *x) {
+  orc_fsum_t s;
+  s.n = 0;
+  for (int64_t i = 0; i < n; i++) orc_fsum_add(&s, x[i]);
+  return orc_fsum_result(&s);
+}
+
+static void orc_fsum_merge(orc_fsum_t *into, const orc_fsum_t *from) {
+  for (int j = 0; j < from->n; j++) orc_fsum_add(into, from->p[j]);
+}
 
 /* ------------------------------------------------------------------------ */
 /* Validation (SPEC.md:26-31 CSR invariants; SPEC.md:357-359 structural      */
@@ -210,15 +289,19 @@ int orc_scale_init(int64_t n, const int64_t *rp, const int32_t *ci,
     s[i] = 1.0 / sqrt(fabs(aii));
   }
   for (int64_t p = 0; p < srp[n]; p++) ahat[p] = 0.0;
+  int missing = 0;
+#pragma omp parallel for schedule(static) num_threads(g_threads) reduction(| : missing)
   for (int64_t i = 0; i < n; i++) {
     for (int64_t q = rp[i]; q < rp[i + 1]; q++) {
       int32_t j = ci[q];
       int64_t p = find_in_row(srp, sci, i, j);
-      if (p < 0) return ORC_ERR_BAD_MATRIX; /* S must contain A */
+      if (p < 0) { missing = 1; continue; } /* S must contain A */
       double aij = (j == i) ? shifted(a[q], shift) : a[q];
       ahat[p] = (aij * s[i]) * s[j];
     }
   }
+  if (missing) return ORC_ERR_BAD_MATRIX;
+#pragma omp parallel for schedule(static) num_threads(g_threads)
   for (int64_t i = 0; i < n; i++) {
     for (int64_t p = srp[i]; p < srp[i + 1]; p++) {
       int32_t j = sci[p];
@@ -255,39 +338,48 @@ int64_t orc_bad_diagonal(int64_t n, const int64_t *srp, const int32_t *sci,
 /* all right-hand values from `old` (iterate s-1).  *resid receives           */
 /*   r(s-1) = sqrt( sum_L (acc - l_ij u_jj)^2 + sum_U (acc - u_ij)^2 )        */
 /*         = ||(Ahat - L U)|_S||_F at iterate s-1,          */
-/* summed in row-major S order.                                               */
+/* each square a rounded product, their sum exact and rounded once (fsum).    */
 /* ------------------------------------------------------------------------ */
 void orc_sweep(int64_t n, const int64_t *srp, const int32_t *sci,
                const double *ahat, const double *old, double *out,
                double omega, double *resid) {
-  double r2 = 0.0;
-  for (int64_t i = 0; i < n; i++) {
-    for (int64_t p = srp[i]; p < srp[i + 1]; p++) {
-      int32_t j = sci[p];
-      int64_t m = (j < i) ? j : i; /* min(i,j) */
-      double acc = ahat[p];
-      for (int64_t q = srp[i]; q < srp[i + 1] && sci[q] < m; q++) {
-        int32_t k = sci[q];
-        int64_t pkj = find_in_row(srp, sci, k, j);
-        if (pkj < 0) continue;
-        double prod = old[q] * old[pkj];
-        acc = acc - prod;
-      }
-      if (j < i) {
-        int64_t pjj = find_in_row(srp, sci, j, j);
-        double ujj = old[pjj];
-        double e = acc - old[p] * ujj;
-        r2 = r2 + e * e;
-        double l = acc / ujj;
-        out[p] = (omega == 1.0) ? l : (1.0 - omega) * old[p] + omega * l;
-      } else {
-        double e = acc - old[p];
-        r2 = r2 + e * e;
-        out[p] = (omega == 1.0) ? acc : (1.0 - omega) * old[p] + omega * acc;
+  orc_fsum_t total;
+  total.n = 0;
+#pragma omp parallel num_threads(g_threads)
+  {
+    orc_fsum_t r2; /* this thread's exact partial sum of squares */
+    r2.n = 0;
+#pragma omp for schedule(static)
+    for (int64_t i = 0; i < n; i++) {
+      for (int64_t p = srp[i]; p < srp[i + 1]; p++) {
+        int32_t j = sci[p];
+        int64_t m = (j < i) ? j : i; /* min(i,j) */
+        double acc = ahat[p];
+        for (int64_t q = srp[i]; q < srp[i + 1] && sci[q] < m; q++) {
+          int32_t k = sci[q];
+          int64_t pkj = find_in_row(srp, sci, k, j);
+          if (pkj < 0) continue;
+          double prod = old[q] * old[pkj];
+          acc = acc - prod;
+        }
+        if (j < i) {
+          int64_t pjj = find_in_row(srp, sci, j, j);
+          double ujj = old[pjj];
+          double e = acc - old[p] * ujj;
+          orc_fsum_add(&r2, e * e);
+          double l = acc / ujj;
+          out[p] = (omega == 1.0) ? l : (1.0 - omega) * old[p] + omega * l;
+        } else {
+          double e = acc - old[p];
+          orc_fsum_add(&r2, e * e);
+          out[p] = (omega == 1.0) ? acc : (1.0 - omega) * old[p] + omega * acc;
+        }
       }
     }
+#pragma omp critical
+    orc_fsum_merge(&total, &r2);
   }
-  *resid = sqrt(r2);
+  *resid = sqrt(orc_fsum_result(&total));
 }
 
 /* ------------------------------------------------------------------------ */
@@ -356,6 +448,7 @@ void orc_jacobi_lower(int64_t n, const int64_t *srp, const int32_t *sci,
   for (int64_t i = 0; i < n; i++) z[i] = 0.0;
   for (int t = 1; t <= ntri; t++) {
     memcpy(zo, z, sizeof(double) * (size_t)n);
+#pragma omp parallel for schedule(static) num_threads(g_threads)
     for (int64_t i = 0; i < n; i++) {
       double acc = y[i];
       for (int64_t p = srp[i]; p < srp[i + 1] && sci[p] < i; p++) {
@@ -375,6 +468,7 @@ void orc_jacobi_upper(int64_t n, const int64_t *srp, const int32_t *sci,
   for (int64_t i = 0; i < n; i++) w[i] = 0.0;
   for (int t = 1; t <= ntri; t++) {
     memcpy(wo, w, sizeof(double) * (size_t)n);
+#pragma omp parallel for schedule(static) num_threads(g_threads)
     for (int64_t i = 0; i < n; i++) {
       double acc = z[i];
       double d = 0.0;

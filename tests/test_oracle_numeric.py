@@ -391,3 +391,198 @@ def test_warmup_trend_gmres():
         i1 = oracle.gmres(a, b, oracle.fastilu_preconditioner(oracle.compute_warmup(a, k, 2),
                                                                 30))[1]
         assert i1 <= i0, (k, i0, i1)
+
+
+# ----------------------------------------------------------------------------- exact residual sum
+def test_fsum_is_exactly_rounded():
+    """The residual accumulator (Shewchuk partials) == math.fsum bitwise, on inputs where a
+    left-to-right sum loses everything (cancellation, tiny terms under huge ones, ties)."""
+    import math
+    rng = np.random.default_rng(5)
+    cases = [
+        np.array([1e16, 1.0, -1e16, 1.0]),
+        np.array([1.0, 1e-16, 1e-16, 1e-16, 1e-16]),
+        np.array([2.0 ** 53, 1.0, 1.0, -2.0 ** 53]),
+        np.array([1.0, 2.0 ** -53, 2.0 ** -106]),             # half-way case decided by the tail
+        np.array([1.0, 2.0 ** -53, -2.0 ** -106]),
+        rng.standard_normal(10000) * 10.0 ** rng.integers(-20, 20, 10000),
+        rng.random(100000) ** 2,
+        np.zeros(0),
+    ]
+    for x in cases:
+        got = oracle.fsum(x)
+        assert got == math.fsum(x), (got, math.fsum(x))
+    y = rng.random(1000)
+    assert sum(y.tolist()) != math.fsum(y) or True  # (documentation: naive sums may differ)
+
+
+def test_residual_sum_is_exact_fsum_of_squares():
+    """r(s-1)^2 of the oracle == math.fsum of the per-entry squared defects, which the test
+    obtains from dense algebra at iterate s-1 on an input where every defect is exact:
+    A with entries in {1, -1/2} and k = 0 on a 1D chain (all products are exact dyadics)."""
+    import math
+    n = 12
+    A = np.eye(n) + np.diag([-0.5] * (n - 1), 1) + np.diag([-0.5] * (n - 1), -1)
+    a = P.Csr(*_dense_to_csr(A))
+    pat = oracle.symbolic(a.row_ptr, a.col_idx, 0)
+    s, ahat, vals = oracle.scale_init(a, pat)
+    L, U = dense_LU(pat, vals)
+    D = to_S(pat, A - L @ U)          # iterate 0 has only dyadic values: L @ U is exact
+    _, r = oracle.sweep(pat, ahat, vals)
+    assert r * r == pytest.approx(math.fsum(D * D), rel=2 * np.finfo(float).eps)
+    assert r == math.sqrt(math.fsum(D * D))
+
+
+def _dense_to_csr(A):
+    rp, ci, v = [0], [], []
+    for i in range(A.shape[0]):
+        for j in range(A.shape[1]):
+            if A[i, j] != 0.0:
+                ci.append(j)
+                v.append(A[i, j])
+        rp.append(len(ci))
+    return rp, ci, v
+
+
+# ----------------------------------------------------------------------------- damping (R1, R6)
+def _golden(name):
+    import json
+    import os
+    return json.load(open(os.path.join(os.path.dirname(__file__), "golden", name)))
+
+
+def _frac(x):
+    from fractions import Fraction
+    return float(Fraction(x))
+
+
+def test_damped_sweeps_hand_derived():
+    """omega = 0.7 iterates s = 1..3 and r(0..2) of the 3x3 tridiagonal example derived by hand
+    in tests/golden/README.md from Fig. algo:fastILU_comp + readings R1-R4.
+    The swapped-weight mutant (w old + (1-w) new) already fails at sweep 1 (u22 = 37/40)."""
+    gd = _golden("damped_3x3.json")
+    a = P.Csr(*_dense_to_csr(np.array(gd["matrix"]["dense"])))
+    w = _frac(gd["omega"])
+    for s, want in gd["sweeps"].items():
+        f = oracle.compute(a, 0, int(s), omega=w)
+        assert f.pattern.nnz == 7 and np.array_equal(f.s, np.ones(3))
+        np.testing.assert_allclose(f.vals, [_frac(v) for v in want], rtol=4 * np.finfo(float).eps,
+                                   atol=0)
+    f = oracle.compute(a, 0, 3, omega=w)
+    want_r2 = [_frac(v) for v in gd["resid_squared"].values()]
+    np.testing.assert_allclose(f.resid ** 2, want_r2, rtol=1e-14)
+
+
+def test_damped_jacobi_hand_derived():
+    """omega_tri = 0.8 Jacobi iterates t = 1..3 for L and U (reading R6),
+    derived by hand in tests/golden/README.md."""
+    gd = _golden("damped_3x3.json")["jacobi"]
+    wt = _frac(gd["omega_tri"])
+    rp = np.array([0, 2, 5, 7], dtype=np.int64)
+    ci = np.array([0, 1, 0, 1, 2, 1, 2], dtype=np.int32)
+    pat = oracle.Pattern(rp, ci, np.zeros(7, dtype=np.int32))
+    lo = gd["lower"]["strict_L"]
+    up = gd["upper"]["U"]
+    vals_L = np.array([1.0, 0.0, _frac(lo["l21"]), 1.0, 0.0, _frac(lo["l32"]), 1.0])
+    vals_U = np.array([_frac(up["u11"]), _frac(up["u12"]), 0.0, _frac(up["u22"]), _frac(up["u23"]),
+                       0.0, _frac(up["u33"])])
+    y = np.array([_frac(v) for v in gd["lower"]["y"]])
+    z = np.array([_frac(v) for v in gd["upper"]["z"]])
+    for t, want in gd["lower"]["z"].items():
+        np.testing.assert_allclose(oracle.jacobi_lower(pat, vals_L, y, int(t), omega=wt),
+                                   [_frac(v) for v in want], rtol=4 * np.finfo(float).eps, atol=0)
+    for t, want in gd["upper"]["w"].items():
+        np.testing.assert_allclose(oracle.jacobi_upper(pat, vals_U, z, int(t), omega=wt),
+                                   [_frac(v) for v in want], rtol=4 * np.finfo(float).eps, atol=0)
+
+
+@pytest.mark.parametrize("w", [0.3, 0.7, 1.0])
+def test_damped_2x2_closed_form(w):
+    """2x2, unit diagonal, k = 0: l21 stays c and u22(s) - (1 - cb) = (1 - w)(u22(s-1) - (1 - cb))
+    (R1-R3), so u22(s) = 1 - cb (1 - (1 - w)^s): geometric convergence at rate 1 - w."""
+    b, c = -0.4, -0.6
+    a = P.Csr([0, 2, 4], [0, 1, 0, 1], [1.0, b, c, 1.0])
+    for s in range(1, 7):
+        f = oracle.compute(a, 0, s, omega=w)
+        assert f.vals[2] == pytest.approx(c, rel=1e-15)
+        assert f.vals[3] == pytest.approx(1 - c * b * (1 - (1 - w) ** s), rel=1e-15)
+
+
+def test_omega_zero_is_the_identity_and_update_is_affine():
+    """omega = 0 leaves every iterate unchanged (sweep and Jacobi); for any omega the damped
+    update satisfies out(w) - old = w (out(1) - old) up to rounding: the weight w multiplies
+    the new value, 1 - w the old one (R1), not the other way round."""
+    a = P.laplace3d_27pt(4)
+    pat = oracle.symbolic(a.row_ptr, a.col_idx, 1)
+    s, ahat, vals = oracle.scale_init(a, pat)
+    vals, _ = oracle.sweep(pat, ahat, vals)          # a generic iterate (fill no longer 0)
+    same, _ = oracle.sweep(pat, ahat, vals, omega=0.0)
+    assert np.array_equal(same, vals)
+    full, _ = oracle.sweep(pat, ahat, vals, omega=1.0)
+    for w in (0.25, 0.7):
+        got, _ = oracle.sweep(pat, ahat, vals, omega=w)
+        np.testing.assert_allclose(got - vals, w * (full - vals), rtol=1e-12, atol=1e-15)
+    y = P.rhs_positive(a.n)
+    assert np.array_equal(oracle.jacobi_lower(pat, full, y, 3, omega=0.0), np.zeros(a.n))
+    z1 = oracle.jacobi_lower(pat, full, y, 1, omega=1.0)
+    np.testing.assert_allclose(oracle.jacobi_lower(pat, full, y, 1, omega=0.6), 0.6 * z1,
+                               rtol=1e-15)
+
+
+# ----------------------------------------------------------------------------- warm-up embedding (R10)
+def test_warmup_embedding_dense():
+    """compute_warmup(k=2, 1 sweep per level) == level 0 sweep, then the level-0 factors placed
+    into S_1 through a dense n x n matrix (fill = +0.0), one S_1 sweep, the same into S_2, one
+    S_2 sweep (reading R10).  The embedding here is independent of the oracle's
+    (a dense matrix, indexed by (row, column))."""
+    a = P.laplace3d_27pt(4)
+    n = a.n
+    vals, r_hist, pat = None, [], None
+    for L in range(3):
+        pat = oracle.symbolic(a.row_ptr, a.col_idx, L)
+        s, ahat, v0 = oracle.scale_init(a, pat)
+        if vals is None:
+            v = v0
+        else:
+            D = np.zeros((n, n))
+            for i in range(n):
+                for p in range(prev.row_ptr[i], prev.row_ptr[i + 1]):
+                    D[i, prev.col_idx[p]] = vals[p]
+            v = to_S(pat, D)
+        vals, r = oracle.sweep(pat, ahat, v)
+        r_hist.append(r)
+        prev = pat
+    f = oracle.compute_warmup(a, 2, 1)
+    assert np.array_equal(f.pattern.col_idx, pat.col_idx)
+    assert np.array_equal(f.vals, vals)
+    assert np.array_equal(f.resid, np.array(r_hist))
+
+
+def test_warmup_without_fill_is_one_longer_run():
+    """A pattern with no fill at any level (tridiagonal, S_0 = S_1 = S_2) makes the warm-up's
+    embedding the identity: FastILU(0), FastILU(1), FastILU(2) with ns sweeps each == one
+    FastILU(0) run with 3 ns sweeps, bitwise (factors and residual history)."""
+    a = P.tridiagonal(30)
+    ns = 2
+    f = oracle.compute_warmup(a, 2, ns)
+    g = oracle.compute(a, 0, 3 * ns)
+    assert np.array_equal(f.vals, g.vals)
+    assert np.array_equal(f.resid, g.resid)
+
+
+# ----------------------------------------------------------------------------- OpenMP mode
+def test_threads_bitwise():
+    """The OpenMP-over-rows mode is bitwise the single-thread oracle (factors, residuals, x)."""
+    a = P.laplace3d_27pt(9, gz=7)
+    b = P.rhs_positive(a.n)
+    try:
+        oracle.set_threads(1)
+        f1 = oracle.compute(a, 1, 3)
+        x1 = oracle.apply(f1, b, 5, omega_tri=0.9)
+        assert oracle.set_threads(4) in (1, 4)
+        f4 = oracle.compute(a, 1, 3)
+        x4 = oracle.apply(f4, b, 5, omega_tri=0.9)
+    finally:
+        oracle.set_threads(1)
+    assert np.array_equal(f1.vals, f4.vals) and np.array_equal(f1.resid, f4.resid)
+    assert np.array_equal(x1, x4)
