@@ -94,6 +94,58 @@ def byte_model(n, nnz_A, nnz_S, nnz_Ls, ns, nt):
     return dict(B_f=B_f, B_L=B_L, B_U=B_U, B_init=B_init, B_apply=B_apply)
 
 
+def layout_model(info, n, nnz_A, nnz_S, nnz_Ls, ns, nt):
+    """Bytes the kernels of this handle's layout must move at least once:
+    the template-SELL layout stores W value slots per row (padded to 32-row slices), Ahat on A's
+    WA template columns and a presence mask, and NO column indices -- so it moves less than the
+    SURVEY Sec. 8(d) CSR model, which charges 4 index bytes per entry.  Per launch:
+      full sweep   read + write the W slots, read Ahat (WA) + mask, write u_ii
+      sweep 1      (init fused) read Ahat + mask, write the W slots + u_ii
+      init         scale: a_ii in, s + ahat_ii out; Ahat: A's WA slots + mask in, WA slots out
+      Jacobi L     the c0 strict-lower slots + mask, rhs, x_old (compulsory), x_new out
+      Jacobi U     the W-c0-1 strict-upper slots + mask, rhs, x_old, u_ii, x_new out
+      first L / U  b, s in, y, z out / z, u_ii in, w out
+    Non-template paths (CSR, block): the SURVEY model (they do move index bytes)."""
+    import re
+    kv = dict(re.findall(r"(\w+)=(\S+)", info))
+    if not info.startswith("path=tsell"):
+        bm = byte_model(n, nnz_A, nnz_S, nnz_Ls, ns, nt)
+        return dict(kind="survey (CSR / block path)", B_f=bm["B_f"], B_f1=bm["B_f"],
+                    B_init=bm["B_init"], B_L=bm["B_L"], B_U=bm["B_U"], B_apply=bm["B_apply"])
+    W, c0, WA = int(kv["W"]), int(kv["c0"]), int(kv["WA"])
+    words = (W + 63) // 64
+    npad = -(-n // 32) * 32
+    B_f = npad * 8 * (2 * W + WA + words) + 8 * n
+    B_init = 24 * n + npad * 8 * (2 * WA + words) + 8 * n
+    if kv.get("st_init") == "1":  # sweep 1 derives iterate 0 from Ahat: it reads no W slots
+        B_f1 = npad * 8 * (W + WA + words) + 8 * n
+    else:  # the init stores iterate 0 (W slots + u_ii) and sweep 1 is a full sweep
+        B_f1 = B_f
+        B_init += npad * 8 * W + 8 * n
+    B_L = npad * 8 * (c0 + words) + 24 * n
+    B_U = npad * 8 * (W - c0 - 1 + words) + 32 * n
+    B_apply = 32 * n + (nt - 1) * B_L + 32 * n + (nt - 1) * B_U
+    return dict(kind="template-SELL layout (no index bytes)", B_f=B_f, B_f1=B_f1, B_init=B_init,
+                B_L=B_L, B_U=B_U, B_apply=B_apply)
+
+
+def cpu_info():
+    """Host cores the oracle may use and the CPU model (lscpu / /proc/cpuinfo)."""
+    try:
+        cores = len(os.sched_getaffinity(0))
+    except AttributeError:
+        cores = os.cpu_count() or 1
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return cores, model
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -179,32 +231,49 @@ def build_matrix(kind, g):
     return a, time.perf_counter() - t
 
 
-def cpu_sample(kind, g, k, ns, nt, planes):
-    """Oracle on a bounded sample of the workload: a g x g x planes slab of the same stencil."""
+def cpu_sample(kind, g, k, ns, nt, planes, threads=1):
+    """Oracle on a bounded sample of the workload: a g x g x planes slab of the same stencil,
+    its per-row loops on `threads` OpenMP threads (bitwise the 1-thread oracle)."""
     import oracle
     sub = P.make(kind, g, gz=planes)
     pat = oracle.symbolic(sub.row_ptr, sub.col_idx, k)
     b = P.rhs_positive(sub.n)
-    t0 = time.perf_counter()
-    f = oracle.compute(sub, k, ns, pat=pat)
-    oracle.apply(f, b, nt)
-    dt = time.perf_counter() - t0
-    return dict(value=pat.nnz * ns / dt, seconds=dt, nnz_S=pat.nnz, n=sub.n,
-                sample=f"{kind} {g}x{g}x{planes} slab, ILU({k}), {ns} sweeps + {nt}/{nt} "
-                       f"trisweeps, scale/init+sweeps+apply timed (symbolic excluded)")
+    used = oracle.set_threads(threads)
+    try:
+        t0 = time.perf_counter()
+        f = oracle.compute(sub, k, ns, pat=pat)
+        oracle.apply(f, b, nt)
+        dt = time.perf_counter() - t0
+    finally:
+        oracle.set_threads(1)
+    return dict(value=pat.nnz * ns / dt, seconds=dt, nnz_S=pat.nnz, n=sub.n, threads=used,
+                sample=f"{kind} {g}x{g}x{planes} slab of the workload, ILU({k}), {ns} sweeps + "
+                       f"{nt}/{nt} trisweeps, scale/init+sweeps+apply timed (symbolic excluded), "
+                       f"{used} OpenMP threads")
+
+
+def cpu_planes_for(kind, g, k, ns, nt, threads, target_s=8.0, cap=64):
+    """Slab thickness giving ~target_s seconds of oracle time on `threads` cores (probe with a
+    2-plane slab); capped so the sample's host memory stays bounded."""
+    probe = cpu_sample(kind, g, k, ns, nt, 2, threads)
+    per_plane = probe["seconds"] / 2
+    return int(max(2, min(cap, g, target_s / max(per_plane, 1e-6))))
 
 
 def run_reference(args, wl):
+    """The reference arm of this tier: the oracle as it stands, on all host cores, on a bounded
+    slab of the workload (rank 0 only; other ranks exit without work)."""
     kind, g, k, ns, nt = wl
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    planes = args.cpu_planes or default_cpu_planes(kind, g, k)
+    cores, model = cpu_info()
+    planes = args.cpu_planes or cpu_planes_for(kind, g, k, ns, nt, cores, target_s=4.0)
     for _ in range(args.warmup):
-        cpu_sample(kind, g, k, ns, nt, planes)
+        cpu_sample(kind, g, k, ns, nt, planes, cores)
     vals, secs = [], []
     for _ in range(args.steps):
-        r = cpu_sample(kind, g, k, ns, nt, planes)
+        r = cpu_sample(kind, g, k, ns, nt, planes, cores)
         vals.append(r["value"])
         secs.append(r["seconds"])
     v = float(np.median(vals))
@@ -213,16 +282,10 @@ def run_reference(args, wl):
             "ms_per_step": 1e3 * float(np.median(secs)), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": args.workload, "sample_planes": planes},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": r["sample"]},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": r["threads"], "cpu": model,
+                             "kind": "oracle", "sample": r["sample"]},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
-
-
-def default_cpu_planes(kind, g, k):
-    # ~10-20 s of single-thread oracle work per sample
-    per_plane = {"7pt": 7, "aniso7pt": 7, "27pt": {0: 27, 1: 63, 2: 115}.get(k, 200)}[kind] * g * g
-    return int(max(2, min(g, 4_000_000 // max(per_plane, 1))))
 
 
 def run_ours(args, wl):
@@ -333,7 +396,9 @@ def run_ours(args, wl):
     # initial guess fused in, A x A terms only), reported separately
     rest_ms = float(np.mean(t_rest)) if ns >= 2 else 0.0
     per_launch_ms = rest_ms / (ns - 1) if ns >= 2 and rest_ms > 0 else sweep_ms / max(ns, 1)
-    achieved = bm["B_f"] / (per_launch_ms * 1e-3) / 1e9
+    info = f.info()
+    lm = layout_model(info, n, nnz_A, nnz_S, nnz_Ls, ns, nt)
+    achieved = lm["B_f"] / (per_launch_ms * 1e-3) / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
@@ -366,21 +431,34 @@ def run_ours(args, wl):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and kind != "3dof":
-        planes = args.cpu_planes or default_cpu_planes(kind, g, k)
-        r = cpu_sample(kind, g, k, ns, nt, planes)
-        cpu = {"value": r["value"], "unit": UNIT, "cores": 1, "kind": "oracle",
-               "sample": r["sample"]}
+        cores, model = cpu_info()
+        planes = args.cpu_planes or cpu_planes_for(kind, g, k, ns, nt, cores)
+        r = cpu_sample(kind, g, k, ns, nt, planes, cores)
+        cpu = {"value": r["value"], "unit": UNIT, "cores": r["threads"], "cpu": model,
+               "kind": "oracle", "sample": r["sample"], "seconds": r["seconds"]}
 
-    info = f.info()
     launches_per_step = 2 + 2 * ns + 2 * nt + (3 if info.startswith("path=bsr") else 0)
-    roof = {"bound": "hbm", "kernel": "sweep_kernel", "achieved": achieved, "peak": peak,
+    # the full sweep kernel (sweeps 2..ns) against the measured copy bandwidth, on the bytes its
+    # layout moves (no index bytes on the template path); the SURVEY 8(d) CSR model alongside
+    roof = {"bound": "hbm", "kernel": "fastilu_tsell_sweep_st" if "staged=1" in info
+            else "sweep_kernel", "achieved": achieved, "peak": peak,
             "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
-            "algorithmic_bytes_per_launch": bm["B_f"]}
+            "bytes_per_launch": lm["B_f"], "byte_model": lm["kind"],
+            "survey_model": {"bytes_per_launch": bm["B_f"],
+                             "achieved": bm["B_f"] / (per_launch_ms * 1e-3) / 1e9,
+                             "frac": bm["B_f"] / (per_launch_ms * 1e-3) / 1e9 / peak,
+                             "note": "SURVEY 8(d): 4 index bytes per entry the layout never "
+                                     "loads; not a bandwidth"}}
+    if traffic:
+        roof["traffic_achieved"] = traffic / (per_launch_ms * 1e-3) / 1e9
+        roof["traffic_frac"] = roof["traffic_achieved"] / peak
     if info.startswith("path=bsr"):
         roof = bsr_roofline(info, n, sweep_ms / max(ns, 1))
     else:  # the secondary bound of the staged sweep (its shared-memory port)
         roof["smem_port"] = smem_port(info, n, per_launch_ms, clk.get("sm_mhz"),
                                       torch.cuda.get_device_properties(dev).multi_processor_count)
+    composite = lm["B_init"] + (lm["B_f1"] + (ns - 1) * lm["B_f"] if ns >= 1 else 0) + \
+        lm["B_apply"]
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -396,8 +474,15 @@ def run_ours(args, wl):
             "sweep_nnz_updates_per_s": nnz_S * ns / (sweep_ms * 1e-3),
             "sweep_ms": sweep_ms, "sweep1_ms": float(np.mean(t_first)),
             "sweep_launch_ms": per_launch_ms, "init_ms": float(np.mean(t_init)), "apply_ms": t_apply,
-            "trisolve_gbs": bm["B_apply"] / (t_apply * 1e-3) / 1e9 if t_apply > 0 else None,
-            "composite_gbs": (bm["B_init"] + ns * bm["B_f"] + bm["B_apply"]) / (ms * 1e-3) / 1e9,
+            # bandwidths on the bytes the layout moves (layout_model), fraction of the measured
+            # copy peak; the SURVEY model's figures (index bytes included) under "survey_model"
+            "trisolve_gbs": lm["B_apply"] / (t_apply * 1e-3) / 1e9 if t_apply > 0 else None,
+            "trisolve_frac": (lm["B_apply"] / (t_apply * 1e-3) / 1e9 / peak
+                              if t_apply > 0 else None),
+            "composite_gbs": composite / (ms * 1e-3) / 1e9,
+            "composite_frac": composite / (ms * 1e-3) / 1e9 / peak,
+            "bytes_per_step": {"layout": composite, "survey_model": (
+                bm["B_init"] + ns * bm["B_f"] + bm["B_apply"]), "byte_model": lm["kind"]},
             "roofline": roof,
             "clocks": clk, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
             "cpu_baseline": cpu,
@@ -429,6 +514,22 @@ def main():
     ns = args.nsweeps if args.nsweeps is not None else ns
     nt = args.ntri if args.ntri is not None else nt
     wl = (kind, g, k, ns, nt)
+    world = os.environ.get("WORLD_SIZE")
+    if world is None and args.gpus > 1:
+        # launched without torchrun: start one rank per GPU ourselves (same arguments), so that
+        # `python bench.py --gpus N` runs N ranks instead of silently running one
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+               f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
+    if world is not None and int(world) != args.gpus:
+        print(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}; refusing to report",
+              file=sys.stderr)
+        sys.exit(2)
     if args.impl == "reference":
         run_reference(args, wl)
     else:

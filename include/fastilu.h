@@ -181,6 +181,9 @@ fastilu_status fastilu_destroy(fastilu_handle h);
 /* ---------------- introspection (tests, bench) ---------------- */
 /* Owned rows and nnz(S) over the owned rows. */
 fastilu_status fastilu_get_sizes(fastilu_handle h, int64_t *n, int64_t *nnz_S, int64_t *nnz_A);
+/* CUDA device ordinal the handle runs on (opts.device, or the caller's current device at create
+ * time when opts.device < 0): device arrays passed to apply / gmres must live there. */
+fastilu_status fastilu_get_device(fastilu_handle h, int *device);
 /* Pattern of the owned rows (host arrays; row_ptr[n+1] rebased to 0, global columns,
  * level[nnz_S]); any pointer may be NULL. */
 fastilu_status fastilu_get_pattern(fastilu_handle h, int64_t *row_ptr, int32_t *col_idx,

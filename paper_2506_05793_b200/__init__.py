@@ -67,6 +67,7 @@ _SIGS = {
     "fastilu_gmres": (C.c_int, [H, C.c_void_p, C.c_void_p, C.c_int, C.c_double, C.c_int, C.c_int,
                                 C.POINTER(C.c_int), C.POINTER(C.c_double)]),
     "fastilu_get_sizes": (C.c_int, [H, I64P, I64P, I64P]),
+    "fastilu_get_device": (C.c_int, [H, C.POINTER(C.c_int)]),
     "fastilu_get_pattern": (C.c_int, [H, I64P, I32P, I8P]),
     "fastilu_get_factors": (C.c_int, [H, F64P, F64P]),
     "fastilu_get_residual_history": (C.c_int, [H, F64P, C.c_int, C.POINTER(C.c_int)]),
@@ -123,6 +124,43 @@ def _check(code, what, h=None):
 def _ptr(t):
     """Device pointer of a torch tensor or an int."""
     return t if isinstance(t, int) else t.data_ptr()
+
+
+def _host_in(a, count: int, what: str):
+    """A host input as a C-contiguous float64 array of exactly `count` entries (the C side reads
+    exactly that many)."""
+    v = np.ascontiguousarray(a, dtype=np.float64)
+    if v.ndim != 1 or v.shape[0] != count:
+        raise ValueError(f"{what}: expected {count} float64 values, got shape {v.shape}")
+    return v
+
+
+def _host_out(out, count: int, what: str):
+    """A caller-supplied host output buffer: float64, C-contiguous, writeable, `count` entries."""
+    if out is None:
+        return np.empty(count, dtype=np.float64)
+    if not (isinstance(out, np.ndarray) and out.dtype == np.float64 and out.ndim == 1 and
+            out.shape[0] == count and out.flags.c_contiguous and out.flags.writeable):
+        raise ValueError(f"{what}: `out` must be a writeable C-contiguous float64 array of "
+                         f"{count} entries")
+    return out
+
+
+def _dev_arg(t, count: int, device: int, what: str):
+    """Device pointer of a CUDA tensor after checking dtype (float64), device, contiguity and
+    length; raw integer pointers are passed through unchecked (the caller's contract)."""
+    if isinstance(t, int):
+        return t
+    if str(getattr(t, "dtype", "")) != "torch.float64":
+        raise ValueError(f"{what}: expected a float64 tensor, got {getattr(t, 'dtype', type(t))}")
+    if not getattr(t, "is_cuda", False):
+        raise ValueError(f"{what}: expected a CUDA tensor")
+    if device >= 0 and t.device.index != device:
+        raise ValueError(f"{what}: tensor on cuda:{t.device.index}, handle on cuda:{device}")
+    if not t.is_contiguous() or t.numel() != count:
+        raise ValueError(f"{what}: expected a contiguous tensor of {count} entries, got "
+                         f"{tuple(t.shape)}")
+    return t.data_ptr()
 
 
 # ---------------------------------------------------------------- ABI names (thin wrappers)
@@ -230,7 +268,12 @@ class FastILU:
         o.shift = float(shift)
         self._rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
         self._ci = np.ascontiguousarray(col_idx, dtype=np.int32)
-        vals = None if values is None else np.ascontiguousarray(values, dtype=np.float64)
+        if self._rp.ndim != 1 or self._rp.shape[0] < 1:
+            raise ValueError("row_ptr: expected a 1-D array of n + 1 offsets")
+        self._nnz_in = int(self._rp[-1])  # values the C side reads (lead rows included)
+        if self._ci.ndim != 1 or self._ci.shape[0] < self._nnz_in:
+            raise ValueError(f"col_idx: expected {self._nnz_in} entries, got {self._ci.shape}")
+        vals = None if values is None else _host_in(values, self._nnz_in, "values")
         nrows = (self._rp.shape[0] - 1 - int(n_lead)) if n is None else int(n)
         st = L.fastilu_create(C.byref(self._h), nrows, _p(self._rp, I64P), _p(self._ci, I32P),
                               None if vals is None else _p(vals, F64P), int(level_k),
@@ -244,15 +287,19 @@ class FastILU:
         L.fastilu_get_sizes(self._h, C.byref(n_), C.byref(s_), C.byref(a_))
         self.n, self.nnz_S, self.nnz_A = n_.value, s_.value, a_.value
         self.level_k = level_k
+        d_ = C.c_int(-1)
+        L.fastilu_get_device(self._h, C.byref(d_))
+        self.device = d_.value
 
     # -- numeric phase
     def set_values(self, values):
-        v = np.ascontiguousarray(values, dtype=np.float64)
+        v = _host_in(values, self._nnz_in, "values")
         _check(lib().fastilu_set_values(self._h, _p(v, F64P)), "fastilu_set_values", self._h)
 
     def set_values_device(self, values_dev):
-        _check(lib().fastilu_set_values_device(self._h, _ptr(values_dev)),
-               "fastilu_set_values_device", self._h)
+        _check(lib().fastilu_set_values_device(
+            self._h, _dev_arg(values_dev, self._nnz_in, self.device, "values")),
+            "fastilu_set_values_device", self._h)
 
     def compute(self, nsweeps: int):
         _check(lib().fastilu_compute(self._h, int(nsweeps)), "fastilu_compute", self._h)
@@ -260,15 +307,15 @@ class FastILU:
     def compute_host(self, values, nsweeps: int):
         """fastilu_compute_host: new host values + nsweeps sweeps, upload pipelined with the
         numeric phase (pass a pinned array for overlap)."""
-        v = np.ascontiguousarray(values, dtype=np.float64)
+        v = _host_in(values, self._nnz_in, "values")
         _check(lib().fastilu_compute_host(self._h, _p(v, F64P), int(nsweeps)),
                "fastilu_compute_host", self._h)
 
     def solve_host(self, values, nsweeps: int, b, ntrisweeps: int, out=None):
         """fastilu_solve_host: new host values, nsweeps sweeps, x = M^-1 b (host arrays)."""
-        v = np.ascontiguousarray(values, dtype=np.float64)
-        bb = np.ascontiguousarray(b, dtype=np.float64)
-        x = out if out is not None else np.empty(self.n, dtype=np.float64)
+        v = _host_in(values, self._nnz_in, "values")
+        bb = _host_in(b, self.n, "b")
+        x = _host_out(out, self.n, "solve_host")
         _check(lib().fastilu_solve_host(self._h, _p(v, F64P), int(nsweeps), _p(bb, F64P),
                                         _p(x, F64P), int(ntrisweeps)), "fastilu_solve_host",
                self._h)
@@ -293,12 +340,13 @@ class FastILU:
 
     def apply(self, b, x, ntrisweeps: int):
         """b, x: float64 CUDA tensors (or raw device pointers) of length n; x may alias b."""
-        _check(lib().fastilu_apply(self._h, _ptr(b), _ptr(x), int(ntrisweeps)), "fastilu_apply",
-               self._h)
+        _check(lib().fastilu_apply(self._h, _dev_arg(b, self.n, self.device, "b"),
+                                   _dev_arg(x, self.n, self.device, "x"), int(ntrisweeps)),
+               "fastilu_apply", self._h)
 
     def apply_host(self, b, ntrisweeps: int, out=None):
-        b = np.ascontiguousarray(b, dtype=np.float64)
-        x = np.empty(self.n) if out is None else out
+        b = _host_in(b, self.n, "b")
+        x = _host_out(out, self.n, "apply_host")
         _check(lib().fastilu_apply_host(self._h, _p(b, F64P), _p(x, F64P), int(ntrisweeps)),
                "fastilu_apply_host", self._h)
         return x
@@ -309,7 +357,8 @@ class FastILU:
         (inner iterations, relative residual)."""
         it = C.c_int(0)
         rr = C.c_double(0.0)
-        _check(lib().fastilu_gmres(self._h, _ptr(b), _ptr(x), int(restart), float(rtol),
+        _check(lib().fastilu_gmres(self._h, _dev_arg(b, self.n, self.device, "b"),
+                                   _dev_arg(x, self.n, self.device, "x"), int(restart), float(rtol),
                                    int(max_iters), int(ntrisweeps), C.byref(it), C.byref(rr)),
                "fastilu_gmres", self._h)
         return it.value, rr.value

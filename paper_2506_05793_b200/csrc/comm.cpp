@@ -127,6 +127,7 @@ struct Comm {
   cudaEvent_t ev_ready = nullptr, ev_done = nullptr;
   int64_t *d_scratch = nullptr;  // NCCL setup / reductions
   size_t scratch_elems = 0;
+  cudaStream_t host_stream = nullptr;  // host-side reductions (created once, NCCL only)
 };
 
 #define CUC(x)                                                    \
@@ -189,6 +190,7 @@ fastilu_status comm_init(Comm *&out, const fastilu_options &o, cudaStream_t st) 
     ncclUniqueId id;
     std::memcpy(&id, o.nccl_unique_id, sizeof(id));
     NCC(nccl().CommInitRank(&c->nc, o.nranks, id, o.rank));
+    CUC(cudaStreamCreateWithFlags(&c->host_stream, cudaStreamNonBlocking));
   } else {
     FAIL(FASTILU_ERR_INVALID_ARG);
   }
@@ -382,8 +384,7 @@ fastilu_status comm_allreduce_host(Comm *c, double *r2, int count, ErrFlags &ef)
   // NCCL: doubles summed, flags min-reduced (as uint64)
   fastilu_status s = scratch(c, (size_t)count + 2);
   if (s) return s;
-  cudaStream_t st = nullptr;
-  CUC(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  cudaStream_t st = c->host_stream;
   double *d = reinterpret_cast<double *>(c->d_scratch);
   uint64_t flags[2] = {ef.zero_diag, ef.zero_pivot};
   if (count) CUC(cudaMemcpyAsync(d, r2, count * sizeof(double), cudaMemcpyHostToDevice, st));
@@ -396,7 +397,6 @@ fastilu_status comm_allreduce_host(Comm *c, double *r2, int count, ErrFlags &ef)
   if (count) CUC(cudaMemcpyAsync(r2, d, count * sizeof(double), cudaMemcpyDeviceToHost, st));
   CUC(cudaMemcpyAsync(flags, c->d_scratch + count, sizeof(flags), cudaMemcpyDeviceToHost, st));
   CUC(cudaStreamSynchronize(st));
-  cudaStreamDestroy(st);
   ef.zero_diag = flags[0];
   ef.zero_pivot = flags[1];
   return FASTILU_OK;
@@ -408,6 +408,7 @@ void comm_destroy(Comm *c) {
   if (c->ev_ready) cudaEventDestroy(c->ev_ready);
   if (c->ev_done) cudaEventDestroy(c->ev_done);
   if (c->d_scratch) cudaFree(c->d_scratch);
+  if (c->host_stream) cudaStreamDestroy(c->host_stream);
   delete c;
 }
 

@@ -120,18 +120,6 @@ cudaError_t launch_tsell_jacobi(const TDev &t, bool lower, const double *vals,
                                 double *xn, double *xfinal, const double *s, int64_t r0,
                                 int64_t r1, int64_t Gh, double omega, bool final,
                                 cudaStream_t st);
-// fused ntri-sweep Jacobi solve (single GPU, template layout): lower (ascending tiles) or upper
-// (descending); sweep t writes buf + (t-1) E, the last upper sweep writes x = s o w if final_x.
-// sync_ws: tsell_trisolve_ws_bytes(ntri, r1 - r0) bytes of device workspace; grid must not
-// exceed the resident block capacity (blocks wait on each other).
-cudaError_t launch_tsell_trisolve_fused(const TDev &t, bool lower, bool final_x, int ntri,
-                                        const double *vals, const double *ud, const double *rhs,
-                                        const double *s, double *buf, double *xout, int64_t r0,
-                                        int64_t r1, int64_t E, int64_t Gh, double omega,
-                                        int64_t bandwidth, unsigned int *sync_ws, int grid,
-                                        cudaStream_t st);
-size_t tsell_trisolve_ws_bytes(int ntri, int64_t rows);
-cudaError_t tsell_trisolve_occupancy(int *blocks_per_sm);
 // deterministic sum of partials into *dst; also resets the tile counter (if non-null) to 0
 cudaError_t launch_reduce_reset(const double *partials, int np, double *dst,
                                 unsigned int *counter, cudaStream_t st);

@@ -91,19 +91,7 @@ struct fastilu_handle_s {
   size_t bsr_smem = 0;
   int bsr_minb = 1;
   int64_t bsr_nterms = 0;
-  // fused multi-sweep compute (template path, single GPU): iterates 0..ns in pool buffers
-  void *jit_fused = nullptr;
-  int fused_grid = 0;
-  std::vector<double *> fpool_v, fpool_u;  // extra value / diagonal buffers (iterates >= 2)
-  double **d_fptr_v = nullptr, **d_fptr_u = nullptr;
-  double *d_fpart = nullptr;
-  unsigned int *d_fws = nullptr;
-  int fused_cap = 0;
   const double *vals_cur = nullptr, *ud_cur = nullptr;  // factors of the last compute
-  // fused multi-sweep trisolve (template path, single GPU)
-  double *d_tribuf = nullptr;
-  unsigned int *d_triws = nullptr;
-  int tri_cap = 0, tri_grid = 0;
   std::vector<unsigned long long *> d_lmask;  // warm-up: presence masks of levels 0..K-1
   void *jit_sweep = nullptr;
   void *jit_sweep_first = nullptr;  // sweep 1 from iterate 0: A x A terms only
@@ -111,16 +99,8 @@ struct fastilu_handle_s {
   // staged sweep (tsell.h StagedCfg): pivot rows through shared memory by TMA
   void *jit_st = nullptr, *jit_st_first = nullptr;
   void *jit_st_init = nullptr;  // sweep 1 with iterate 0 computed from ahat (single GPU)
-  void *jit_tri[2] = {nullptr, nullptr};  // wavefront trisolve L / U (single GPU)
-  int tri_jgrid = 0;
-  void *jit_lag[2] = {nullptr, nullptr};  // lagged multi-sweep trisolve L / U (single GPU)
-  int lag_grid = 0;
   void *jit_scale = nullptr, *jit_ahat = nullptr;  // template-specialised a2 / a3 (tsell)
   void *jit_jac[2] = {nullptr, nullptr};            // template-specialised a8 / a9 sweeps
-  void *jit_jac2[2] = {nullptr, nullptr};  // two lagged sweeps per launch (single GPU)
-  double *d_z3 = nullptr, *d_w3 = nullptr;  // third iterate buffers of the paired sweeps
-  unsigned int *d_j2ws = nullptr;           // counter + per-tile flags of a paired launch
-  int j2_grid = 0, j2_lag = 0;
   StagedCfg st{}, st_init{};
   int st_grid = 0, st_init_grid = 0;
   int64_t st_ntiles = 0, st_init_ntiles = 0;
@@ -419,7 +399,7 @@ static fastilu_status setup_tsell(fastilu_handle h, const std::vector<unsigned l
     FAIL(FASTILU_ERR_UNSUPPORTED);
   }
   if (!std::getenv("FASTILU_NO_FIRST_SWEEP")) {
-    const std::string s1 = sweep_source(T, threads, parts, minb, false, pf, false, true);
+    const std::string s1 = sweep_source(T, threads, parts, minb, false, pf, true);
     if (jit_get(s1, "fastilu_tsell_sweep_first", h->device, &h->jit_sweep_first, &log))
       FAIL(FASTILU_ERR_UNSUPPORTED);
   }
@@ -507,22 +487,6 @@ static fastilu_status setup_tsell(fastilu_handle h, const std::vector<unsigned l
       }
     }
   }
-  // wavefront trisolve kernels (factor rows in registers across sweeps): single GPU, up to 40
-  // entries per triangular row (27-pt ILU(1) has 31).  Opt-in (FASTILU_JIT_TRISOLVE=1): it
-  // reads the factor once per apply but each tile's sweeps are latency-bound and wait on their
-  // neighbours -- measured 18.3 ms vs 6.7 ms for the streaming per-sweep kernels (c4, 5+5).
-  if (h->opt.nranks <= 1 && T.c0 <= 40 && T.W - T.c0 - 1 <= 40 &&
-      std::getenv("FASTILU_JIT_TRISOLVE") && atoi(std::getenv("FASTILU_JIT_TRISOLVE")) != 0) {
-    int tb = 0, ub = 0;
-    const std::string sl = trisolve_source(T, true, 256), su = trisolve_source(T, false, 256);
-    if (!jit_get(sl, "fastilu_tsell_tri_L", h->device, &h->jit_tri[0], &log) &&
-        !jit_get(su, "fastilu_tsell_tri_U", h->device, &h->jit_tri[1], &log) &&
-        !jit_occupancy(h->jit_tri[0], 256, 0, &tb) && !jit_occupancy(h->jit_tri[1], 256, 0, &ub) &&
-        tb > 0 && ub > 0)
-      h->tri_jgrid = sm_count(h->device) * std::min(tb, ub);
-    else
-      h->jit_tri[0] = h->jit_tri[1] = nullptr;
-  }
   // template-specialised scale / ahat kernels (FASTILU_NO_JIT_PREP=1 keeps the generic ones)
   if (!std::getenv("FASTILU_NO_JIT_PREP") && T.c0 >= 0 && T.w2a[T.c0] >= 0) {
     const std::string sp = prep_source(T, h->opt.nranks > 1);
@@ -539,46 +503,6 @@ static fastilu_status setup_tsell(fastilu_handle h, const std::vector<unsigned l
     if (jit_get(jl, "fastilu_tsell_jac_L", h->device, &h->jit_jac[0], &log) ||
         jit_get(ju, "fastilu_tsell_jac_U", h->device, &h->jit_jac[1], &log))
       h->jit_jac[0] = h->jit_jac[1] = nullptr;
-  }
-  // two lagged Jacobi sweeps per launch: opt-in (FASTILU_JAC2=1), measured
-  // slower than the streaming sweeps (c4 apply 6.3-7.2 ms vs 5.8 ms)
-  if (h->opt.nranks <= 1 && h->jit_jac[0] && h->jit_jac[1] && std::getenv("FASTILU_JAC2") &&
-      atoi(std::getenv("FASTILU_JAC2")) != 0) {
-    int lb = 0, ub = 0;
-    const char *em = std::getenv("FASTILU_JAC2_MODE");
-    const unsigned j2m = em ? (unsigned)atoi(em) : 0u;
-    if (!jit_get(jacobi_pair_source(T, true, j2m), "fastilu_tsell_jac2_L", h->device,
-                 &h->jit_jac2[0], &log) &&
-        !jit_get(jacobi_pair_source(T, false, j2m), "fastilu_tsell_jac2_U", h->device,
-                 &h->jit_jac2[1], &log) &&
-        !jit_occupancy(h->jit_jac2[0], 256, 0, &lb) && !jit_occupancy(h->jit_jac2[1], 256, 0, &ub) &&
-        lb > 0 && ub > 0) {
-      const char *eb = std::getenv("FASTILU_JAC2_BPS"), *el = std::getenv("FASTILU_JAC2_LAG");
-      const int bps = std::min(eb ? std::max(1, atoi(eb)) : 8, std::min(lb, ub));
-      h->j2_grid = sm_count(h->device) * bps;
-      // lag in tiles: above the steps in flight (one per resident block), so item B's
-      // dependencies are done when it starts
-      h->j2_lag = el ? std::max(1, atoi(el)) : h->j2_grid + 64;
-    } else {
-      h->jit_jac2[0] = h->jit_jac2[1] = nullptr;
-    }
-  }
-  // lagged multi-sweep trisolve: opt-in (FASTILU_TRILAG=1), measured slower than the streaming
-  // per-sweep kernels (c4 5+5: 9.2-16 ms vs 6.7 ms)
-  if (h->opt.nranks <= 1 && std::getenv("FASTILU_TRILAG") && atoi(std::getenv("FASTILU_TRILAG"))) {
-    int lb = 0, ub = 0;
-    const std::string sl = trisolve_lag_source(T, true, 256), su = trisolve_lag_source(T, false, 256);
-    if (!jit_get(sl, "fastilu_tsell_trilag_L", h->device, &h->jit_lag[0], &log) &&
-        !jit_get(su, "fastilu_tsell_trilag_U", h->device, &h->jit_lag[1], &log) &&
-        !jit_occupancy(h->jit_lag[0], 256, 0, &lb) && !jit_occupancy(h->jit_lag[1], 256, 0, &ub) &&
-        lb > 0 && ub > 0)
-    {  // resident blocks bound the lag and so the L2 footprint of the re-read factor rows
-      const char *eb = std::getenv("FASTILU_TRILAG_BPS");
-      const int cap = eb ? std::max(1, atoi(eb)) : 3;
-      h->lag_grid = sm_count(h->device) * std::min(cap, std::min(lb, ub));
-    }
-    else
-      h->jit_lag[0] = h->jit_lag[1] = nullptr;
   }
   int bps = 0;
   jit_func_info(h->jit_sweep, &h->t_regs, &h->t_spill, threads, &bps);
@@ -974,6 +898,7 @@ extern "C" fastilu_status fastilu_create(fastilu_handle *out, int64_t n, const i
                                          int level_k, const fastilu_options *opts) {
   if (!out) FAIL(FASTILU_ERR_INVALID_ARG);
   *out = nullptr;
+  DeviceGuard dg_(-1);  // restores the caller's device (create switches to opts->device)
   fastilu_handle h = new (std::nothrow) fastilu_handle_s();
   if (!h) return FASTILU_ERR_OOM;
   *out = h;
@@ -1000,98 +925,17 @@ extern "C" fastilu_status fastilu_create(fastilu_handle *out, int64_t n, const i
 
 extern "C" fastilu_status fastilu_set_values(fastilu_handle h, const double *values) {
   if (!h || !values || !h->d_aval) FAIL(FASTILU_ERR_INVALID_ARG);
-  cudaSetDevice(h->device);
+  DeviceGuard dg_(h->device);
   return upload_values(h, values, false);
 }
 
 extern "C" fastilu_status fastilu_set_values_device(fastilu_handle h, const double *values) {
   if (!h || !values || !h->d_aval) FAIL(FASTILU_ERR_INVALID_ARG);
-  cudaSetDevice(h->device);
+  DeviceGuard dg_(h->device);
   return upload_values(h, values, true);
 }
 
 // --------------------------------------------------------------------------- compute
-// Wavefront (multi-sweep) kernels: opt-in with FASTILU_FUSED=1 (measured slower than the
-// per-sweep kernels so far, profiles/ and DESIGN.md); FASTILU_NO_FUSED_* force them off.
-static bool fused_enabled(const char *off_var) {
-  const char *on = std::getenv("FASTILU_FUSED");
-  return on && atoi(on) != 0 && !std::getenv(off_var);
-}
-
-// All nsweeps synchronous sweeps in ONE persistent wavefront kernel (template path, single GPU):
-// sweep s of row i reads iterate s-1 of rows <= i only, so tiles are processed in row order and
-// each block runs every sweep of its tile, waiting until all earlier tiles finished the previous
-// sweep; iterate s lives in its own buffer.  Same per-row arithmetic as the per-sweep kernel.
-static fastilu_status sweeps_fused(fastilu_handle h, int ns, cudaStream_t st) {
-  const Template &T = h->T;
-  if (!h->jit_fused) {
-    std::string log;
-    const std::string src = sweep_source(T, h->t_threads, h->t_parts, h->t_minb, false, false,
-                                         true);
-    if (jit_get(src, "fastilu_tsell_compute_fused", h->device, &h->jit_fused, &log))
-      FAIL(FASTILU_ERR_UNSUPPORTED);
-    int bps = 0;
-    jit_func_info(h->jit_fused, nullptr, nullptr, h->t_threads, &bps);
-    if (bps < 1) FAIL(FASTILU_ERR_UNSUPPORTED);
-    h->fused_grid = sm_count(h->device) * bps;
-  }
-  const int64_t rpt = sweep_rows_per_tile(h->t_threads, h->t_parts, true);
-  const int64_t ntiles = (h->n + rpt - 1) / rpt;
-  const int64_t nv = h->nsl * T.W * 32;
-  if (ns > h->fused_cap) {
-    for (int q = (int)h->fpool_v.size(); q < ns - 1; q++) {  // iterates 2..ns
-      double *v = nullptr, *u = nullptr;
-      CU(dalloc(&v, nv));
-      CU(cudaMemset(v, 0, sizeof(double) * nv));  // absent slots stay +0.0
-      CU(dalloc(&u, h->E));
-      CU(cudaMemset(u, 0, sizeof(double) * h->E));
-      h->fpool_v.push_back(v);
-      h->fpool_u.push_back(u);
-    }
-    if (h->d_fptr_v) cudaFree(h->d_fptr_v);
-    if (h->d_fptr_u) cudaFree(h->d_fptr_u);
-    if (h->d_fpart) cudaFree(h->d_fpart);
-    if (h->d_fws) cudaFree(h->d_fws);
-    std::vector<double *> pv{h->d_vals[0], h->d_vals[1]}, pu{h->d_ud[0], h->d_ud[1]};
-    for (size_t q = 0; q < h->fpool_v.size(); q++) {
-      pv.push_back(h->fpool_v[q]);
-      pu.push_back(h->fpool_u[q]);
-    }
-    CU(dalloc(&h->d_fptr_v, (int64_t)pv.size()));
-    CU(dalloc(&h->d_fptr_u, (int64_t)pu.size()));
-    CU(cudaMemcpy(h->d_fptr_v, pv.data(), sizeof(double *) * pv.size(), cudaMemcpyHostToDevice));
-    CU(cudaMemcpy(h->d_fptr_u, pu.data(), sizeof(double *) * pu.size(), cudaMemcpyHostToDevice));
-    CU(dalloc(&h->d_fpart, (int64_t)ns * ntiles));
-    CU(cudaMalloc((void **)&h->d_fws, 128 + (size_t)ns * ntiles + 16));
-    h->fused_cap = ns;
-  }
-  const size_t ws = 128 + (size_t)ns * ntiles;
-  CU(cudaMemsetAsync(h->d_fws, 0, ws, st));
-  double **bufs = h->d_fptr_v, **udbufs = h->d_fptr_u;
-  int nsw = ns;
-  unsigned int *ctr = h->d_fws;
-  unsigned char *flags = reinterpret_cast<unsigned char *>(h->d_fws) + 128;
-  // tiles a tile's sweep reads from: pivots and divisors lie within the lower bandwidth
-  int dep = (int)std::min<int64_t>(ntiles, (-(int64_t)T.off[0] + rpt - 1) / rpt + 1);
-  const double *ahat = h->d_ahat;
-  const unsigned long long *mk = h->d_tmask;
-  long long a0 = h->G, a1 = h->G + h->n;
-  double om = h->opt.omega;
-  double *part = h->d_fpart;
-  unsigned long long *zp = &h->d_err->zero_pivot;
-  int sstr1 = 1;  // the wavefront kernel walks consecutive slices
-  void *args[] = {&bufs, &udbufs, &nsw, &dep, &flags, &ahat, &mk, &a0, &a1, &om, &part, &zp,
-                  &ctr, &sstr1};
-  const int grid = (int)std::min<int64_t>(h->fused_grid, ntiles);
-  if (jit_launch(h->jit_fused, grid, h->t_threads, st, args)) FAIL(FASTILU_ERR_CUDA);
-  for (int sw = 1; sw <= ns; sw++)
-    CU(launch_reduce(h->d_fpart + (int64_t)(sw - 1) * ntiles, (int)ntiles, h->d_r2 + (sw - 1),
-                     st));
-  h->vals_cur = ns == 0 ? h->d_vals[0] : ns == 1 ? h->d_vals[1] : h->fpool_v[ns - 2];
-  h->ud_cur = ns == 0 ? h->d_ud[0] : ns == 1 ? h->d_ud[1] : h->fpool_u[ns - 2];
-  return FASTILU_OK;
-}
-
 // nsweeps synchronous sweeps; with rtol > 0, stop after the first sweep s whose residual of
 // iterate s-1 satisfies r(s-1) <= rtol ||Ahat|_S||_F (reading G15), at most nsweeps.
 static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, int *done,
@@ -1113,7 +957,7 @@ static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, i
     nsweeps = per_level * (h->K + 1);
   }
   if (!h->have_values || !h->d_aval) FAIL(FASTILU_ERR_STATE);
-  cudaSetDevice(h->device);
+  DeviceGuard dg_(h->device);
   (void)cudaGetLastError();  // clear a non-sticky error left by the caller's own CUDA work
   h->computed = false;
   h->err_index = -1;
@@ -1154,8 +998,7 @@ static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, i
   // rows and scales are local), so sweep 1 stages them like owned rows and iterate 0 needs no
   // halo.
   const bool fuse_init = h->tsell && h->jit_st_init && h->jit_st && h->jit_ahat && !warmup &&
-                         !async && nsweeps >= 1 && h->opt.omega == 1.0 &&
-                         !fused_enabled("FASTILU_NO_FUSED_SWEEPS");
+                         !async && nsweeps >= 1 && h->opt.omega == 1.0;
   if (h->tsell && fuse_init) {
     const double *aT = h->d_aT, *sv = h->d_s;
     const unsigned long long *mk = h->d_tmask;
@@ -1197,15 +1040,8 @@ static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, i
     thr2 = rtol * rtol * a2;
   }
   int executed = 0;
-  const bool fused = h->tsell && !h->comm && !warmup && !async && thr2 < 0.0 && nsweeps > 0 &&
-                     fused_enabled("FASTILU_NO_FUSED_SWEEPS");
-  if (fused) {
-    fastilu_status fs = sweeps_fused(h, nsweeps, st);
-    if (fs) return fs;
-    executed = nsweeps;
-  }
   // a4/a5: nsweeps synchronous sweeps, ping-pong buffers
-  for (int sw = 1; sw <= nsweeps && !fused; sw++) {
+  for (int sw = 1; sw <= nsweeps; sw++) {
     if (sw == 2) CU(cudaEventRecord(h->ev[5], st));  // sweep 1 / the rest split
     executed = sw;
     const int ib_async = 0;  // asynchronous sweeps stay in buffer 0 (in place)
@@ -1304,8 +1140,8 @@ static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, i
   CU(cudaEventElapsedTime(&h->t_init, h->ev[0], h->ev[1]));
   CU(cudaEventElapsedTime(&h->t_sweeps, h->ev[1], h->ev[2]));
   h->t_sweep1 = h->t_sweeps;
-  h->last_ns = fused ? 0 : executed;
-  if (!fused && executed >= 2) CU(cudaEventElapsedTime(&h->t_sweep1, h->ev[1], h->ev[5]));
+  h->last_ns = executed;
+  if (executed >= 2) CU(cudaEventElapsedTime(&h->t_sweep1, h->ev[1], h->ev[5]));
   h->resid.assign(nsweeps, 0.0);
   std::vector<double> r2(h->h_r2, h->h_r2 + nsweeps);
   ErrFlags ef = *h->h_err;  // local rows -> global rows
@@ -1318,10 +1154,8 @@ static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, i
   for (size_t q = 0; q < r2tol.size() && q < r2.size(); q++) r2[q] = r2tol[q];
   for (int i = 0; i < nsweeps; i++) h->resid[i] = std::sqrt(r2[i]);
   h->cur = async ? 0 : (nsweeps & 1);
-  if (!fused) {
-    h->vals_cur = h->d_vals[h->cur];
-    h->ud_cur = h->d_ud[h->cur];
-  }
+  h->vals_cur = h->d_vals[h->cur];
+  h->ud_cur = h->d_ud[h->cur];
   if (ef.zero_diag != ~0ull) {
     h->err_index = (int64_t)ef.zero_diag;
     return FASTILU_ERR_ZERO_DIAG;
@@ -1356,7 +1190,7 @@ static fastilu_status compute_host_impl(fastilu_handle h, const double *values, 
   const int C = (int)((h->n + chunk - 1) / std::max<int64_t>(chunk, 1));
   const bool ok = h->tsell && !h->comm && h->jit_st && h->jit_st_init && h->jit_ahat &&
                   h->jit_scale && nsweeps >= 1 && h->opt.omega == 1.0 && h->G == 0 &&
-                  h->st.shift == 0 && C >= 2 && !fused_enabled("FASTILU_NO_FUSED_SWEEPS") &&
+                  h->st.shift == 0 && C >= 2 &&
                   !std::getenv("FASTILU_NO_PIPELINE");
   if (!ok) {
     fastilu_status us = upload_values(h, values, false);
@@ -1364,6 +1198,7 @@ static fastilu_status compute_host_impl(fastilu_handle h, const double *values, 
     return compute_impl(h, nsweeps, 0.0, nullptr);
   }
   h->computed = false;
+  h->have_values = false;  // d_aval is overwritten below; set again once every chunk landed
   h->err_index = -1;
   cudaStream_t st = h->stream;
   if (!h->copy_stream) CU(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
@@ -1514,11 +1349,18 @@ static fastilu_status compute_host_impl(fastilu_handle h, const double *values, 
   return FASTILU_OK;
 }
 
+// On any failure after copies were queued, wait for the copy stream so that no DMA still reads
+// the caller's buffers when the call returns (the caller may free them).
+static fastilu_status drain_copies(fastilu_handle h, fastilu_status s) {
+  if (s != FASTILU_OK && h->copy_stream) cudaStreamSynchronize(h->copy_stream);
+  return s;
+}
+
 extern "C" fastilu_status fastilu_compute_host(fastilu_handle h, const double *values,
                                                int nsweeps) {
   if (!h || !values || !h->d_aval || nsweeps < 0) FAIL(FASTILU_ERR_INVALID_ARG);
-  cudaSetDevice(h->device);
-  return compute_host_impl(h, values, nsweeps);
+  DeviceGuard dg_(h->device);
+  return drain_copies(h, compute_host_impl(h, values, nsweeps));
 }
 
 // fastilu_solve_host: compute_host(values, nsweeps) + apply_host(b, x, ntri), b's upload queued
@@ -1528,9 +1370,9 @@ extern "C" fastilu_status fastilu_solve_host(fastilu_handle h, const double *val
   if (!h || !values || !h->d_aval || nsweeps < 0 || ntrisweeps < 1 ||
       (h->n > 0 && (!b || !x)))
     FAIL(FASTILU_ERR_INVALID_ARG);
-  cudaSetDevice(h->device);
+  DeviceGuard dg_(h->device);
   bool queued = false;
-  fastilu_status s = compute_host_impl(h, values, nsweeps, b, &queued);
+  fastilu_status s = drain_copies(h, compute_host_impl(h, values, nsweeps, b, &queued));
   if (s) return s;
   if (!queued) return fastilu_apply_host(h, b, x, ntrisweeps);
   CU(cudaStreamWaitEvent(h->stream, h->chunk_ev[h->chunk_b], 0));
@@ -1564,128 +1406,6 @@ extern "C" fastilu_status fastilu_compute_tol(fastilu_handle h, double rtol, int
 }
 
 // --------------------------------------------------------------------------- apply
-static fastilu_status apply_fused(fastilu_handle h, const double *b, double *x, int ntri) {
-  cudaStream_t st = h->stream;
-  if (ntri > h->tri_cap) {
-    if (h->d_tribuf) cudaFree(h->d_tribuf);
-    if (h->d_triws) cudaFree(h->d_triws);
-    h->d_tribuf = nullptr;
-    h->d_triws = nullptr;
-    CU(dalloc(&h->d_tribuf, (int64_t)2 * ntri * h->E));
-    CU(cudaMemset(h->d_tribuf, 0, sizeof(double) * 2 * ntri * h->E));
-    const size_t ws = tsell_trisolve_ws_bytes(ntri, h->n);
-    CU(cudaMalloc((void **)&h->d_triws, ws));
-    h->tri_cap = ntri;
-    if (!h->tri_grid) {  // resident capacity: blocks wait on each other
-      int bps = 0;
-      CU(tsell_trisolve_occupancy(&bps));
-      h->tri_grid = std::max(1, sm_count(h->device) * bps);
-    }
-  }
-  const int64_t r0 = h->G, r1 = h->G + h->n;
-  const int64_t ntiles = (h->n + 255) / 256;
-  const int grid = (int)std::min<int64_t>(h->tri_grid, ntiles);
-  const double om = h->opt.omega_tri;
-  const double *vals = h->vals_cur, *ud = h->ud_cur;
-  double *zb = h->d_tribuf, *wb = h->d_tribuf + (int64_t)ntri * h->E;
-  // y = s o b into d_y (the L solve's right-hand side)
-  CU(launch_trisolve_first_L(b, h->d_s, h->d_y, zb, r0, r1, h->G, 1.0, st));
-  const int64_t bwl = -(int64_t)h->T.off[0], bwu = (int64_t)h->T.off[h->T.W - 1];
-  CU(launch_tsell_trisolve_fused(tdev(h), true, false, ntri, vals, nullptr, h->d_y, h->d_s, zb,
-                                 nullptr, r0, r1, h->E, h->G, om, bwl, h->d_triws, grid, st));
-  const double *zf = zb + (int64_t)(ntri - 1) * h->E;
-  CU(launch_tsell_trisolve_fused(tdev(h), false, true, ntri, vals, ud, zf, h->d_s, wb, x, r0, r1,
-                                 h->E, h->G, om, bwu, h->d_triws, grid, st));
-  return FASTILU_OK;
-}
-
-// a8 + a9 as two wavefront kernels (tsell.h trisolve_source): all ntri sweeps of a triangle in
-// one launch, the factor read once.
-static fastilu_status apply_jit(fastilu_handle h, const double *b, double *x, int ntri) {
-  cudaStream_t st = h->stream;
-  const int64_t R = 256, ntiles = (h->n + R - 1) / R;
-  const size_t ws = 128 + (size_t)ntri * ntiles;
-  if (ntri > h->tri_cap || !h->d_tribuf) {
-    if (h->d_tribuf) cudaFree(h->d_tribuf);
-    if (h->d_triws) cudaFree(h->d_triws);
-    h->d_tribuf = nullptr;
-    h->d_triws = nullptr;
-    CU(dalloc(&h->d_tribuf, (int64_t)2 * ntri * h->E));
-    CU(cudaMemset(h->d_tribuf, 0, sizeof(double) * 2 * ntri * h->E));
-    CU(cudaMalloc((void **)&h->d_triws, std::max(ws, tsell_trisolve_ws_bytes(ntri, h->n))));
-    h->tri_cap = ntri;
-  }
-  long long r0 = h->G, r1 = h->G + h->n, E = h->E, Gh = h->G, nt = ntiles;
-  double om = h->opt.omega_tri;
-  const double *vals = h->vals_cur, *ud = h->ud_cur, *sv = h->d_s;
-  const unsigned long long *mk = h->d_tmask;
-  const int grid = (int)std::min<int64_t>(h->tri_jgrid, ntiles);
-  int nts = ntri;
-  for (int tri = 0; tri < 2; tri++) {
-    const bool lower = tri == 0;
-    double *bufp = h->d_tribuf + (lower ? 0 : (int64_t)ntri * h->E);
-    const double *rhs = lower ? b : h->d_tribuf + (int64_t)(ntri - 1) * h->E;
-    double *xo = x;
-    unsigned int *ctr = h->d_triws;
-    unsigned char *flags = reinterpret_cast<unsigned char *>(h->d_triws) + 128;
-    const int64_t bw = lower ? -(int64_t)h->T.off[0] : (int64_t)h->T.off[h->T.W - 1];
-    int dep = (int)std::min<int64_t>(ntiles, (bw + R - 1) / R + 1);
-    int fx = lower ? 0 : 1;
-    CU(cudaMemsetAsync(h->d_triws, 0, ws, st));
-    void *args[] = {&vals, &ud, &mk, &rhs, &sv, &bufp, &xo, &r0, &r1, &E, &Gh, &nts, &om,
-                    &ctr, &flags, &nt, &dep, &fx};
-    if (jit_launch(h->jit_tri[tri], grid, 256, st, args)) return FASTILU_ERR_CUDA;
-  }
-  return FASTILU_OK;
-}
-
-// a8 + a9 with the lagged multi-sweep kernels (tsell.h trisolve_lag_source): launches of up to
-// S sweeps (FASTILU_TRILAG_S, default 3) in which a tile's factor rows are re-read from L2.
-static fastilu_status apply_lag(fastilu_handle h, const double *b, double *x, int ntri) {
-  cudaStream_t st = h->stream;
-  const int64_t R = 256, ntiles = (h->n + R - 1) / R;
-  const size_t ws = 128 + (size_t)ntri * ntiles;
-  if (ntri > h->tri_cap || !h->d_tribuf) {
-    if (h->d_tribuf) cudaFree(h->d_tribuf);
-    if (h->d_triws) cudaFree(h->d_triws);
-    h->d_tribuf = nullptr;
-    h->d_triws = nullptr;
-    CU(dalloc(&h->d_tribuf, (int64_t)2 * ntri * h->E));
-    CU(cudaMemset(h->d_tribuf, 0, sizeof(double) * 2 * ntri * h->E));
-    CU(cudaMalloc((void **)&h->d_triws, std::max(ws, tsell_trisolve_ws_bytes(ntri, h->n))));
-    h->tri_cap = ntri;
-  }
-  const char *ev = std::getenv("FASTILU_TRILAG_S");
-  const int smax = ev ? std::max(1, atoi(ev)) : 3;
-  long long r0 = h->G, r1 = h->G + h->n, E = h->E, Gh = h->G, nt = ntiles;
-  double om = h->opt.omega_tri;
-  const double *vals = h->vals_cur, *ud = h->ud_cur, *sv = h->d_s;
-  const unsigned long long *mk = h->d_tmask;
-  const int grid = (int)std::min<int64_t>(h->lag_grid, ntiles + 2 * (int64_t)h->lag_grid);
-  int lag = h->lag_grid + 32, nts = ntri;
-  unsigned int *ctr = h->d_triws;
-  unsigned char *flags = reinterpret_cast<unsigned char *>(h->d_triws) + 128;
-  for (int tri = 0; tri < 2; tri++) {
-    const bool lower = tri == 0;
-    double *bufp = h->d_tribuf + (lower ? 0 : (int64_t)ntri * h->E);
-    const double *rhs = lower ? b : h->d_tribuf + (int64_t)(ntri - 1) * h->E;
-    double *xo = x;
-    const int64_t bw = lower ? -(int64_t)h->T.off[0] : (int64_t)h->T.off[h->T.W - 1];
-    int dep = (int)std::min<int64_t>(ntiles, (bw + R - 1) / R + 1);
-    int fx = lower ? 0 : 1;
-    CU(cudaMemsetAsync(h->d_triws, 0, ws, st));
-    for (int t0 = 1; t0 <= ntri;) {
-      int S = std::min(smax, ntri - t0 + 1);
-      if (t0 > 1) CU(cudaMemsetAsync(ctr, 0, sizeof(unsigned int), st));
-      void *args[] = {&vals, &ud, &mk, &rhs, &sv, &bufp, &xo, &r0, &r1, &E, &Gh, &nts, &t0,
-                      &S, &lag, &om, &ctr, &flags, &nt, &dep, &fx};
-      if (jit_launch(h->jit_lag[tri], grid, 256, st, args)) return FASTILU_ERR_CUDA;
-      t0 += S;
-    }
-  }
-  return FASTILU_OK;
-}
-
 // one template-specialised Jacobi sweep (tsell.h jacobi_source); nonzero on a launch error
 static int jit_jacobi(fastilu_handle h, bool lower, const double *vals, const double *ud,
                       const double *rhs, const double *xo, double *xn, double *xf, int64_t r0,
@@ -1700,85 +1420,8 @@ static int jit_jacobi(fastilu_handle h, bool lower, const double *vals, const do
                     args);
 }
 
-// a8 + a9 with two sweeps per launch (tsell.h jacobi_pair_source): z^t lives in zb[t % 3] so a
-// launch's input, middle and output iterates are distinct buffers; an odd sweep left over runs
-// the streaming kernel.  The last U sweep writes x = s o w.
-static fastilu_status apply_jac2(fastilu_handle h, const double *b, double *x, int ntri) {
-  cudaStream_t st = h->stream;
-  const int64_t R = 256, ntiles = (h->n + R - 1) / R;
-  const size_t ws = 128 + (size_t)ntiles;
-  if (!h->d_z3) {
-    CU(dalloc(&h->d_z3, h->E));
-    CU(dalloc(&h->d_w3, h->E));
-    CU(cudaMemset(h->d_z3, 0, sizeof(double) * h->E));
-    CU(cudaMemset(h->d_w3, 0, sizeof(double) * h->E));
-    CU(cudaMalloc((void **)&h->d_j2ws, ws));
-  }
-  const int64_t r0 = h->G, r1 = h->G + h->n;
-  const double om = h->opt.omega_tri;
-  const double *vals = h->vals_cur, *ud = h->ud_cur;
-  double *zb[3] = {h->d_z[0], h->d_z[1], h->d_z3}, *wb[3] = {h->d_w[0], h->d_w[1], h->d_w3};
-  unsigned int *ctr = h->d_j2ws;
-  unsigned char *flags = reinterpret_cast<unsigned char *>(h->d_j2ws) + 128;
-  auto pair = [&](bool lower, const double *rhs, double **vb, int t, bool final_x) -> int {
-    if (cudaMemsetAsync(h->d_j2ws, 0, ws, st) != cudaSuccess) return 1;
-    const double *xa = vb[(t - 1) % 3];
-    double *xb = vb[t % 3], *xc = vb[(t + 1) % 3], *xf = x;
-    const unsigned long long *mk = h->d_tmask;
-    const double *sv = h->d_s;
-    long long a0 = r0, a1 = r1, g = h->G, nt = ntiles;
-    double omv = om;
-    int fx = final_x ? 1 : 0, lag = h->j2_lag;
-    const int64_t bw = lower ? -(int64_t)h->T.off[0] : (int64_t)h->T.off[h->T.W - 1];
-    int dep = (int)std::min<int64_t>(ntiles, (bw + R - 1) / R + 1);
-    const int grid = (int)std::min<int64_t>(h->j2_grid, ntiles + lag);
-    void *args[] = {&vals, &ud, &mk, &rhs, &xa, &xb, &xc, &xf, &sv, &a0, &a1, &g, &omv, &fx,
-                    &ctr, &flags, &nt, &lag, &dep};
-    return jit_launch(h->jit_jac2[lower ? 0 : 1], grid, 256, st, args);
-  };
-  // a8: t = 1: z1 = w y, y = s o b (z0 = 0)
-  CU(launch_trisolve_first_L(b, h->d_s, h->d_y, zb[1], r0, r1, h->G, om, st));
-  for (int t = 2; t <= ntri;) {
-    if (t + 1 <= ntri) {
-      if (pair(true, h->d_y, zb, t, false)) FAIL(FASTILU_ERR_CUDA);
-      t += 2;
-    } else {
-      if (jit_jacobi(h, true, vals, nullptr, h->d_y, zb[(t - 1) % 3], zb[t % 3], nullptr, r0, r1,
-                     0, om, false))
-        FAIL(FASTILU_ERR_CUDA);
-      t += 1;
-    }
-  }
-  const double *zf = zb[ntri % 3];
-  // a9: t = 1: w1 = w z / u_ii; the last sweep writes x = s o w
-  CU(launch_trisolve_first_U(zf, ud, h->d_s, wb[1], x, r0, r1, h->G, om, ntri == 1, st));
-  for (int t = 2; t <= ntri;) {
-    if (t + 1 <= ntri) {
-      if (pair(false, zf, wb, t, t + 1 == ntri)) FAIL(FASTILU_ERR_CUDA);
-      t += 2;
-    } else {
-      if (jit_jacobi(h, false, vals, ud, zf, wb[(t - 1) % 3], wb[t % 3], x, r0, r1, h->G, om,
-                     t == ntri))
-        FAIL(FASTILU_ERR_CUDA);
-      t += 1;
-    }
-  }
-  return FASTILU_OK;
-}
-
 static fastilu_status apply_impl(fastilu_handle h, const double *b, double *x, int ntri) {
   cudaStream_t st = h->stream;
-  if (h->tsell && !h->comm && h->jit_jac2[0] && h->jit_jac2[1] && ntri >= 3 &&
-      !(h->jit_lag[0] && h->jit_lag[1]) && !(h->jit_tri[0] && h->jit_tri[1]) &&
-      !fused_enabled("FASTILU_NO_FUSED_TRISOLVE"))
-    return apply_jac2(h, b, x, ntri);
-  if (h->tsell && !h->comm && h->jit_lag[0] && h->jit_lag[1] && ntri >= 1 &&
-      !(h->jit_tri[0] && h->jit_tri[1]))
-    return apply_lag(h, b, x, ntri);
-  if (h->tsell && !h->comm && h->jit_tri[0] && h->jit_tri[1] && ntri >= 1)
-    return apply_jit(h, b, x, ntri);
-  if (h->tsell && !h->comm && fused_enabled("FASTILU_NO_FUSED_TRISOLVE"))
-    return apply_fused(h, b, x, ntri);
   DevPattern P{h->d_rp, h->d_ci, h->d_dloc};
   const int64_t r0 = h->G, r1 = h->G + h->n;
   const double om = h->opt.omega_tri;
@@ -1828,7 +1471,7 @@ extern "C" fastilu_status fastilu_apply(fastilu_handle h, const double *b, doubl
                                         int ntrisweeps) {
   if (!h || ntrisweeps < 1 || (h->n > 0 && (!b || !x))) FAIL(FASTILU_ERR_INVALID_ARG);
   if (!h->computed) FAIL(FASTILU_ERR_STATE);
-  cudaSetDevice(h->device);
+  DeviceGuard dg_(h->device);
   (void)cudaGetLastError();  // clear a non-sticky error left by the caller's own CUDA work
   CU(cudaEventRecord(h->ev[3], h->stream));
   fastilu_status s = apply_impl(h, b, x, ntrisweeps);
@@ -1842,7 +1485,7 @@ extern "C" fastilu_status fastilu_apply_host(fastilu_handle h, const double *b, 
                                              int ntrisweeps) {
   if (!h || ntrisweeps < 1 || (h->n > 0 && (!b || !x))) FAIL(FASTILU_ERR_INVALID_ARG);
   if (!h->computed) FAIL(FASTILU_ERR_STATE);
-  cudaSetDevice(h->device);
+  DeviceGuard dg_(h->device);
   (void)cudaGetLastError();  // clear a non-sticky error left by the caller's own CUDA work
   if (!h->d_bx) CU(dalloc(&h->d_bx, 2 * h->n));
   CU(cudaMemcpyAsync(h->d_bx, b, sizeof(double) * h->n, cudaMemcpyHostToDevice, h->stream));
@@ -1870,7 +1513,7 @@ extern "C" fastilu_status fastilu_gmres(fastilu_handle h, const double *b, doubl
       (h->n > 0 && (!b || !x)))
     FAIL(FASTILU_ERR_INVALID_ARG);
   if (!h->computed) FAIL(FASTILU_ERR_STATE);
-  cudaSetDevice(h->device);
+  DeviceGuard dg_(h->device);
   (void)cudaGetLastError();  // clear a non-sticky error left by the caller's own CUDA work
   cudaStream_t st = h->stream;
   const int64_t n = h->n;
@@ -1999,6 +1642,12 @@ extern "C" fastilu_status fastilu_gmres(fastilu_handle h, const double *b, doubl
 }
 
 // --------------------------------------------------------------------------- introspection
+extern "C" fastilu_status fastilu_get_device(fastilu_handle h, int *device) {
+  if (!h || !device) FAIL(FASTILU_ERR_INVALID_ARG);
+  *device = h->device;
+  return FASTILU_OK;
+}
+
 extern "C" fastilu_status fastilu_get_sizes(fastilu_handle h, int64_t *n, int64_t *nnz_S,
                                             int64_t *nnz_A) {
   if (!h) FAIL(FASTILU_ERR_INVALID_ARG);
@@ -2028,7 +1677,7 @@ extern "C" fastilu_status fastilu_get_pattern(fastilu_handle h, int64_t *row_ptr
 extern "C" fastilu_status fastilu_get_factors(fastilu_handle h, double *vals, double *s) {
   if (!h) FAIL(FASTILU_ERR_INVALID_ARG);
   if (!h->computed) FAIL(FASTILU_ERR_STATE);
-  cudaSetDevice(h->device);
+  DeviceGuard dg_(h->device);
   (void)cudaGetLastError();  // clear a non-sticky error left by the caller's own CUDA work
   CU(cudaStreamSynchronize(h->stream));
   if (vals && h->tsell) {  // gather the owned rows' S entries out of the template slots
@@ -2062,7 +1711,7 @@ extern "C" fastilu_status fastilu_get_residual_history(fastilu_handle h, double 
 
 extern "C" fastilu_status fastilu_get_timings(fastilu_handle h, double *t3) {
   if (!h || !t3) FAIL(FASTILU_ERR_INVALID_ARG);
-  cudaSetDevice(h->device);
+  DeviceGuard dg_(h->device);
   float ta = 0.f;
   if (h->apply_timed && cudaEventQuery(h->ev[4]) == cudaSuccess &&
       cudaEventElapsedTime(&ta, h->ev[3], h->ev[4]) != cudaSuccess) {
@@ -2121,7 +1770,7 @@ extern "C" fastilu_status fastilu_get_info(fastilu_handle h, char *buf, int cap)
 
 extern "C" fastilu_status fastilu_destroy(fastilu_handle h) {
   if (!h) return FASTILU_OK;
-  cudaSetDevice(h->device);
+  DeviceGuard dg_(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
   if (h->comm) comm_destroy(h->comm);
   void *ptrs[] = {h->d_rp,    h->d_ci,    h->d_dloc,     h->d_arp,  h->d_aci,     h->d_apos,
@@ -2130,8 +1779,7 @@ extern "C" fastilu_status fastilu_destroy(fastilu_handle h) {
                   h->d_w[0],  h->d_w[1],  h->d_bx,       h->d_partials, h->d_r2,  h->d_err,
                   h->d_rclass, h->d_coff, h->d_caoff, h->d_prog, h->d_toff, h->d_toffA,
                   h->d_tasrc, h->d_tw2a, h->d_tmask, h->d_counter, h->gm_V, h->gm_w,
-                  h->gm_ext, h->gm_u, h->gm_r, h->gm_part, h->gm_c, h->d_aT, h->d_tribuf,
-                  h->d_triws, h->d_z3, h->d_w3, h->d_j2ws, h->d_fptr_v, h->d_fptr_u, h->d_fpart, h->d_fws,
+                  h->gm_ext, h->gm_u, h->gm_r, h->gm_part, h->gm_c, h->d_aT,
                   h->d_bptr, h->d_tptr, h->d_brow, h->d_bcol, h->d_bdiag, h->d_terms,
                   h->d_vb[0], h->d_vb[1], h->d_ahb};
   for (void *p : ptrs)
@@ -2140,8 +1788,6 @@ extern "C" fastilu_status fastilu_destroy(fastilu_handle h) {
   if (h->h_r2) cudaFreeHost(h->h_r2);
   if (h->gm_hbuf) cudaFreeHost(h->gm_hbuf);
   for (auto *p : h->d_lmask) cudaFree(p);
-  for (auto *p : h->fpool_v) cudaFree(p);
-  for (auto *p : h->fpool_u) cudaFree(p);
   for (int i = 0; i < 6; i++)
     if (h->ev[i]) cudaEventDestroy(h->ev[i]);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);

@@ -16,6 +16,15 @@
 
 namespace fastilu {
 
+DeviceGuard::DeviceGuard(int device) {
+  if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+  if (device >= 0 && device != prev) cudaSetDevice(device);
+}
+DeviceGuard::~DeviceGuard() {
+  int cur = -1;
+  if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+}
+
 namespace {
 
 struct Api {
@@ -140,7 +149,7 @@ int jit_get(const std::string &src, const char *name, int device, void **fn, std
   std::vector<char> cubin(n);
   a.GetCUBIN(prog, cubin.data());
   a.DestroyProgram(&prog);
-  cudaSetDevice(device);
+  DeviceGuard dg_(device);
   cudaFree(nullptr);  // make sure the primary context is current
   CUmodule mod;
   if (a.ModuleLoadData(&mod, cubin.data()) != CUDA_SUCCESS) return 4;

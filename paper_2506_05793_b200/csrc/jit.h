@@ -4,6 +4,17 @@
 
 namespace fastilu {
 
+// RAII guard for the calling thread's current CUDA device: switches to `device` (if >= 0 and
+// different) and restores the caller's device on scope exit, so no ABI entry point leaves the
+// caller on another GPU.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int device);
+  ~DeviceGuard();
+  DeviceGuard(const DeviceGuard &) = delete;
+  DeviceGuard &operator=(const DeviceGuard &) = delete;
+};
+
 bool jit_available(std::string *why);
 // Compiles (cached per device and source) and returns the CUfunction `name`; 0 on success,
 // otherwise an error code with the NVRTC log in *log.

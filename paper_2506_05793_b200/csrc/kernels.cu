@@ -967,145 +967,5 @@ cudaError_t launch_axpby(double a, const double *x, double b, double *y, int64_t
   return cudaGetLastError();
 }
 
-// ----------------------------------------------------------------------------------------
-// Fused multi-sweep Jacobi trisolve on the template layout (single GPU).  Sweep t of row i reads
-// iterate t-1 of rows on ONE side of i only (j < i for L, j > i for U), so tiles of rows are
-// processed in dependency order (ascending for L, descending for U; acquired from a counter)
-// and each block runs all ntri sweeps of its tile, waiting before sweep t until the dep_tiles
-// tiles just before it (the rows its sweep reads: the template bandwidth) have finished sweep
-// t-1 -- every thread checks one completion flag, no sequential prefix chain.  Iterates live
-// in separate buffers buf[t-1] (extended length E), so nothing is overwritten early; the
-// factors of a tile are read from DRAM once and re-read from L1/L2 for the other sweeps.  The
-// arithmetic per row is the per-sweep kernel's (oracle order), so x is unchanged bitwise.
-// ----------------------------------------------------------------------------------------
-struct FusedTri {
-  int ntri, lower, final_x;
-  int64_t r0, r1, ntiles, E, Gh;
-  double omega;
-  const double *vals, *ud, *rhs, *s;
-  double *buf;        // ntri * E
-  double *xout;       // final output (lower: z in buf; upper & final_x: x = s o w)
-  unsigned int *counter;
-  unsigned char *flags;  // ntri * ntiles: tile finished sweep t
-  int dep_tiles;         // tiles a sweep of a tile depends on (before it in acquisition order)
-};
-
-// Block-wide wait until flags[ta-1], ..., flags[ta-dep] are all set (tiles < 0 count as set).
-__device__ __forceinline__ void wait_window(const unsigned char *flags, long long ta, int dep) {
-  for (int base = 0; base < dep; base += blockDim.x) {
-    const int q = base + (int)threadIdx.x;
-    const long long tt = ta - 1 - q;
-    const volatile unsigned char *fl = flags;
-    int ns = 32;
-    for (;;) {
-      const int ok = (q >= dep || tt < 0) ? 1 : (int)fl[tt];
-      if (__syncthreads_and(ok)) break;
-      __nanosleep(ns);
-      if (ns < 1024) ns *= 2;
-    }
-  }
-  __threadfence();
-}
-
-constexpr int kTriRows = 4;  // rows per thread of a fused-trisolve tile (1024-row tiles)
-
-__global__ void __launch_bounds__(256)
-tsell_trisolve_fused_kernel(TDev t, FusedTri f) {
-  __shared__ int32_t soff[128];
-  __shared__ long long s_tile;
-  for (int q = threadIdx.x; q < t.W; q += blockDim.x) soff[q] = t.off[q];
-  __syncthreads();
-  const int w0 = f.lower ? 0 : t.c0 + 1, w1 = f.lower ? t.c0 : t.W;
-  const int64_t tile_rows = (int64_t)blockDim.x * kTriRows;
-  for (;;) {
-    if (threadIdx.x == 0) s_tile = (long long)atomicAdd(f.counter, 1u);
-    __syncthreads();
-    const long long ta = s_tile;  // acquisition index = dependency order
-    __syncthreads();
-    if (ta >= f.ntiles) break;
-    const long long tile = f.lower ? ta : f.ntiles - 1 - ta;
-    for (int sw = 1; sw <= f.ntri; sw++) {
-      if (sw > 1) wait_window(f.flags + (int64_t)(sw - 2) * f.ntiles, ta, f.dep_tiles);
-      for (int rr = 0; rr < kTriRows; rr++) {
-        // upper solves walk their tile top-down too (rows above first), lower bottom-up
-        const int sub = f.lower ? rr : kTriRows - 1 - rr;
-        const int64_t i = f.r0 + tile * tile_rows + (int64_t)sub * blockDim.x + threadIdx.x;
-        if (i < f.r1) {
-          const int64_t sl = i >> 5, ln = i & 31;
-          unsigned long long m[2] = {0ull, 0ull};
-          for (int q = 0; q < t.words; q++) m[q] = t.mask[(sl * t.words + q) * 32 + ln];
-          const double *row = f.vals + sl * t.W * 32 + ln;
-          double acc = f.rhs[i], prev = 0.0;
-          if (sw > 1) {
-            const double *xo = f.buf + (int64_t)(sw - 2) * f.E;
-            for (int w = w0; w < w1; w++)
-              if (tbit(m, w)) acc = __dsub_rn(acc, __dmul_rn(row[w * 32], xo[i + soff[w]]));
-            prev = xo[i];
-          }
-          if (!f.lower) acc = __ddiv_rn(acc, f.ud[i]);
-          const double v = (f.omega == 1.0)
-                               ? acc
-                               : (sw == 1 ? __dmul_rn(f.omega, acc)
-                                          : __dadd_rn(__dmul_rn(1.0 - f.omega, prev),
-                                                      __dmul_rn(f.omega, acc)));
-          if (sw == f.ntri && f.final_x)
-            f.xout[i - f.Gh] = __dmul_rn(f.s[i], v);
-          else
-            f.buf[(int64_t)(sw - 1) * f.E + i] = v;
-        }
-      }
-      __threadfence();
-      __syncthreads();
-      if (threadIdx.x == 0)  // publish: this tile finished sweep sw
-        *(volatile unsigned char *)(f.flags + (int64_t)(sw - 1) * f.ntiles + ta) = 1;
-    }
-  }
-}
-
-cudaError_t launch_tsell_trisolve_fused(const TDev &t, bool lower, bool final_x, int ntri,
-                                        const double *vals, const double *ud, const double *rhs,
-                                        const double *s, double *buf, double *xout, int64_t r0,
-                                        int64_t r1, int64_t E, int64_t Gh, double omega,
-                                        int64_t bandwidth, unsigned int *sync_ws, int grid,
-                                        cudaStream_t st) {
-  if (r1 <= r0) return cudaSuccess;
-  const int threads = 256;
-  const int64_t tile_rows = (int64_t)threads * kTriRows;
-  const int64_t ntiles = (r1 - r0 + tile_rows - 1) / tile_rows;
-  // workspace: [counter (128 B)][flags ntri*ntiles bytes]
-  const size_t ws = 128 + (size_t)ntri * ntiles;
-  cudaError_t e = cudaMemsetAsync(sync_ws, 0, ws, st);
-  if (e != cudaSuccess) return e;
-  FusedTri f;
-  f.ntri = ntri;
-  f.lower = lower;
-  f.final_x = final_x;
-  f.r0 = r0;
-  f.r1 = r1;
-  f.ntiles = ntiles;
-  f.E = E;
-  f.Gh = Gh;
-  f.omega = omega;
-  f.vals = vals;
-  f.ud = ud;
-  f.rhs = rhs;
-  f.s = s;
-  f.buf = buf;
-  f.xout = xout;
-  f.counter = sync_ws;
-  f.flags = reinterpret_cast<unsigned char *>(sync_ws) + 128;
-  f.dep_tiles = (int)std::min<int64_t>(ntiles, (bandwidth + tile_rows - 1) / tile_rows + 1);
-  tsell_trisolve_fused_kernel<<<grid, threads, 0, st>>>(t, f);
-  return cudaGetLastError();
-}
-
-cudaError_t tsell_trisolve_occupancy(int *blocks_per_sm) {
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, tsell_trisolve_fused_kernel,
-                                                       256, 0);
-}
-
-size_t tsell_trisolve_ws_bytes(int ntri, int64_t rows) {
-  return 128 + (size_t)ntri * ((rows + 255) / 256) + 16;  // >= flags for kTriRows >= 1
-}
 
 }  // namespace fastilu

@@ -116,3 +116,29 @@ def test_bench_smem_port_bytes():
     assert abs(r["peak"] - 128 * 100 * 1000e6 / 1e9) < 1e-9
     assert abs(r["achieved"] - (r["lds_bytes"] + r["tma_bytes"]) / 1e-3 / 1e9) < 1e-6
     assert bench.smem_port("path=tsell W=7 terms=3", n, 1.0, 1000.0) is None
+
+
+def test_binding_argument_checks():
+    """The binding checks length, dtype, device and contiguity before any pointer reaches the C
+    side (which reads / writes a fixed count): ADVICE r1."""
+    import torch
+    v = F._host_in([1, 2, 3], 3, "v")
+    assert v.dtype == np.float64 and v.flags.c_contiguous
+    with pytest.raises(ValueError):
+        F._host_in(np.zeros(4), 3, "v")
+    with pytest.raises(ValueError):
+        F._host_in(np.zeros((3, 1)), 3, "v")
+    assert F._host_out(None, 5, "o").shape == (5,)
+    for bad in (np.zeros(5, dtype=np.float32), np.zeros(4), np.zeros(10)[::2],
+                np.zeros(5).reshape(5, 1)):
+        with pytest.raises(ValueError):
+            F._host_out(bad, 5, "o")
+    ro = np.zeros(5)
+    ro.flags.writeable = False
+    with pytest.raises(ValueError):
+        F._host_out(ro, 5, "o")
+    assert F._dev_arg(12345, 5, 0, "b") == 12345  # raw pointers pass through
+    with pytest.raises(ValueError):  # float32
+        F._dev_arg(torch.zeros(5, dtype=torch.float32), 5, 0, "b")
+    with pytest.raises(ValueError):  # not on a GPU
+        F._dev_arg(torch.zeros(5, dtype=torch.float64), 5, 0, "b")

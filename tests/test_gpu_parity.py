@@ -309,23 +309,6 @@ def test_async_quality_vs_synchronous():
     assert ra <= rs * 1.05, (ra, rs)
 
 
-@pytest.mark.parametrize("kind,g,k,ns,nt", [("27pt", 14, 1, 3, 5), ("27pt", 10, 2, 4, 3),
-                                             ("7pt", 24, 0, 2, 5), ("27pt", 9, 1, 1, 1)])
-def test_fused_wavefront_equals_per_sweep_kernels(kind, g, k, ns, nt, monkeypatch):
-    """The persistent wavefront kernels (all sweeps of compute / all Jacobi sweeps of apply in
-    one pass) compute exactly what the per-sweep kernels compute."""
-    a = P.make(kind, g)
-    b = P.rhs_positive(a.n)
-    monkeypatch.setenv("FASTILU_FUSED", "1")
-    _, v1, _, x1 = gpu_run(a, k, ns, nt, b)
-    monkeypatch.delenv("FASTILU_FUSED")
-    _, v2, _, x2 = gpu_run(a, k, ns, nt, b)
-    assert np.array_equal(v1, v2) and np.array_equal(x1, x2)
-    fo = oracle.compute(a, k, ns)
-    assert np.array_equal(v1, fo.vals)
-    assert np.array_equal(x1, oracle.apply(fo, b, nt))
-
-
 @pytest.mark.parametrize("kind,g,k,omega", [("27pt", 10, 1, 1.0), ("27pt", 9, 2, 0.7),
                                              ("7pt", 12, 1, 1.0)])
 def test_first_sweep_kernel_equals_full_sweep(kind, g, k, omega, monkeypatch):
@@ -369,16 +352,6 @@ _VARIANTS = [
     ("two part-warps per slice, 256-row tiles",
      {"FASTILU_TSELL_STAGED": "1", "FASTILU_TSELL_ST_PARTS": "2", "FASTILU_TSELL_ST_THREADS": "512"},
      None),
-    ("wavefront trisolve", {"FASTILU_JIT_TRISOLVE": "1"}, None),
-    ("paired Jacobi sweeps", {"FASTILU_JAC2": "1"}, None),
-    ("paired Jacobi sweeps, L1 gathers + L2 hints", {"FASTILU_JAC2": "1",
-                                                     "FASTILU_JAC2_MODE": "3"}, None),
-    ("paired Jacobi sweeps, lag 1 (flag waits taken)", {"FASTILU_JAC2": "1", "FASTILU_JAC2_LAG": "1",
-                                                        "FASTILU_JAC2_BPS": "2"}, None),
-    ("paired Jacobi sweeps, lag 5, one block per SM", {"FASTILU_JAC2": "1", "FASTILU_JAC2_LAG": "5",
-                                                       "FASTILU_JAC2_BPS": "1"}, None),
-    ("lagged 3-sweep trisolve", {"FASTILU_TRILAG": "1", "FASTILU_TRILAG_S": "3"}, None),
-    ("lagged 5-sweep trisolve", {"FASTILU_TRILAG": "1", "FASTILU_TRILAG_S": "5"}, None),
     ("divisions through __ddiv_rn", {"FASTILU_TSELL_STAGED": "1", "FASTILU_TSELL_ST_OPTS": "0"},
      "staged=1"),
 ]
