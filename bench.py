@@ -16,6 +16,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import re
 import statistics
 import subprocess
 import sys
@@ -288,6 +289,70 @@ def run_reference(args, wl):
     print(json.dumps(line), flush=True)
 
 
+def gmres_arms(args, f, a, ns, stream):
+    """BASELINE configs[4] (config 5): FastILU-preconditioned GMRES(60) to a 1e-6 relative
+    residual, x0 = 0, b = A x_true with x_true ~ U[0,1) (SURVEY 8(d) "Config 5
+    comparison arms").  Device-timed (CUDA events on the handle's stream), per ntri = 1..5:
+      A: FastILU factors (ns sweeps) + ntri Jacobi sweeps per apply   (compute + GMRES timed)
+      B: the factors at the sweep map's fixed point (compute_tol(1e-14): the exact ILU(0) up to
+         rounding, SURVEY 8(c) "Sweep map") + ntri Jacobi sweeps        (GMRES timed)
+    Arm C (the CPU oracle's exact ILU(0) + exact substitution) is part of the cpu_baseline leg."""
+    import torch
+    rows = np.repeat(np.arange(a.n), np.diff(a.row_ptr))
+    b = np.bincount(rows, weights=a.values * P.x_true(a.n)[a.col_idx], minlength=a.n)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    tb = torch.tensor(b, device=dev)
+    tx = torch.zeros_like(tb)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    out = {"restart": 60, "rtol": 1e-6, "nsweeps": ns, "arms": []}
+    nts = args.gmres_ntri
+    f.compute(ns)
+    f.gmres(tb, tx, 60, 1e-6, 20, 1)  # warm-up (JIT, workspace)
+    for nt in nts:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        f.compute(ns)
+        it, rr = f.gmres(tb, tx, 60, 1e-6, 5000, nt)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        out["arms"].append({"arm": "A", "ntri": nt, "iterations": it, "relres": rr,
+                            "time_to_solution_ms": e0.elapsed_time(e1)})
+    torch.cuda.synchronize()
+    e0.record(stream)
+    s_fix = f.compute_tol(1e-14, 5000)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    out["arm_B_factors"] = {"sweeps": s_fix, "ms": e0.elapsed_time(e1),
+                            "resid": float(f.residual_history()[-1])}
+    for nt in nts:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        it, rr = f.gmres(tb, tx, 60, 1e-6, 5000, nt)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        out["arms"].append({"arm": "B", "ntri": nt, "iterations": it, "relres": rr,
+                            "time_to_solution_ms": e0.elapsed_time(e1)})
+    return out, b
+
+
+def gmres_arm_c(a, b, cores):
+    """Arm C (cpu_baseline leg): the oracle's exact ILU(0) + exact substitution as the
+    preconditioner of the oracle's GMRES(60) (numpy), timed on the host."""
+    import oracle
+    used = oracle.set_threads(cores)
+    try:
+        t0 = time.perf_counter()
+        fe = oracle.compute(a, 0, 0)
+        fe.vals = oracle.exact_ilu(fe.pattern, fe.ahat)
+        t1 = time.perf_counter()
+        _, it, rr = oracle.gmres(a, b, oracle.exact_preconditioner(fe), 60, 1e-6, 5000)
+        t2 = time.perf_counter()
+    finally:
+        oracle.set_threads(1)
+    return {"arm": "C", "iterations": it, "relres": rr, "factor_s": t1 - t0, "gmres_s": t2 - t1,
+            "threads": used}
+
+
 def run_ours(args, wl):
     import torch
     import torch.distributed as dist
@@ -437,6 +502,11 @@ def run_ours(args, wl):
         cpu = {"value": r["value"], "unit": UNIT, "cores": r["threads"], "cpu": model,
                "kind": "oracle", "sample": r["sample"], "seconds": r["seconds"]}
 
+    gm = None
+    if kind == "aniso7pt" and world == 1 and not args.no_gmres:
+        gm, b_gm = gmres_arms(args, f, a, ns, stream)
+        if cpu is not None and args.arm_c:
+            cpu["gmres_arm_c"] = gmres_arm_c(a, b_gm, cpu["cores"])
     launches_per_step = 2 + 2 * ns + 2 * nt + (3 if info.startswith("path=bsr") else 0)
     # the full sweep kernel (sweeps 2..ns) against the measured copy bandwidth, on the bytes its
     # layout moves (no index bytes on the template path); the SURVEY 8(d) CSR model alongside
@@ -469,6 +539,9 @@ def run_ours(args, wl):
                        "nsweeps": ns, "ntrisweeps": nt, "tol": args.tol, "n": n, "nnz_A": nnz_A, "nnz_S": nnz_S,
                        "parallelism": (f"row-block z-slabs x{world}, NCCL halos"
                                        if world > 1 else "1gpu"),
+                       "comm": ({"nccl_ranks": world, "halo_bytes_per_sweep":
+                                 int(dict(re.findall(r"(\w+)=(\S+)", info)).get(
+                                     "halo_bytes", 0))} if world > 1 else None),
                        "global_grid": [g, g, g * world],
                        "l2": "working set >> 126 MB L2 (no flush needed)"},
             "sweep_nnz_updates_per_s": nnz_S * ns / (sweep_ms * 1e-3),
@@ -484,6 +557,7 @@ def run_ours(args, wl):
             "bytes_per_step": {"layout": composite, "survey_model": (
                 bm["B_init"] + ns * bm["B_f"] + bm["B_apply"]), "byte_model": lm["kind"]},
             "roofline": roof,
+            "gmres": gm,
             "clocks": clk, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
             "cpu_baseline": cpu,
             "setup_s": {"generate": t_gen, "create": t_setup},
@@ -507,6 +581,10 @@ def main():
     ap.add_argument("--cpu-planes", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-gmres", action="store_true", help="config 5: skip the GMRES arms")
+    ap.add_argument("--arm-c", action="store_true",
+                    help="config 5: add arm C (CPU oracle exact ILU(0) + substitution; minutes)")
+    ap.add_argument("--gmres-ntri", type=int, nargs="+", default=[1, 2, 3, 4, 5])
     ap.add_argument("--tol", type=float, default=None,
                     help="sweeps to convergence: stop at r(s-1) <= tol ||Ahat|_S||_F (config 3)")
     args = ap.parse_args()

@@ -175,6 +175,16 @@ fastilu_status fastilu_gmres(fastilu_handle h, const double *b, double *x, int r
                              double rtol, int max_iters, int ntrisweeps, int *iters,
                              double *relres);
 
+/* Loads EXTERNAL factors instead of computing them (config 5 arm B: e.g. the exact ILU(k) of Ahat,
+ * to isolate the factor-sweep error from the trisolve's; BASELINE.json configs[4], SURVEY.md
+ * Sec. 8(d) "Config 5 comparison arms").  vals: HOST array of the owned rows' S entries in S row
+ * order (the layout fastilu_get_factors returns: l_ij below the diagonal, u_ij on and above it);
+ * s: HOST array of the n scaling factors (apply returns x = s o U^-1 L^-1 (s o b), reading R5).
+ * The pattern is the handle's (create); the caller keeps ownership of both arrays.  Afterwards
+ * apply / gmres use these factors until the next compute.  Errors: INVALID_ARG (NULL arrays),
+ * ZERO_PIVOT (a u_ii that is 0 or non-finite; index = first such global row).  Synchronises. */
+fastilu_status fastilu_set_factors(fastilu_handle h, const double *vals, const double *s);
+
 /* Frees everything; fastilu_destroy(NULL) is a no-op. */
 fastilu_status fastilu_destroy(fastilu_handle h);
 

@@ -70,6 +70,7 @@ _SIGS = {
     "fastilu_get_device": (C.c_int, [H, C.POINTER(C.c_int)]),
     "fastilu_get_pattern": (C.c_int, [H, I64P, I32P, I8P]),
     "fastilu_get_factors": (C.c_int, [H, F64P, F64P]),
+    "fastilu_set_factors": (C.c_int, [H, F64P, F64P]),
     "fastilu_get_residual_history": (C.c_int, [H, F64P, C.c_int, C.POINTER(C.c_int)]),
     "fastilu_get_timings": (C.c_int, [H, F64P]),
     "fastilu_get_sweep_split": (C.c_int, [H, F64P]),
@@ -378,6 +379,14 @@ class FastILU:
         _check(lib().fastilu_get_factors(self._h, _p(v, F64P), _p(s, F64P)),
                "fastilu_get_factors", self._h)
         return v[:self.nnz_S], s[:self.n]
+
+    def set_factors(self, vals, s):
+        """fastilu_set_factors: external factors (S row order of the owned rows, as factors()
+        returns them) and scaling vector s; apply / gmres then use them (config 5 arm B)."""
+        v = _host_in(vals, self.nnz_S, "vals")
+        sv = _host_in(s, self.n, "s")
+        _check(lib().fastilu_set_factors(self._h, _p(v, F64P), _p(sv, F64P)),
+               "fastilu_set_factors", self._h)
 
     def residual_history(self, cap: int = 4096):
         h = np.empty(cap)

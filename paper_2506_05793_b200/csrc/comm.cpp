@@ -128,6 +128,11 @@ struct Comm {
   int64_t *d_scratch = nullptr;  // NCCL setup / reductions
   size_t scratch_elems = 0;
   cudaStream_t host_stream = nullptr;  // host-side reductions (created once, NCCL only)
+  // packed factor halo (template layout), overlapped with the interior sweep
+  cudaStream_t halo_stream = nullptr;
+  cudaEvent_t ev_src = nullptr, ev_halo = nullptr;
+  double *d_hsend = nullptr, *d_hrecv = nullptr;
+  int64_t hsend_cap = 0, hrecv_cap = 0;
 };
 
 #define CUC(x)                                                    \
@@ -196,6 +201,9 @@ fastilu_status comm_init(Comm *&out, const fastilu_options &o, cudaStream_t st) 
   }
   CUC(cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming));
   CUC(cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming));
+  CUC(cudaEventCreateWithFlags(&c->ev_src, cudaEventDisableTiming));
+  CUC(cudaEventCreateWithFlags(&c->ev_halo, cudaEventDisableTiming));
+  CUC(cudaStreamCreateWithFlags(&c->halo_stream, cudaStreamNonBlocking));
   (void)st;
   return FASTILU_OK;
 }
@@ -333,6 +341,17 @@ fastilu_status comm_vector_halo(Comm *c, double *x, cudaStream_t st, bool lower,
   return exchange(c, sends, recvs, st);
 }
 
+fastilu_status comm_vector_halo_async(Comm *c, double *x, cudaStream_t st, bool lower,
+                                      bool upper, cudaEvent_t *done) {
+  CUC(cudaEventRecord(c->ev_src, st));
+  CUC(cudaStreamWaitEvent(c->halo_stream, c->ev_src, 0));
+  fastilu_status s = comm_vector_halo(c, x, c->halo_stream, lower, upper);
+  if (s) return s;
+  CUC(cudaEventRecord(c->ev_halo, c->halo_stream));
+  *done = c->ev_halo;
+  return FASTILU_OK;
+}
+
 fastilu_status comm_factor_halo(Comm *c, double *vals, const int64_t *, double *udiag,
                                 cudaStream_t st) {
   const int P = c->nranks, p = c->rank;
@@ -356,6 +375,49 @@ fastilu_status comm_factor_halo(Comm *c, double *vals, const int64_t *, double *
     return exchange(c, s2, r2, st);
   }
   return exchange(c, sends, recvs, st);
+}
+
+fastilu_status comm_factor_halo_upper(Comm *c, double *vals, double *udiag, int W, int c0,
+                                      cudaStream_t st, cudaEvent_t *done) {
+  const int P = c->nranks, p = c->rank;
+  const int64_t NC = W - c0;
+  const int64_t gn = (p + 1 < P) ? c->GG[p + 1] : 0;  // owned rows rank p+1 keeps as ghosts
+  if ((gn % 32) || (c->G % 32)) FAIL(FASTILU_ERR_UNSUPPORTED);
+  const int64_t ns_send = gn / 32, ns_recv = c->G / 32;
+  const int64_t cnt_send = ns_send * NC * 32, cnt_recv = ns_recv * NC * 32;
+  if (cnt_send > c->hsend_cap) {
+    if (c->d_hsend) cudaFree(c->d_hsend);
+    c->d_hsend = nullptr;
+    CUC(cudaMalloc((void **)&c->d_hsend, sizeof(double) * cnt_send));
+    c->hsend_cap = cnt_send;
+  }
+  if (cnt_recv > c->hrecv_cap) {
+    if (c->d_hrecv) cudaFree(c->d_hrecv);
+    c->d_hrecv = nullptr;
+    CUC(cudaMalloc((void **)&c->d_hrecv, sizeof(double) * cnt_recv));
+    c->hrecv_cap = cnt_recv;
+  }
+  cudaStream_t hs = c->halo_stream;
+  // the iterate is complete on the compute stream before it is packed
+  CUC(cudaEventRecord(c->ev_src, st));
+  CUC(cudaStreamWaitEvent(hs, c->ev_src, 0));
+  if (ns_send)
+    CUC(launch_tsell_pack_upper(vals, (c->G + c->n - gn) / 32, ns_send, W, c0, c->d_hsend, hs));
+  std::vector<Xfer> sends, recvs;
+  if (p + 1 < P) sends.push_back({c->d_hsend, nullptr, cnt_send, p + 1});
+  if (p > 0) recvs.push_back({nullptr, c->d_hrecv, cnt_recv, p - 1});
+  fastilu_status s = exchange(c, sends, recvs, hs);
+  if (s) return s;
+  if (ns_recv) CUC(launch_tsell_unpack_upper(c->d_hrecv, 0, ns_recv, W, c0, vals, udiag, hs));
+  CUC(cudaEventRecord(c->ev_halo, hs));
+  *done = c->ev_halo;
+  return FASTILU_OK;
+}
+
+int64_t comm_halo_bytes(const Comm *c, int W, int c0) {
+  const int P = c->nranks, p = c->rank;
+  const int64_t gn = (p + 1 < P) ? c->GG[p + 1] : 0;
+  return W > 0 ? gn * (int64_t)(W - c0) * 8 : c->send_cnt * 8;
 }
 
 fastilu_status comm_allreduce_host(Comm *c, double *r2, int count, ErrFlags &ef) {
@@ -409,6 +471,11 @@ void comm_destroy(Comm *c) {
   if (c->ev_done) cudaEventDestroy(c->ev_done);
   if (c->d_scratch) cudaFree(c->d_scratch);
   if (c->host_stream) cudaStreamDestroy(c->host_stream);
+  if (c->halo_stream) cudaStreamDestroy(c->halo_stream);
+  if (c->ev_src) cudaEventDestroy(c->ev_src);
+  if (c->ev_halo) cudaEventDestroy(c->ev_halo);
+  if (c->d_hsend) cudaFree(c->d_hsend);
+  if (c->d_hrecv) cudaFree(c->d_hrecv);
   delete c;
 }
 

@@ -27,11 +27,25 @@ fastilu_status comm_layout(Comm *c, int64_t row_begin, int64_t n, int64_t G, int
 // Vector halo on an extended vector [G | n | H]: lower ghosts from rank-1's last G owned
 // entries, upper ghosts from rank+1's first H owned entries.
 fastilu_status comm_vector_halo(Comm *c, double *x, cudaStream_t st, bool lower, bool upper);
+// The same on the comm's halo stream, after `st`'s work so far; *done marks the ghosts in place
+// (the caller overlaps the rows that read no ghost entry).
+fastilu_status comm_vector_halo_async(Comm *c, double *x, cudaStream_t st, bool lower,
+                                      bool upper, cudaEvent_t *done);
 // Factor halo before a sweep: the G ghost rows' values (whole rows: CSR S order, or whole
 // 32-row template slices when tsell_W > 0) and their
 // diagonal copies from rank-1.
 fastilu_status comm_factor_halo(Comm *c, double *vals, const int64_t *d_rp, double *udiag,
                                 cudaStream_t st);
+// Template layout: the factor halo of a sweep restricted to what the sweep kernels read from a
+// ghost row -- columns [c0, W) (diagonal + strict upper part) -- packed into one contiguous
+// message per neighbour (about half of whole rows), on the comm's own halo stream after the
+// iterate is complete on `st`; unpacked into the ghost slices (+ udiag).  *done is recorded on
+// the halo stream when the ghost rows are in place: the caller sweeps the rows that read no
+// ghost row meanwhile and waits on *done before the others.
+fastilu_status comm_factor_halo_upper(Comm *c, double *vals, double *udiag, int W, int c0,
+                                      cudaStream_t st, cudaEvent_t *done);
+// bytes this rank sends per factor halo (template: packed columns; CSR: whole rows)
+int64_t comm_halo_bytes(const Comm *c, int W, int c0);
 // Host-side sum of the residual history and min of the (GLOBAL-index) error flags over ranks.
 fastilu_status comm_allreduce_host(Comm *c, double *r2, int count, ErrFlags &ef);
 void comm_destroy(Comm *c);

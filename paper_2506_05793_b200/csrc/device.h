@@ -109,6 +109,12 @@ struct TDev {
 cudaError_t launch_tsell_gather_a(const TDev &t, const double *aval, int64_t nrows, double *aT,
                                   cudaStream_t st);
 // same for local rows [r0, r1) only
+// multi-GPU factor halo (template layout): columns [c0, W) of nslices slices from slice0 into a
+// contiguous buffer, and back into the ghost slices (+ the compact diagonal copy udiag)
+cudaError_t launch_tsell_pack_upper(const double *vals, int64_t slice0, int64_t nslices, int W,
+                                    int c0, double *buf, cudaStream_t st);
+cudaError_t launch_tsell_unpack_upper(const double *buf, int64_t slice0, int64_t nslices, int W,
+                                      int c0, double *vals, double *udiag, cudaStream_t st);
 cudaError_t launch_tsell_gather_a_range(const TDev &t, const double *aval, int64_t r0,
                                         int64_t r1, double *aT, cudaStream_t st);
 cudaError_t launch_tsell_init(const TDev &t, const double *aT, const double *s,

@@ -431,6 +431,7 @@ static fastilu_status setup_tsell(fastilu_handle h, const std::vector<unsigned l
           sweep_source_staged(T, sthreads, sparts, nst, sminb, false, &c, sopts);
       const std::string s1 =
           sweep_source_staged(T, sthreads, sparts, nst, sminb, true, nullptr, sopts);
+      if (std::getenv("FASTILU_DUMP_SRC")) fprintf(stderr, "%s\n", s0.c_str());
       int sbps = 0;
       if (!jit_get(s0, "fastilu_tsell_sweep_st", h->device, &h->jit_st, &log) &&
           !jit_get(s1, "fastilu_tsell_sweep_st_first", h->device, &h->jit_st_first, &log) &&
@@ -539,9 +540,9 @@ static fastilu_status setup_tsell(fastilu_handle h, const std::vector<unsigned l
   CU(dalloc(&h->d_toff, T.W));
   CU(dalloc(&h->d_toffA, T.WA));
   CU(dalloc(&h->d_tw2a, T.W));
-  CU(dalloc(&h->d_counter, 1));
-  CU(dalloc(&h->d_partials,
-            std::max<int64_t>(std::max(std::max(h->t_ntiles, h->st_ntiles), h->st_init_ntiles),
+  CU(dalloc(&h->d_counter, 2));  // [1]: second launch of a split (halo-overlapped) sweep
+  CU(dalloc(&h->d_partials,  // +2: a split sweep has one partial tile per launch more
+            std::max<int64_t>(std::max(std::max(h->t_ntiles, h->st_ntiles), h->st_init_ntiles) + 2,
                               kSumsqBlocks)));
   if (h->jit_st)
     for (int b = 0; b < 2; b++)
@@ -562,7 +563,7 @@ static fastilu_status setup_tsell(fastilu_handle h, const std::vector<unsigned l
   if (h->jit_st_init && jit_tmap_sell(h->st_tmap_own_ahat.b, h->d_ahat, T.WA, h->nsl,
                                       std::max(1, h->st_init.own_cols), h->st_init.rows / 32))
     h->jit_st_init = nullptr;
-  CU(cudaMemset(h->d_counter, 0, sizeof(unsigned int)));
+  CU(cudaMemset(h->d_counter, 0, 2 * sizeof(unsigned int)));
   CU(cudaMemcpy(h->d_tmask, mask.data(), 8 * mask.size(), cudaMemcpyHostToDevice));
   CU(cudaMemcpy(h->d_tasrc, asrc.data(), 4 * asrc.size(), cudaMemcpyHostToDevice));
   CU(cudaMemcpy(h->d_toff, T.off.data(), 4 * T.W, cudaMemcpyHostToDevice));
@@ -1062,54 +1063,92 @@ static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, i
       }
     }
     const int ib = async ? ib_async : (sw - 1) & 1, ob = async ? ib_async : sw & 1;
+    // multi-GPU template path: the factor halo (diagonal + strict-upper columns of the ghost
+    // rows, packed) flies on the comm stream while the rows that read no ghost row are swept;
+    // the first `bnd` owned rows (pivot rows reach below them into the ghosts) follow
+    cudaEvent_t halo_done = nullptr;
+    int64_t bnd = 0;
     if (h->comm && !(sw == 1 && fuse_init)) {  // fused sweep 1 reads no stored iterate 0
-      fastilu_status cs = comm_factor_halo(h->comm, h->d_vals[ib], h->d_rp, h->d_ud[ib], st);
+      fastilu_status cs =
+          h->tsell ? comm_factor_halo_upper(h->comm, h->d_vals[ib], h->d_ud[ib], h->T.W,
+                                            h->T.c0, st, &halo_done)
+                   : comm_factor_halo(h->comm, h->d_vals[ib], h->d_rp, h->d_ud[ib], st);
       if (cs) return cs;
+      if (halo_done) {
+        bnd = std::min<int64_t>(h->n, (-(int64_t)h->T.off[0] + 31) / 32 * 32);
+        if (std::getenv("FASTILU_NO_HALO_OVERLAP")) bnd = h->n;
+      }
     }
     SweepArgs sa{P,           h->d_arp,      h->d_apos,     h->d_ahat, h->d_vals[ib],
                  h->d_vals[ob], h->d_ud[ib], h->d_ud[ob], r0,        r1,
                  h->opt.omega,  h->d_partials, h->d_err};
     if (h->tsell) {
       const double *old = h->d_vals[ib], *ahat = h->d_ahat, *udo = h->d_ud[ib];
-      double *outp = h->d_vals[ob], *udn = h->d_ud[ob], *part = h->d_partials;
+      double *outp = h->d_vals[ob], *udn = h->d_ud[ob];
       const unsigned long long *mk = h->d_tmask;
       if (warmup && per_level > 0) {
         const int lvl = (sw - 1) / per_level;
         if (lvl < h->K) mk = h->d_lmask[lvl];
       }
-      long long a0 = r0, a1 = r1;
       double om = h->opt.omega;
       unsigned long long *zp = &h->d_err->zero_pivot;
-      unsigned int *ctr = h->d_counter;
       int sstr = h->t_sstride;
-      if (h->jit_st && !async) {
-        void *sargs[] = {&old, &outp, &ahat, &mk, &udn, &a0, &a1, &om, &part, &zp, &ctr,
-                         h->st_tmap[ib].b, h->st_tmap_own[ib].b};
-        void *fn = (sw == 1 && !warmup && h->jit_st_first) ? h->jit_st_first : h->jit_st;
-        int smem = h->st.smem, grid = h->st_grid, thr = h->st.threads;
-        int64_t ntl = h->st_ntiles;
+      const bool staged = h->jit_st && !async;
+      void *fn = nullptr;
+      int smem = 0, grid = 0, thr = 0;
+      int64_t rows_tile = 0;
+      void *tm0 = nullptr, *tm1 = nullptr;
+      if (staged) {
+        fn = (sw == 1 && !warmup && h->jit_st_first) ? h->jit_st_first : h->jit_st;
+        smem = h->st.smem, grid = h->st_grid, thr = h->st.threads, rows_tile = h->st.rows;
+        tm0 = h->st_tmap[ib].b, tm1 = h->st_tmap_own[ib].b;
         if (sw == 1 && fuse_init) {
           fn = h->jit_st_init;
-          smem = h->st_init.smem;
-          grid = h->st_init_grid;
-          thr = h->st_init.threads;
-          ntl = h->st_init_ntiles;
-          sargs[11] = h->st_tmap_ahat.b;
-          sargs[12] = h->st_tmap_own_ahat.b;
+          smem = h->st_init.smem, grid = h->st_init_grid, thr = h->st_init.threads;
+          rows_tile = h->st_init.rows;
+          tm0 = h->st_tmap_ahat.b, tm1 = h->st_tmap_own_ahat.b;
         }
-        if (jit_launch_smem(fn, grid, thr, smem, st, sargs)) return FASTILU_ERR_CUDA;
-        CU(launch_reduce_reset(h->d_partials, (int)ntl, h->d_r2 + (sw - 1), h->d_counter, st));
+      } else {
+        fn = async ? h->jit_sweep_async
+             : (sw == 1 && !warmup && h->jit_sweep_first) ? h->jit_sweep_first
+                                                          : h->jit_sweep;
+        grid = h->t_grid, thr = h->t_threads;
+      }
+      // one launch over local rows [a0, a1) with its own tile counter and partials; returns the
+      // number of tiles (partials written) or -1
+      auto sweep_range = [&](int64_t b0, int64_t b1, unsigned int *ctr, double *part) -> int64_t {
+        if (b1 <= b0) return 0;
+        long long a0 = b0, a1 = b1;
+        int64_t ntl;
+        if (staged) {
+          ntl = (b1 - b0 + rows_tile - 1) / rows_tile;
+          void *sargs[] = {&old, &outp, &ahat, &mk, &udn, &a0, &a1, &om, &part, &zp, &ctr,
+                           tm0, tm1};
+          if (jit_launch_smem(fn, (int)std::min<int64_t>(grid, ntl), thr, smem, st, sargs))
+            return -1;
+        } else {
+          const int64_t spt = h->t_rows_tile / 32, ss = h->t_sstride;
+          ntl = ((b1 - b0 + 31) / 32 + spt * ss - 1) / (spt * ss) * ss;
+          void *args[] = {&old, &outp, &ahat, &mk, &udo, &udn, &a0, &a1, &om, &part, &zp, &ctr,
+                          &sstr};
+          if (jit_launch(fn, (int)std::min<int64_t>(grid, ntl), thr, st, args)) return -1;
+        }
+        return ntl;
+      };
+      if (!halo_done) {
+        const int64_t nt = sweep_range(r0, r1, h->d_counter, h->d_partials);
+        if (nt < 0) return FASTILU_ERR_CUDA;
+        CU(launch_reduce_reset(h->d_partials, (int)nt, h->d_r2 + (sw - 1), h->d_counter, st));
         continue;
       }
-      void *args[] = {&old, &outp, &ahat, &mk, &udo, &udn, &a0, &a1, &om, &part, &zp, &ctr, &sstr};
-      void *fn = async ? h->jit_sweep_async
-                 : (sw == 1 && !warmup && h->jit_sweep_first) ? h->jit_sweep_first
-                                                              : h->jit_sweep;
-      if (jit_launch(fn, h->t_grid, h->t_threads, st,
-                     args))
-        return FASTILU_ERR_CUDA;
-      CU(launch_reduce_reset(h->d_partials, (int)h->t_ntiles, h->d_r2 + (sw - 1), h->d_counter,
+      const int64_t nt1 = sweep_range(r0 + bnd, r1, h->d_counter, h->d_partials);
+      if (nt1 < 0) return FASTILU_ERR_CUDA;
+      CU(cudaStreamWaitEvent(st, halo_done, 0));
+      const int64_t nt2 = sweep_range(r0, r0 + bnd, h->d_counter + 1, h->d_partials + nt1);
+      if (nt2 < 0) return FASTILU_ERR_CUDA;
+      CU(launch_reduce_reset(h->d_partials, (int)(nt1 + nt2), h->d_r2 + (sw - 1), h->d_counter,
                              st));
+      CU(cudaMemsetAsync(h->d_counter + 1, 0, sizeof(unsigned int), st));
       continue;
     }
     if (h->bsr) {
@@ -1429,6 +1468,44 @@ static fastilu_status apply_impl(fastilu_handle h, const double *b, double *x, i
   const double *ud = h->ud_cur;
   // a8: L sweeps.  t = 1: z1 = w y with y = s o b (z0 = 0)
   CU(launch_trisolve_first_L(b, h->d_s, h->d_y, h->d_z[0], r0, r1, h->G, om, st));
+  // multi-GPU template path: the vector halo of a sweep flies on the comm's halo stream while
+  // the rows that read no ghost entry are swept (L: the first -o_0 owned rows read the lower
+  // ghosts; U: the last o_{W-1} read the upper ones)
+  const bool ovl = h->comm && h->tsell && h->jit_jac[0] && h->jit_jac[1] &&
+                   !std::getenv("FASTILU_NO_HALO_OVERLAP");
+  if (ovl) {
+    const int64_t bl = std::min<int64_t>(h->n, -(int64_t)h->T.off[0]);
+    const int64_t bu = std::min<int64_t>(h->n, (int64_t)h->T.off[h->T.W - 1]);
+    for (int t = 2; t <= ntri; t++) {
+      const double *zo = h->d_z[(t - 2) & 1];
+      double *zn = h->d_z[(t - 1) & 1];
+      cudaEvent_t done = nullptr;
+      fastilu_status cs =
+          comm_vector_halo_async(h->comm, h->d_z[(t - 2) & 1], st, true, false, &done);
+      if (cs) return cs;
+      if (jit_jacobi(h, true, vals, nullptr, h->d_y, zo, zn, nullptr, r0 + bl, r1, 0, om, false))
+        FAIL(FASTILU_ERR_CUDA);
+      CU(cudaStreamWaitEvent(st, done, 0));
+      if (jit_jacobi(h, true, vals, nullptr, h->d_y, zo, zn, nullptr, r0, r0 + bl, 0, om, false))
+        FAIL(FASTILU_ERR_CUDA);
+    }
+    const double *zf = h->d_z[(ntri - 1) & 1];
+    CU(launch_trisolve_first_U(zf, ud, h->d_s, h->d_w[0], x, r0, r1, h->G, om, ntri == 1, st));
+    for (int t = 2; t <= ntri; t++) {
+      const double *wo = h->d_w[(t - 2) & 1];
+      double *wn = h->d_w[(t - 1) & 1];
+      cudaEvent_t done = nullptr;
+      fastilu_status cs =
+          comm_vector_halo_async(h->comm, h->d_w[(t - 2) & 1], st, false, true, &done);
+      if (cs) return cs;
+      if (jit_jacobi(h, false, vals, ud, zf, wo, wn, x, r0, r1 - bu, h->G, om, t == ntri))
+        FAIL(FASTILU_ERR_CUDA);
+      CU(cudaStreamWaitEvent(st, done, 0));
+      if (jit_jacobi(h, false, vals, ud, zf, wo, wn, x, r1 - bu, r1, h->G, om, t == ntri))
+        FAIL(FASTILU_ERR_CUDA);
+    }
+    return FASTILU_OK;
+  }
   for (int t = 2; t <= ntri; t++) {
     const double *zo = h->d_z[(t - 2) & 1];
     if (h->comm) {
@@ -1700,6 +1777,54 @@ extern "C" fastilu_status fastilu_get_factors(fastilu_handle h, double *vals, do
   return FASTILU_OK;
 }
 
+extern "C" fastilu_status fastilu_set_factors(fastilu_handle h, const double *vals,
+                                              const double *s) {
+  if (!h || (h->nnz_own > 0 && !vals) || (h->n > 0 && !s)) FAIL(FASTILU_ERR_INVALID_ARG);
+  if (h->bsr && !h->d_vals[0]) FAIL(FASTILU_ERR_UNSUPPORTED);
+  DeviceGuard dg_(h->device);
+  (void)cudaGetLastError();
+  CU(cudaStreamSynchronize(h->stream));
+  h->computed = false;
+  h->err_index = -1;
+  // u_ii of the owned rows (local index G + r), zero-pivot check
+  std::vector<double> ud((size_t)h->E, 0.0);
+  for (int64_t r = 0; r < h->n; r++) {
+    const int64_t g = h->row_begin + r;
+    double d = 0.0;
+    for (int64_t p = h->h_rp[r]; p < h->h_rp[r + 1]; p++)
+      if (h->h_ci[p] == g) d = vals[p];
+    if (!(d != 0.0 && std::fabs(d) <= 1.7976931348623157e308)) {
+      h->err_index = g;
+      return FASTILU_ERR_ZERO_PIVOT;
+    }
+    ud[(size_t)(h->G + r)] = d;
+  }
+  if (h->tsell) {  // scatter into the template slots (absent / ghost slots +0.0)
+    const Template &T = h->T;
+    std::vector<double> tv((size_t)h->nsl * T.W * 32, 0.0);
+    for (int64_t r = 0; r < h->n; r++) {
+      const int64_t i = h->G + r, g = h->row_begin + r;
+      for (int64_t p = h->h_rp[r]; p < h->h_rp[r + 1]; p++) {
+        const int32_t o = (int32_t)(h->h_ci[p] - g);
+        const int w = (int)(std::lower_bound(T.off.begin(), T.off.end(), o) - T.off.begin());
+        tv[((i >> 5) * T.W + w) * 32 + (i & 31)] = vals[p];
+      }
+    }
+    CU(cudaMemcpy(h->d_vals[0], tv.data(), sizeof(double) * tv.size(), cudaMemcpyHostToDevice));
+  } else {
+    CU(cudaMemcpy(h->d_vals[0] + h->own_off, vals, sizeof(double) * h->nnz_own,
+                  cudaMemcpyHostToDevice));
+  }
+  CU(cudaMemcpy(h->d_ud[0], ud.data(), sizeof(double) * ud.size(), cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(h->d_s + h->G, s, sizeof(double) * h->n, cudaMemcpyHostToDevice));
+  h->cur = 0;
+  h->vals_cur = h->d_vals[0];
+  h->ud_cur = h->d_ud[0];
+  h->resid.clear();
+  h->computed = true;
+  return FASTILU_OK;
+}
+
 extern "C" fastilu_status fastilu_get_residual_history(fastilu_handle h, double *hist, int cap,
                                                        int *count) {
   if (!h) FAIL(FASTILU_ERR_INVALID_ARG);
@@ -1764,6 +1889,11 @@ extern "C" fastilu_status fastilu_get_info(fastilu_handle h, char *buf, int cap)
              h->scfg.prog ? "csr-classes" : (h->scfg.hash ? "csr-hash" : "csr-bsearch"),
              h->scfg.G, h->scfg.E, h->scfg.threads, h->scfg.grid, (long long)h->nclasses,
              h->G_tri, (long long)h->G, (long long)h->H);
+  if (h->comm) {  // multi-GPU: ranks and the bytes this rank sends per factor halo
+    const size_t L = strlen(tmp);
+    snprintf(tmp + L, sizeof(tmp) - L, " nranks=%d halo_bytes=%lld", h->opt.nranks,
+             (long long)comm_halo_bytes(h->comm, h->tsell ? h->T.W : 0, h->tsell ? h->T.c0 : 0));
+  }
   snprintf(buf, cap, "%s", tmp);
   return FASTILU_OK;
 }

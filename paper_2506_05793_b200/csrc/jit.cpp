@@ -171,6 +171,13 @@ int jit_launch(void *fn, int grid, int block, void *stream, void **args) {
 int jit_set_smem(void *fn, int bytes) {
   Api &a = api();
   if (!a.FuncSetAttribute) return 1;
+  // a request above the opt-in limit is a configuration that does not fit: report it without
+  // issuing the failing driver call
+  int dev = 0, mx = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess &&
+      cudaDeviceGetAttribute(&mx, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) == cudaSuccess &&
+      bytes > mx)
+    return 3;
   return a.FuncSetAttribute((CUfunction)fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
                             bytes) == CUDA_SUCCESS
              ? 0

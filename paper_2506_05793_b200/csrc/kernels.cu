@@ -669,6 +669,53 @@ tsell_gather_a_kernel(TDev t, const double *__restrict__ aval, int64_t r0, int64
   }
 }
 
+// Multi-GPU factor halo on the template layout: only the columns [c0, W) of
+// a ghost row -- its diagonal and strict-upper part -- are read by the sweep kernels (pivot rows
+// u_kj, divisor u_jj), so the halo moves those, packed slice by slice: buf[(s NC + c) 32 + l] =
+// vals[((slice0 + s) W + c0 + c) 32 + l], NC = W - c0 (coalesced both ways).
+__global__ void tsell_pack_upper_kernel(const double *__restrict__ vals, int64_t slice0,
+                                        int64_t total, int W, int c0, double *__restrict__ buf) {
+  const int64_t per = (int64_t)(W - c0) * 32;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = q / per, rem = q - s * per;
+    buf[q] = vals[(slice0 + s) * W * 32 + (int64_t)c0 * 32 + rem];
+  }
+}
+
+// inverse of the pack into the ghost slices; column c0 also refreshes the compact diagonal copy
+// (udiag, read by the register-pivot kernels)
+__global__ void tsell_unpack_upper_kernel(const double *__restrict__ buf, int64_t slice0,
+                                          int64_t total, int W, int c0, double *__restrict__ vals,
+                                          double *__restrict__ udiag) {
+  const int64_t per = (int64_t)(W - c0) * 32;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = q / per, rem = q - s * per;
+    const double v = buf[q];
+    vals[(slice0 + s) * W * 32 + (int64_t)c0 * 32 + rem] = v;
+    if (rem < 32) udiag[(slice0 + s) * 32 + rem] = v;
+  }
+}
+
+cudaError_t launch_tsell_pack_upper(const double *vals, int64_t slice0, int64_t nslices, int W,
+                                    int c0, double *buf, cudaStream_t st) {
+  const int64_t total = nslices * (int64_t)(W - c0) * 32;
+  if (total <= 0) return cudaSuccess;
+  tsell_pack_upper_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, 4096), 256, 0, st>>>(
+      vals, slice0, total, W, c0, buf);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tsell_unpack_upper(const double *buf, int64_t slice0, int64_t nslices, int W,
+                                      int c0, double *vals, double *udiag, cudaStream_t st) {
+  const int64_t total = nslices * (int64_t)(W - c0) * 32;
+  if (total <= 0) return cudaSuccess;
+  tsell_unpack_upper_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, 4096), 256, 0,
+                              st>>>(buf, slice0, total, W, c0, vals, udiag);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_tsell_gather_a(const TDev &t, const double *aval, int64_t nrows, double *aT,
                                   cudaStream_t st) {
   return launch_tsell_gather_a_range(t, aval, 0, nrows, aT, st);

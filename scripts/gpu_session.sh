@@ -33,7 +33,7 @@ for step in "$@"; do
         timeout 300 python bench.py --workload $w --tol 1e-10 --steps 5 --warmup 3 --no-e2e
       done > gpurun_out/${TAG}_tol.log 2>&1 ;;
     c5)
-      timeout 1200 python bench.py --workload c5_aniso7pt_256_ilu0 --steps 3 --warmup 3 \
+      timeout 1500 python bench.py --workload c5_aniso7pt_256_ilu0 --steps 5 --warmup 3 --arm-c \
         > gpurun_out/${TAG}_c5.log 2>&1 ;;
     launches)
       timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \

@@ -42,3 +42,46 @@ def test_gmres_27pt_ilu1_restarts():
     fo = oracle.compute(a, 1, 3)
     _, it_o, rr_o = oracle.gmres(a, b, oracle.fastilu_preconditioner(fo, 3), 5, 1e-9, 500)
     assert rr <= 1e-9 and abs(it - it_o) <= 1, (it, it_o)
+
+
+@pytest.mark.parametrize("path", ["tsell", "csr"])
+def test_set_factors_arm_b(path, monkeypatch):
+    """Config 5 arm B: the oracle's EXACT ILU(0) factors uploaded with fastilu_set_factors; the
+    GPU Jacobi apply of them equals the oracle's apply of the same factors bitwise, and GMRES
+    with them needs no more iterations than the 2-sweep FastILU factors (arm A) and matches the
+    oracle's GMRES with the same preconditioner (+-1)."""
+    if path == "csr":
+        monkeypatch.setenv("FASTILU_NO_TSELL", "1")
+    a = P.aniso3d_7pt(24)
+    fe = oracle.compute(a, 0, 0)
+    fe.vals = oracle.exact_ilu(fe.pattern, fe.ahat)
+    f = F.FastILU(a.row_ptr, a.col_idx, a.values, 0)
+    assert f.info().startswith("path=" + ("tsell" if path == "tsell" else "csr")), f.info()
+    f.set_factors(fe.vals, fe.s)
+    v, s = f.factors()
+    assert np.array_equal(v, fe.vals) and np.array_equal(s, fe.s)
+    bp = P.rhs_positive(a.n)
+    assert np.array_equal(f.apply_host(bp, 5), oracle.apply(fe, bp, 5))
+    b = oracle.spmv(a, P.x_true(a.n))
+    tb = torch.tensor(b, device="cuda")
+    tx = torch.zeros_like(tb)
+    it_b, rr_b = f.gmres(tb, tx, 60, 1e-6, 2000, 5)
+    _, it_o, _ = oracle.gmres(a, b, oracle.fastilu_preconditioner(fe, 5), 60, 1e-6, 2000)
+    assert rr_b <= 1e-6 and abs(it_b - it_o) <= 1, (it_b, it_o)
+    f.compute(2)  # arm A on the same handle: compute replaces the uploaded factors
+    it_a, _ = f.gmres(tb, tx, 60, 1e-6, 2000, 5)
+    assert it_b <= it_a, (it_b, it_a)
+
+
+def test_set_factors_errors():
+    a = P.laplace3d_7pt(6)
+    f = F.FastILU(a.row_ptr, a.col_idx, a.values, 0)
+    fo = oracle.compute(a, 0, 1)
+    v = fo.vals.copy()
+    d = np.flatnonzero(fo.pattern.col_idx == np.repeat(np.arange(a.n), np.diff(fo.pattern.row_ptr)))
+    v[d[7]] = 0.0
+    with pytest.raises(F.FastILUError) as ei:
+        f.set_factors(v, fo.s)
+    assert ei.value.status == "ZERO_PIVOT" and ei.value.index == 7
+    with pytest.raises(ValueError):
+        f.set_factors(v[:-1], fo.s)

@@ -131,3 +131,57 @@ def test_partition_fused_first_sweep_and_tolerance():
         assert len(o[3]) == s1
         np.testing.assert_allclose(o[3], f1.residual_history(), rtol=1e-12)
     assert np.array_equal(np.concatenate([o[0] for o in out]), v1)
+
+
+@pytest.mark.parametrize("overlap", ["1", "0"])
+def test_partition_128_four_ranks_bitwise(overlap, monkeypatch):
+    """27-pt 128^3 ILU(1) (config 3a) on 4 in-process ranks of 32 planes: the ghost
+    region (one plane + a line, ~16.6k rows) spans whole TMA boxes of the staged sweep, the
+    packed factor halo moves only the diagonal + upper columns, and the interior rows are swept
+    while it flies (overlap "1"; "0": FASTILU_NO_HALO_OVERLAP, halo first).  Factors and x are
+    bitwise the single-GPU run's."""
+    if overlap == "0":
+        monkeypatch.setenv("FASTILU_NO_HALO_OVERLAP", "1")
+    kind, g, gz, k, ns, nt, world = "27pt", 128, 128, 1, 3, 5, 4
+    a = P.make(kind, g, gz)
+    b = P.rhs_positive(a.n)
+    f1 = F.FastILU(a.row_ptr, a.col_idx, a.values, k)
+    f1.compute(ns)
+    v1 = f1.factors()[0]
+    tb = torch.tensor(b, device="cuda")
+    tx = torch.empty_like(tb)
+    f1.apply(tb, tx, nt)
+    torch.cuda.synchronize()
+    x1 = tx.cpu().numpy()
+    r1 = f1.residual_history()
+    f1.close()
+    del a
+    info = [None] * world
+    out, _ = run_partitioned(kind, g, gz, k, ns, nt, world, info=info)
+    assert all("staged=1" in i and "halo_bytes=" in i for i in info), info
+    assert np.array_equal(np.concatenate([o[0] for o in out]), v1)
+    assert np.array_equal(np.concatenate([o[2] for o in out]), x1)
+    assert np.array_equal(np.concatenate([o[5] for o in out]), x1)  # solve_host
+    for o in out:
+        np.testing.assert_allclose(o[3], r1, rtol=1e-12)
+    # the packed halo: diagonal + upper columns (32 of W = 63) of the ghost rows
+    hb = [int(i.split("halo_bytes=")[1].split()[0]) for i in info]
+    assert hb[-1] == 0 and all(h == hb[0] for h in hb[:-1])
+    assert hb[0] == (128 * 128 + 128 + 1 + 31) // 32 * 32 * 32 * 8, hb
+
+
+def test_nccl_two_processes():
+    """The NCCL transport across two GPUs (one process per GPU, torchrun): factors and x of a
+    2-rank run are bitwise the single-GPU run's.  Skips on a box with fewer than 2 GPUs."""
+    import os
+    import subprocess
+    import sys
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node=2", "--master-addr=127.0.0.1", "--master-port=29611",
+                        os.path.join(root, "tests", "nccl_worker.py")],
+                       capture_output=True, text=True, timeout=600, cwd=root)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert '"ok": true' in r.stdout, r.stdout[-2000:]

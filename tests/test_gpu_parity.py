@@ -122,7 +122,7 @@ def test_random_sparse(seed, k):
 
 
 def test_damping():
-    full_check(P.laplace3d_27pt(9), 1, 4, 5, omega=0.7, omega_tri=0.8)
+    full_check(P.laplace3d_27pt(9, gz=11), 1, 4, 5, omega=0.7, omega_tri=0.8)
 
 
 @pytest.mark.parametrize("path", ["tsell", "csr"])
@@ -391,7 +391,7 @@ def test_banded_templates(offsets, k, staged, monkeypatch):
     b = P.rhs_positive(a.n)
     f, vals, _, x = gpu_run(a, k, 3, 4, b)
     assert f.info().startswith("path=tsell"), f.info()
-    assert ("staged=1" in f.info()) == (staged == "1"), f.info()
+    assert ("staged=1" in f.info()) == (staged != "0"), f.info()
     fo = oracle.compute(a, k, 3)
     assert np.array_equal(vals, fo.vals)
     assert np.array_equal(x, oracle.apply(fo, b, 4))

@@ -53,3 +53,15 @@ def test_partition_gloo(world, kw):
     assert all(r["ok"] for r in res), res
     assert res[0]["G"] == 0 and res[-1]["H"] == 0
     assert all(r["G"] > 0 for r in res[1:]) and all(r["H"] > 0 for r in res[:-1])
+
+
+def test_bench_refuses_world_size_mismatch():
+    """bench.py --gpus N under a launcher whose WORLD_SIZE differs must not print a result line
+    (a plain `--gpus 8` silently ran one rank)."""
+    import subprocess
+    import sys
+    env = dict(os.environ, WORLD_SIZE="2", RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(os.path.dirname(HERE), "bench.py"), "--gpus", "1"],
+                       capture_output=True, text=True, env=env, timeout=120)
+    assert r.returncode == 2 and not r.stdout.strip(), (r.returncode, r.stdout, r.stderr)
+    assert "refusing" in r.stderr
