@@ -139,8 +139,16 @@ fastilu_status fastilu_solve_host(fastilu_handle h, const double *values, int ns
 /* The paper's asynchronous in-place sweeps: every thread updates its entries in
  * place, reading whatever mix of old and already-updated values it finds (Gauss-Seidel-like,
  * non-deterministic; same fixed point).  The residual history is the by-product of those
- * mixed reads.  Template-SELL layout, single GPU (FASTILU_ERR_UNSUPPORTED otherwise). */
+ * mixed reads.  Template-SELL or block (3-dof) layout, single GPU (FASTILU_ERR_UNSUPPORTED
+ * otherwise).  Default block size: half a row's targets (template) / one 3x3 block (block). */
 fastilu_status fastilu_compute_async(fastilu_handle h, int nsweeps);
+/* The same with the paper's option "Block Size (or number of nonzeroes per thread)"
+ * (PAPER.md:722): every thread updates about nnz_per_thread consecutive entries of the factor,
+ * in order and in place, so the later ones use its own new values.  Template layout: a
+ * contiguous block of ceil(W / parts) targets of one row, parts = the power of two (<= 8) that
+ * brings the block to <= nnz_per_thread; block layout: max(1, nnz_per_thread / bs^2)
+ * consecutive bs x bs target blocks.  nnz_per_thread = 0: the default.  INVALID_ARG if < 0. */
+fastilu_status fastilu_compute_async_block(fastilu_handle h, int nsweeps, int nnz_per_thread);
 
 /* Option "Warm up": FastILU(0), FastILU(1), ..., FastILU(k), each with nsweeps
  * sweeps, the factors of level L-1 initialising the entries of S_{L-1} inside S_L (new fill

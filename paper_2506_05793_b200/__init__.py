@@ -59,6 +59,7 @@ _SIGS = {
     "fastilu_compute_tol": (C.c_int, [H, C.c_double, C.c_int, C.POINTER(C.c_int)]),
     "fastilu_compute_warmup": (C.c_int, [H, C.c_int]),
     "fastilu_compute_async": (C.c_int, [H, C.c_int]),
+    "fastilu_compute_async_block": (C.c_int, [H, C.c_int, C.c_int]),
     "fastilu_compute_host": (C.c_int, [H, F64P, C.c_int]),
     "fastilu_solve_host": (C.c_int, [H, F64P, C.c_int, F64P, F64P, C.c_int]),
     "fastilu_apply": (C.c_int, [H, C.c_void_p, C.c_void_p, C.c_int]),
@@ -322,10 +323,15 @@ class FastILU:
                self._h)
         return x
 
-    def compute_async(self, nsweeps: int):
-        """The paper's asynchronous in-place sweeps (non-deterministic; fastilu_compute_async)."""
-        _check(lib().fastilu_compute_async(self._h, int(nsweeps)), "fastilu_compute_async",
-               self._h)
+    def compute_async(self, nsweeps: int, nnz_per_thread: int | None = None):
+        """The paper's asynchronous in-place sweeps (non-deterministic; fastilu_compute_async),
+        optionally with its "Block Size" option (nonzeros per thread)."""
+        if nnz_per_thread is None:
+            _check(lib().fastilu_compute_async(self._h, int(nsweeps)), "fastilu_compute_async",
+                   self._h)
+        else:
+            _check(lib().fastilu_compute_async_block(self._h, int(nsweeps), int(nnz_per_thread)),
+                   "fastilu_compute_async_block", self._h)
 
     def compute_warmup(self, nsweeps: int):
         """Warm-up option: FastILU(0..k) with nsweeps each (fastilu_compute_warmup)."""

@@ -185,6 +185,119 @@ bsr_sweep_kernel(BsrDev B, const double *__restrict__ ahb, const double *__restr
   }
 }
 
+// The paper's ASYNCHRONOUS in-place sweep on the block layout ("updated in
+// parallel (in place) ... non-deterministic"; option "Block Size (number of nonzeroes per
+// thread)").  Thread q updates the nb consecutive target blocks [q nb, (q+1) nb)
+// (block row order) one after the other, in place: every value it reads (pivot blocks, divisor
+// blocks, its own earlier blocks) is whatever the factor holds at that moment, so entries it
+// updated before are used fresh, entries of other threads maybe; inside a block the entries are
+// updated in row-major order and the tail terms use the block's new values (Gauss-Seidel order).
+// nb * BS^2 = nonzeros per thread.  The residual partials use the values the update read.
+template <int BS>
+__global__ void __launch_bounds__(256)
+bsr_sweep_async_kernel(BsrDev B, const double *__restrict__ ahb, double *vals, double omega,
+                       double *__restrict__ partials, ErrFlags *err, int nb) {
+  constexpr int BB = BS * BS, ST = (BB + 1) & ~1;
+  const bool damp = (omega != 1.0);
+  const double om1 = 1.0 - omega;
+  double r2 = 0.0;
+  const int64_t nthr = (B.nblk + nb - 1) / nb;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nthr;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t b = q * nb; b < min((q + 1) * (int64_t)nb, B.nblk); b++) {
+      const int I = B.brow[b], J = B.bcol[b];
+      double a[BB];
+      ld_block<BB, ST>(ahb + b * ST, a);
+      for (int64_t t = B.tptr[b]; t < B.tptr[b + 1]; t++) {  // pivot blocks K ascending
+        const int2 pr = B.terms[t];
+        double L[BB], U[BB];
+        ld_block_any<BB, ST>(vals + (int64_t)pr.x * ST, L);
+        ld_block_any<BB, ST>(vals + (int64_t)pr.y * ST, U);
+#pragma unroll
+        for (int d = 0; d < BS; d++)
+#pragma unroll
+          for (int e = 0; e < BS; e++) {
+            double v = a[d * BS + e];
+#pragma unroll
+            for (int c = 0; c < BS; c++) v = __dsub_rn(v, __dmul_rn(L[d * BS + c], U[c * BS + e]));
+            a[d * BS + e] = v;
+          }
+      }
+      double o[BB], nv[BB];
+      ld_block_any<BB, ST>(vals + b * ST, o);
+      if (J < I) {
+        double D[BB];
+        ld_block_any<BB, ST>(vals + (int64_t)B.bdiag[J] * ST, D);
+#pragma unroll
+        for (int d = 0; d < BS; d++)
+#pragma unroll
+          for (int e = 0; e < BS; e++) {
+            double v = a[d * BS + e];
+#pragma unroll
+            for (int c = 0; c < e; c++) v = __dsub_rn(v, __dmul_rn(nv[d * BS + c], D[c * BS + e]));
+            const double ujj = D[e * BS + e], ol = o[d * BS + e];
+            const double ee = __dsub_rn(v, __dmul_rn(ol, ujj));
+            r2 = fma(ee, ee, r2);
+            const double l = __ddiv_rn(v, ujj);
+            nv[d * BS + e] = damp ? __dadd_rn(__dmul_rn(om1, ol), __dmul_rn(omega, l)) : l;
+          }
+      } else if (J == I) {
+#pragma unroll
+        for (int d = 0; d < BS; d++)
+#pragma unroll
+          for (int e = 0; e < BS; e++) {
+            double v = a[d * BS + e];
+#pragma unroll
+            for (int c = 0; c < (d < e ? d : e); c++)
+              v = __dsub_rn(v, __dmul_rn(nv[d * BS + c], nv[c * BS + e]));
+            const double od = o[d * BS + e];
+            if (d > e) {
+              const double ujj = nv[e * BS + e];
+              const double ee = __dsub_rn(v, __dmul_rn(od, ujj));
+              r2 = fma(ee, ee, r2);
+              const double l = __ddiv_rn(v, ujj);
+              nv[d * BS + e] = damp ? __dadd_rn(__dmul_rn(om1, od), __dmul_rn(omega, l)) : l;
+            } else {
+              const double ee = __dsub_rn(v, od);
+              r2 = fma(ee, ee, r2);
+              nv[d * BS + e] = damp ? __dadd_rn(__dmul_rn(om1, od), __dmul_rn(omega, v)) : v;
+            }
+          }
+#pragma unroll
+        for (int d = 0; d < BS; d++)
+          if (bsr_bad_pivot(nv[d * BS + d]))
+            atomicMin(&err->zero_pivot, (unsigned long long)I * BS + d);
+      } else {
+        double D[BB];
+        ld_block_any<BB, ST>(vals + (int64_t)B.bdiag[I] * ST, D);
+#pragma unroll
+        for (int d = 0; d < BS; d++)
+#pragma unroll
+          for (int e = 0; e < BS; e++) {
+            double v = a[d * BS + e];
+#pragma unroll
+            for (int c = 0; c < d; c++) v = __dsub_rn(v, __dmul_rn(D[d * BS + c], nv[c * BS + e]));
+            const double ou = o[d * BS + e];
+            const double ee = __dsub_rn(v, ou);
+            r2 = fma(ee, ee, r2);
+            nv[d * BS + e] = damp ? __dadd_rn(__dmul_rn(om1, ou), __dmul_rn(omega, v)) : v;
+          }
+      }
+      st_block<BB, ST>(vals + b * ST, nv);
+    }
+  }
+  __shared__ double wsum[32];
+  double v = r2;
+  for (int q = 16; q > 0; q >>= 1) v += __shfl_down_sync(0xffffffffu, v, q);
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); w++) t += wsum[w];
+    partials[blockIdx.x] = t;
+  }
+}
+
 // scalar CSR (S row order) <-> block layout; one warp per scalar row r = BS I + d, whose S row
 // is block row I's columns expanded (entry q of the row = block q / BS, column e = q % BS).
 template <int BS, int DIR>  // DIR 0: CSR -> blocks, 1: blocks -> CSR (+ u_ii copy)
@@ -274,6 +387,14 @@ cudaError_t launch_bsr_sweep(const BsrDev &B, const double *ahb, const double *o
                              int threads, size_t smem, int minb, cudaStream_t st) {
   return minb >= 4 ? launch_bsr_t<4>(B, ahb, old, out, omega, partials, err, grid, threads, smem, st)
                    : launch_bsr_t<1>(B, ahb, old, out, omega, partials, err, grid, threads, smem, st);
+}
+
+cudaError_t launch_bsr_sweep_async(const BsrDev &B, const double *ahb, double *vals, double omega,
+                                   double *partials, ErrFlags *err, int grid, int nb,
+                                   cudaStream_t st) {
+  FASTILU_BS_DISPATCH(B.bs, (bsr_sweep_async_kernel<BS><<<grid, 256, 0, st>>>(
+                                B, ahb, vals, omega, partials, err, nb)))
+  return cudaGetLastError();
 }
 
 static unsigned conv_grid(int64_t nrows) {

@@ -167,6 +167,11 @@ struct BsrDev {
 // smem > 0: stage each tile's block rows in smem bytes of shared memory (when they fit)
 // minb: __launch_bounds__ resident-CTA hint (1 or 4)
 cudaError_t bsr_sweep_occupancy(int bs, int threads, size_t smem, int minb, int *blocks_per_sm);
+// asynchronous in-place block sweep: nb consecutive target blocks per thread;
+// grid blocks of 256 threads, partials[grid]
+cudaError_t launch_bsr_sweep_async(const BsrDev &B, const double *ahb, double *vals, double omega,
+                                   double *partials, ErrFlags *err, int grid, int nb,
+                                   cudaStream_t st);
 cudaError_t launch_bsr_sweep(const BsrDev &B, const double *ahb, const double *old, double *out,
                              double omega, double *partials, ErrFlags *err, int grid,
                              int threads, size_t smem, int minb, cudaStream_t st);

@@ -95,7 +95,10 @@ struct fastilu_handle_s {
   std::vector<unsigned long long *> d_lmask;  // warm-up: presence masks of levels 0..K-1
   void *jit_sweep = nullptr;
   void *jit_sweep_first = nullptr;  // sweep 1 from iterate 0: A x A terms only
-  void *jit_sweep_async = nullptr;  // compiled on the first asynchronous compute
+  void *jit_sweep_async = nullptr;  // the asynchronous kernel of the current block size
+  std::vector<std::pair<int, void *>> jit_async;  // (parts, kernel), compiled on first use
+  int async_ept = 0;                              // nonzeros per thread of the next async compute
+  int async_parts = 0, async_rows = 0;
   // staged sweep (tsell.h StagedCfg): pivot rows through shared memory by TMA
   void *jit_st = nullptr, *jit_st_first = nullptr;
   void *jit_st_init = nullptr;  // sweep 1 with iterate 0 computed from ahat (single GPU)
@@ -942,14 +945,29 @@ extern "C" fastilu_status fastilu_set_values_device(fastilu_handle h, const doub
 static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, int *done,
                                    bool warmup = false, bool async = false) {
   if (!h || nsweeps < 0) FAIL(FASTILU_ERR_INVALID_ARG);
-  if (async) {  // in-place variant of the template kernel (single GPU)
-    if (!h->tsell || h->comm) FAIL(FASTILU_ERR_UNSUPPORTED);
-    if (!h->jit_sweep_async) {
-      std::string log;
-      const std::string src =
-          sweep_source(h->T, h->t_threads, h->t_parts, h->t_minb, true, h->t_prefetch);
-      if (jit_get(src, "fastilu_tsell_sweep_async", h->device, &h->jit_sweep_async, &log))
-        FAIL(FASTILU_ERR_UNSUPPORTED);
+  if (async) {  // in-place variants (single GPU): template kernel or block kernel
+    if (!(h->tsell || h->bsr) || h->comm) FAIL(FASTILU_ERR_UNSUPPORTED);
+    if (h->tsell) {
+      // "Block Size": each thread updates a contiguous block of ~ept targets of
+      // its row; parts = W / ept rounded up to a divisor of the block's warps
+      const int warps = h->t_threads / 32;
+      const int ept = h->async_ept > 0 ? h->async_ept : (h->T.W + h->t_parts - 1) / h->t_parts;
+      int parts = 1;
+      while (parts < warps && (h->T.W + parts - 1) / parts > ept) parts *= 2;
+      void *fn = nullptr;
+      for (auto &pr : h->jit_async)
+        if (pr.first == parts) fn = pr.second;
+      if (!fn) {
+        std::string log;
+        const std::string src = sweep_source(h->T, h->t_threads, parts, 0, true, false, false,
+                                             true);
+        if (jit_get(src, "fastilu_tsell_sweep_async", h->device, &fn, &log))
+          FAIL(FASTILU_ERR_UNSUPPORTED);
+        h->jit_async.push_back({parts, fn});
+      }
+      h->jit_sweep_async = fn;
+      h->async_parts = parts;
+      h->async_rows = 32 * (warps / parts);
     }
   }
   const int per_level = nsweeps;
@@ -1126,6 +1144,12 @@ static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, i
                            tm0, tm1};
           if (jit_launch_smem(fn, (int)std::min<int64_t>(grid, ntl), thr, smem, st, sargs))
             return -1;
+        } else if (async) {
+          ntl = (b1 - b0 + h->async_rows - 1) / h->async_rows;
+          int one = 1;
+          void *args[] = {&old, &outp, &ahat, &mk, &udo, &udn, &a0, &a1, &om, &part, &zp, &ctr,
+                          &one};
+          if (jit_launch(fn, (int)std::min<int64_t>(grid, ntl), thr, st, args)) return -1;
         } else {
           const int64_t spt = h->t_rows_tile / 32, ss = h->t_sstride;
           ntl = ((b1 - b0 + 31) / 32 + spt * ss - 1) / (spt * ss) * ss;
@@ -1151,6 +1175,17 @@ static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, i
       CU(cudaMemsetAsync(h->d_counter + 1, 0, sizeof(unsigned int), st));
       continue;
     }
+    if (h->bsr && async) {  // nb consecutive target blocks per thread, in place
+      const int bb = h->B.bs * h->B.bs;
+      const int nb = std::max(1, (h->async_ept > 0 ? h->async_ept : bb) / bb);
+      const int64_t nthr = (h->B.nblk + nb - 1) / nb;
+      const int grid = (int)std::max<int64_t>(
+          1, std::min<int64_t>((nthr + 255) / 256, (int64_t)sm_count(h->device) * 8));
+      CU(launch_bsr_sweep_async(h->B, h->d_ahb, h->d_vb[0], h->opt.omega, h->d_partials,
+                                h->d_err, grid, nb, st));
+      CU(launch_reduce(h->d_partials, grid, h->d_r2 + (sw - 1), st));
+      continue;
+    }
     if (h->bsr) {
       CU(launch_bsr_sweep(h->B, h->d_ahb, h->d_vb[ib], h->d_vb[ob], h->opt.omega, h->d_partials,
                           h->d_err, h->bsr_grid, h->bsr_threads, h->bsr_smem, h->bsr_minb,
@@ -1168,9 +1203,10 @@ static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, i
   }
   nsweeps = executed;
   if (done) *done = executed;
-  if (h->bsr)  // factors back to S row order (+ u_ii) for apply / get_factors
-    CU(launch_bsr_to_csr(h->B, h->d_rp, h->d_vb[nsweeps & 1], h->d_vals[nsweeps & 1],
-                         h->d_ud[nsweeps & 1], h->n, st));
+  if (h->bsr) {  // factors back to S row order (+ u_ii) for apply / get_factors
+    const int fb = async ? 0 : (nsweeps & 1);
+    CU(launch_bsr_to_csr(h->B, h->d_rp, h->d_vb[fb], h->d_vals[fb], h->d_ud[fb], h->n, st));
+  }
   CU(cudaEventRecord(h->ev[2], st));
   CU(cudaMemcpyAsync(h->h_err, h->d_err, sizeof(ErrFlags), cudaMemcpyDeviceToHost, st));
   if (nsweeps)
@@ -1430,7 +1466,16 @@ extern "C" fastilu_status fastilu_compute(fastilu_handle h, int nsweeps) {
   return compute_impl(h, nsweeps, 0.0, nullptr);
 }
 
+extern "C" fastilu_status fastilu_compute_async_block(fastilu_handle h, int nsweeps,
+                                                      int nnz_per_thread) {
+  if (!h || nnz_per_thread < 0) FAIL(FASTILU_ERR_INVALID_ARG);
+  h->async_ept = nnz_per_thread;
+  return compute_impl(h, nsweeps, 0.0, nullptr, false, true);
+}
+
 extern "C" fastilu_status fastilu_compute_async(fastilu_handle h, int nsweeps) {
+  if (!h) FAIL(FASTILU_ERR_INVALID_ARG);
+  h->async_ept = 0;  // default block size
   return compute_impl(h, nsweeps, 0.0, nullptr, false, true);
 }
 

@@ -30,6 +30,15 @@ def run_full(kind, g, k, ns, nt):
     return a, b, f, vals, s, rp, ci, tx.cpu().numpy()
 
 
+@pytest.fixture(autouse=True)
+def oracle_threads():
+    """The windowed oracle on all host cores (bitwise the 1-thread oracle)."""
+    import os
+    oracle.set_threads(len(os.sched_getaffinity(0)))
+    yield
+    oracle.set_threads(1)
+
+
 def check_planes(a, b, kind, g, k, ns, nt, planes, vals, rp, ci, x):
     plane = g * g
     for z in planes:
@@ -73,11 +82,30 @@ def test_config3_to_convergence_128():
     assert h[-1] <= thr * (1 + 1e-9) and h[-2] > thr * (1 - 1e-9)
 
 
+def test_config3_to_convergence_128_windowed_oracle():
+    """Config 3a 'to convergence' (reading G15) at full size: the GPU's factors at its stopping
+    sweep s* and x after 5 + 5 Jacobi sweeps equal the windowed oracle's at the same s*, bitwise,
+    on the middle plane (margins: s* + ntri + k + 4 planes below)."""
+    g, k, nt = 128, 1, 5
+    a = P.laplace3d_27pt(g)
+    b = P.rhs_positive(a.n)
+    f = F.FastILU(a.row_ptr, a.col_idx, a.values, k)
+    s_star = f.compute_tol(1e-10, 100)
+    tb = torch.tensor(b, device="cuda")
+    tx = torch.empty_like(tb)
+    f.apply(tb, tx, nt)
+    torch.cuda.synchronize()
+    vals, _ = f.factors()
+    rp, ci, _ = f.pattern()
+    check_planes(a, b, "27pt", g, k, s_star, nt, [64], vals, rp, ci, tx.cpu().numpy())
+
+
 def test_config4_27pt_256():
     g, k, ns, nt = 256, 1, 3, 5
     a, b, f, vals, s, rp, ci, x = run_full("27pt", g, k, ns, nt)
     assert f.info().startswith("path=tsell")
-    check_planes(a, b, "27pt", g, k, ns, nt, [128], vals, rp, ci, x)
+    # first and last planes (TMA zero-fill below plane 0, the last tile's tail) and the middle
+    check_planes(a, b, "27pt", g, k, ns, nt, [0, 128, 255], vals, rp, ci, x)
 
 
 def test_config2_7pt_128_exact():
