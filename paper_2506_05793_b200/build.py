@@ -19,8 +19,7 @@ LIB = os.path.join(HERE, "lib", "libfastilu_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_SRCS = ["kernels.cu", "bsr.cu", "fastilu.cu"]
-CXX_SRCS = ["symbolic.cpp", "comm.cpp", "classes.cpp", "tsell.cpp", "tsell_split.cpp", "jit.cpp",
-            "blocks.cpp"]
+CXX_SRCS = ["symbolic.cpp", "comm.cpp", "classes.cpp", "tsell.cpp", "jit.cpp", "blocks.cpp"]
 HDRS = ["host.h", "device.h", "comm.h", "tsell.h", "jit.h", "blocks.h"]
 
 

@@ -430,17 +430,10 @@ static fastilu_status setup_tsell(fastilu_handle h, const std::vector<unsigned l
       const char *ev_smb = std::getenv("FASTILU_TSELL_ST_MINB");
       const int sminb = ev_smb ? atoi(ev_smb) : 0;
       StagedCfg c{};
-      // column-split ring (Sec. 4m): FASTILU_TSELL_SPLIT=1, stages FASTILU_TSELL_STAGES (4)
-      const char *ev_split = std::getenv("FASTILU_TSELL_SPLIT");
-      const bool split = ev_split && atoi(ev_split) != 0 && (T.W - T.c0) % 2 == 0;
-      const int nst_split = ev_st ? std::max(2, atoi(ev_st)) : 4;
       const std::string s0 =
-          split ? sweep_source_staged_split(T, sthreads, sparts, nst_split, sminb, false, &c, sopts)
-                : sweep_source_staged(T, sthreads, sparts, nst, sminb, false, &c, sopts);
+          sweep_source_staged(T, sthreads, sparts, nst, sminb, false, &c, sopts);
       const std::string s1 =
-          split ? sweep_source_staged_split(T, sthreads, sparts, nst_split, sminb, true, nullptr,
-                                            sopts)
-                : sweep_source_staged(T, sthreads, sparts, nst, sminb, true, nullptr, sopts);
+          sweep_source_staged(T, sthreads, sparts, nst, sminb, true, nullptr, sopts);
       if (std::getenv("FASTILU_DUMP_SRC")) fprintf(stderr, "%s\n", s0.c_str());
       int sbps = 0;
       if (!jit_get(s0, "fastilu_tsell_sweep_st", h->device, &h->jit_st, &log) &&
@@ -1251,9 +1244,6 @@ static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, i
 }
 
 static fastilu_status apply_impl(fastilu_handle h, const double *b, double *x, int ntri);
-static int jit_jacobi(fastilu_handle h, bool lower, const double *vals, const double *ud,
-                      const double *rhs, const double *xo, double *xn, double *xf, int64_t r0,
-                      int64_t r1, int64_t Gh, double om, bool final_x);
 
 // fastilu_compute_host: new values from host memory + nsweeps sweeps, the upload pipelined with
 // the compute.  Chunks of >= A's bandwidth rows: chunk c's values go up on a copy stream; on
@@ -1264,10 +1254,8 @@ static int jit_jacobi(fastilu_handle h, bool lower, const double *vals, const do
 // arithmetic as set_values + compute; only the residual's sum is taken per chunk.
 static fastilu_status compute_host_impl(fastilu_handle h, const double *values, int nsweeps,
                                         const double *b_host = nullptr,
-                                        bool *b_queued = nullptr, int ntri = 0,
-                                        double *x_host = nullptr, bool *solved = nullptr) {
+                                        bool *b_queued = nullptr) {
   if (b_queued) *b_queued = false;
-  if (solved) *solved = false;
   const int64_t R = h->st.rows > 0 ? h->st.rows : 256;
   int64_t bwA = 0;
   for (int32_t o : h->T.offA) bwA = std::max<int64_t>(bwA, std::abs((int64_t)o));
@@ -1316,18 +1304,6 @@ static fastilu_status compute_host_impl(fastilu_handle h, const double *values, 
   // previous work (the previous compute may still read d_aval / d_aT)
   CU(cudaEventRecord(h->ev[1], st));
   CU(cudaStreamWaitEvent(h->copy_stream, h->ev[1], 0));
-  // solve_host with the pipelined L solve: the right-hand side goes FIRST, so the L Jacobi
-  // sweeps of a chunk can run as soon as its factors are final (during the upload)
-  const bool lpipe = b_host && x_host && solved && ntri >= 1 && h->jit_jac[0] && h->jit_jac[1] &&
-                     !std::getenv("FASTILU_NO_SOLVE_PIPELINE");
-  if (b_host) {
-    if (!h->d_bx) CU(dalloc(&h->d_bx, 2 * h->n));
-    if (lpipe) {
-      CU(cudaMemcpyAsync(h->d_bx, b_host, sizeof(double) * h->n, cudaMemcpyHostToDevice,
-                         h->copy_stream));
-      CU(cudaEventRecord(h->chunk_ev[C], h->copy_stream));
-    }
-  }
   for (int c = 0; c < C; c++) {
     const int64_t a0 = h->h_arp[rb(c)], a1 = h->h_arp[rb(c + 1)];
     if (a1 > a0)
@@ -1335,12 +1311,11 @@ static fastilu_status compute_host_impl(fastilu_handle h, const double *values, 
                          cudaMemcpyHostToDevice, h->copy_stream));
     CU(cudaEventRecord(h->chunk_ev[c], h->copy_stream));
   }
-  if (b_host) {  // solve_host: (without the L pipeline) b follows the values
-    if (!lpipe) {
-      CU(cudaMemcpyAsync(h->d_bx, b_host, sizeof(double) * h->n, cudaMemcpyHostToDevice,
-                         h->copy_stream));
-      CU(cudaEventRecord(h->chunk_ev[C], h->copy_stream));
-    }
+  if (b_host) {  // solve_host: the right-hand side follows the values on the copy stream
+    if (!h->d_bx) CU(dalloc(&h->d_bx, 2 * h->n));
+    CU(cudaMemcpyAsync(h->d_bx, b_host, sizeof(double) * h->n, cudaMemcpyHostToDevice,
+                       h->copy_stream));
+    CU(cudaEventRecord(h->chunk_ev[C], h->copy_stream));
     h->chunk_b = C;
     *b_queued = true;
   }
@@ -1405,86 +1380,18 @@ static fastilu_status compute_host_impl(fastilu_handle h, const double *values, 
     }
     return FASTILU_OK;
   };
-  // L Jacobi sweeps of the solve along a second diagonal: once factor step d made chunk
-  // cf = d - nsweeps + 1 final, L step e = cf runs sweep t on chunk e - t + 1 (t ascending), the
-  // same ping-pong argument as the factor diagonal (sweep t of chunk c reads z^{t-1} of chunks
-  // c-1, c only, and is launched before sweep t+1 of chunk c-1 overwrites that buffer)
-  const double omt = h->opt.omega_tri;
-  const double *fvals = h->d_vals[nsweeps & 1], *fud = h->d_ud[nsweeps & 1];
-  bool b_waited = false;
-  auto lstep = [&](int e) -> fastilu_status {
-    for (int t = 1; t <= ntri; t++) {
-      const int c = e - t + 1;
-      if (c < 0 || c >= C) continue;
-      if (!b_waited) {
-        CU(cudaStreamWaitEvent(st, h->chunk_ev[C], 0));
-        b_waited = true;
-      }
-      if (t == 1) {
-        CU(launch_trisolve_first_L(h->d_bx, h->d_s, h->d_y, h->d_z[0], rb(c), rb(c + 1), 0,
-                                   omt, st));
-      } else if (jit_jacobi(h, true, fvals, nullptr, h->d_y, h->d_z[(t - 2) & 1],
-                            h->d_z[(t - 1) & 1], nullptr, rb(c), rb(c + 1), 0, omt, false)) {
-        FAIL(FASTILU_ERR_CUDA);
-      }
-    }
-    return FASTILU_OK;
-  };
-  auto diag_l = [&](int d) -> fastilu_status {
-    fastilu_status f1 = diag(d);
-    if (f1 || !lpipe) return f1;
-    return lstep(d - nsweeps + 1);
-  };
   fastilu_status fs;
   for (int c = 0; c < C; c++) {
     if ((fs = prep(c))) return fs;
     if (c >= 1) {
       if ((fs = ahat(c - 1))) return fs;
-      if ((fs = diag_l(c - 1))) return fs;
+      if ((fs = diag(c - 1))) return fs;
     }
   }
   if ((fs = ahat(C - 1))) return fs;
   for (int d = C - 1; d <= C + nsweeps - 2; d++)
-    if ((fs = diag_l(d))) return fs;
-  if (lpipe)
-    for (int e = C; e <= C + ntri - 2; e++)
-      if ((fs = lstep(e))) return fs;
+    if ((fs = diag(d))) return fs;
   CU(cudaEventRecord(h->ev[2], st));
-  if (lpipe) {
-    // the U sweeps need every chunk's z: full range, except the last sweep, which runs chunk by
-    // chunk from the top so that each chunk's x goes back over PCIe while the next computes
-    const double *zf = h->d_z[(ntri - 1) & 1];
-    double *xd = h->d_bx + h->n;
-    CU(cudaEventRecord(h->ev[3], st));
-    if (ntri == 1) {
-      for (int c = C - 1; c >= 0; c--) {
-        CU(launch_trisolve_first_U(zf, fud, h->d_s, h->d_w[0], xd, rb(c), rb(c + 1), 0, omt,
-                                   true, st));
-        CU(cudaEventRecord(h->chunk_ev[c], st));
-      }
-    } else {
-      CU(launch_trisolve_first_U(zf, fud, h->d_s, h->d_w[0], xd, 0, h->n, 0, omt, false, st));
-      for (int t = 2; t < ntri; t++)
-        if (jit_jacobi(h, false, fvals, fud, zf, h->d_w[(t - 2) & 1], h->d_w[(t - 1) & 1], xd, 0,
-                       h->n, 0, omt, false))
-          FAIL(FASTILU_ERR_CUDA);
-      for (int c = C - 1; c >= 0; c--) {
-        if (jit_jacobi(h, false, fvals, fud, zf, h->d_w[(ntri - 2) & 1], h->d_w[(ntri - 1) & 1],
-                       xd, rb(c), rb(c + 1), 0, omt, true))
-          FAIL(FASTILU_ERR_CUDA);
-        CU(cudaEventRecord(h->chunk_ev[c], st));
-      }
-    }
-    CU(cudaEventRecord(h->ev[4], st));
-    h->apply_timed = true;
-    for (int c = C - 1; c >= 0; c--) {
-      CU(cudaStreamWaitEvent(h->copy_stream, h->chunk_ev[c], 0));
-      CU(cudaMemcpyAsync(x_host + rb(c), xd + rb(c), sizeof(double) * (rb(c + 1) - rb(c)),
-                         cudaMemcpyDeviceToHost, h->copy_stream));
-    }
-    CU(cudaStreamSynchronize(h->copy_stream));
-    *solved = true;
-  }
   std::vector<double> r2c((size_t)C * nsweeps);
   CU(cudaMemcpyAsync(h->h_err, h->d_err, sizeof(ErrFlags), cudaMemcpyDeviceToHost, st));
   CU(cudaMemcpyAsync(r2c.data(), h->d_r2c, sizeof(double) * r2c.size(), cudaMemcpyDeviceToHost,
@@ -1539,10 +1446,9 @@ extern "C" fastilu_status fastilu_solve_host(fastilu_handle h, const double *val
       (h->n > 0 && (!b || !x)))
     FAIL(FASTILU_ERR_INVALID_ARG);
   DeviceGuard dg_(h->device);
-  bool queued = false, solved = false;
-  fastilu_status s = drain_copies(
-      h, compute_host_impl(h, values, nsweeps, b, &queued, ntrisweeps, x, &solved));
-  if (s || solved) return s;  // solved inside: L sweeps pipelined with the upload
+  bool queued = false;
+  fastilu_status s = drain_copies(h, compute_host_impl(h, values, nsweeps, b, &queued));
+  if (s) return s;
   if (!queued) return fastilu_apply_host(h, b, x, ntrisweeps);
   CU(cudaStreamWaitEvent(h->stream, h->chunk_ev[h->chunk_b], 0));
   CU(cudaEventRecord(h->ev[3], h->stream));

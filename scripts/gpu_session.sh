@@ -46,7 +46,7 @@ for step in "$@"; do
     sanitize)
       for tool in memcheck racecheck synccheck initcheck; do
         echo "== $tool"
-        timeout 900 compute-sanitizer --tool $tool --print-limit 20 python scripts/sanitize_case.py 2>&1 | tail -25
+        timeout 900 compute-sanitizer --tool $tool --print-limit 20 python tests/sanitize_case.py 2>&1 | tail -25
       done > gpurun_out/${TAG}_sanitize.log 2>&1 ;;
     ab)
       IFS=';' read -ra envs <<< "${AB_ENVS:-}"

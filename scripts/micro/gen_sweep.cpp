@@ -1,7 +1,7 @@
 // Host-only dump of a generated sweep kernel, for compiling / inspecting it without a GPU:
 //   g++ -O2 -std=c++17 -pthread -Ipaper_2506_05793_b200/csrc -Iinclude scripts/micro/gen_sweep.cpp \
-//       paper_2506_05793_b200/csrc/{symbolic,tsell,tsell_split}.cpp -o /tmp/gen_sweep
-//   /tmp/gen_sweep row|init|async|split K G THREADS PARTS > k.cu
+//       paper_2506_05793_b200/csrc/{symbolic,tsell}.cpp -o /tmp/gen_sweep
+//   /tmp/gen_sweep row|init|async K G THREADS PARTS > k.cu
 //   nvcc -arch=sm_100a -cubin -Xptxas -v k.cu       (register / spill report)
 #include <cstdio>
 #include <cstdlib>
@@ -46,9 +46,7 @@ int main(int argc, char **argv) {
   StagedCfg c{};
   std::string src;
   const unsigned opts = kStagedFastDiv | kStagedOwnL | kStagedLastIssues;
-  if (!strcmp(mode, "split"))
-    src = sweep_source_staged_split(T, threads, parts, 4, 0, false, &c, opts);
-  else if (!strcmp(mode, "async"))
+  if (!strcmp(mode, "async"))
     src = sweep_source(T, threads, parts, 0, true, false, false, true);
   else if (!strcmp(mode, "init"))
     src = sweep_source_staged(T, threads, parts, 2, 0, true, &c, opts | kStagedFromAhat);

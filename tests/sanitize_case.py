@@ -4,7 +4,7 @@ the register-pivot sweep (7-pt ILU(0), W <= 16), the template scale / Ahat / Jac
 CSR path, the block path, and a tolerance-mode compute.  Checks parity with the oracle so a run
 under a tool still proves the kernels computed the right thing.
 
-    compute-sanitizer --tool racecheck python scripts/sanitize_case.py
+    compute-sanitizer --tool racecheck python tests/sanitize_case.py
 """
 import os
 import sys

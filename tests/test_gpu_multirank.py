@@ -185,3 +185,56 @@ def test_nccl_two_processes():
                        capture_output=True, text=True, timeout=600, cwd=root)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert '"ok": true' in r.stdout, r.stdout[-2000:]
+
+
+def test_partition_gmres():
+    """Config 5's GMRES(60) on 3 in-process ranks (SpMV vector halos, dot products summed over
+    ranks, FastILU apply with trisolve halos): the iteration count equals the single-GPU run's
+    (+-1: the dot products are summed rank by rank) and both reach the 1e-6 relative residual."""
+    kind, g, gz, k, ns, nt, world = "aniso7pt", 16, 24, 0, 2, 5, 3
+    a = P.make(kind, g, gz)
+    xt = P.x_true(a.n)
+    b = oracle.spmv(a, xt)
+    f1 = F.FastILU(a.row_ptr, a.col_idx, a.values, k)
+    f1.compute(ns)
+    tb = torch.tensor(b, device="cuda")
+    tx = torch.zeros_like(tb)
+    it1, rr1 = f1.gmres(tb, tx, 60, 1e-6, 2000, nt)
+    plane = g * g
+    grp = F.fastilu_group_create(world)
+    res = [None] * world
+    errs = [None] * world
+
+    def worker(r):
+        try:
+            torch.cuda.set_device(0)
+            z0, z1 = split_planes(gz, world)[r]
+            need = F.fastilu_required_lead_rows(P.bandwidth(kind, g), k)
+            lp = min(z0, -(-need // plane))
+            blk = P.make(kind, g, gz, planes=(z0 - lp, z1))
+            f = F.FastILU(blk.row_ptr, blk.col_idx, blk.values, k, rank=r, nranks=world,
+                          comm_kind=F.COMM_LOCAL, group=grp, global_n=a.n,
+                          row_begin=z0 * plane, n_lead=lp * plane, n=(z1 - z0) * plane)
+            f.compute(ns)
+            tbr = torch.tensor(b[z0 * plane:z1 * plane], device="cuda")
+            txr = torch.zeros_like(tbr)
+            res[r] = f.gmres(tbr, txr, 60, 1e-6, 2000, nt) + (txr.cpu().numpy(),)
+            f.close()
+        except Exception as e:
+            errs[r] = e
+
+    th = [threading.Thread(target=worker, args=(r,), daemon=True) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    F.fastilu_group_destroy(grp)
+    for e in errs:
+        if e is not None:
+            raise e
+    its = {r[0] for r in res}
+    assert len(its) == 1, its  # every rank ran the same iterations
+    itP, rrP = res[0][0], res[0][1]
+    assert rr1 <= 1e-6 and rrP <= 1e-6 and abs(itP - it1) <= 1, (itP, it1)
+    x = np.concatenate([r[2] for r in res])
+    assert np.linalg.norm(b - oracle.spmv(a, x)) <= 1e-6 * np.linalg.norm(b) * (1 + 1e-9)
