@@ -62,10 +62,13 @@ def bsr_roofline(info, n, sweep_ms):
 
 
 def smem_port(info, n, launch_ms, sm_mhz, sms=148):
-    """Staged template sweep: shared-memory port bytes per launch, a lower
-    bound -- one 8-byte LDS per term and row (the pivot value u_kj) plus the TMA pivot-box
-    writes (groups x box bytes per tile) -- against 128 B/clk/SM (B300_MICROARCH.md LDS/STS
-    table) x SMs x the SM clock measured in the timed region."""
+    """Staged template sweep: shared-memory port bytes per launch against
+    128 B/clk/SM (B300_MICROARCH.md LDS/STS table) x SMs x the SM clock measured in the timed
+    region.  Bytes = the distinct 8-byte shared-memory loads the generated kernel issues per row
+    (st_lds: pivot values u_kj, divisors u_jj, own l_it and own old u_ij, counted by the generator
+    over all part-warps) x n + the TMA bytes written into shared memory per tile (st_tma: pivot
+    boxes + own-row boxes) x tiles.  `lower_bound` keeps round 1's figure (one LDS per term + the
+    pivot boxes only)."""
     import re
     kv = dict(re.findall(r"(\w+)=(\S+)", info))
     if kv.get("staged") != "1" or launch_ms <= 0:
@@ -73,13 +76,18 @@ def smem_port(info, n, launch_ms, sm_mhz, sms=148):
     terms, rows = int(kv["terms"]), int(kv["st_rows"])
     bx, by, bz = (int(v) for v in kv["st_box"].split("x"))
     tiles = -(-n // rows)
-    lds = n * terms * 8
-    tma = tiles * int(kv["st_groups"]) * bx * by * bz * 8
+    lds_lb = n * terms * 8
+    tma_lb = tiles * int(kv["st_groups"]) * bx * by * bz * 8
+    lds = n * int(kv["st_lds"]) * 8 if "st_lds" in kv else lds_lb
+    tma = tiles * int(kv["st_tma"]) if "st_tma" in kv else tma_lb
     mhz = sm_mhz or 1965.0
     peak = 128 * sms * mhz * 1e6 / 1e9
     ach = (lds + tma) / (launch_ms * 1e-3) / 1e9
     return {"achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
             "bytes_per_launch": lds + tma, "lds_bytes": lds, "tma_bytes": tma,
+            "lds_per_row": int(kv.get("st_lds", terms)),
+            "lower_bound": {"bytes_per_launch": lds_lb + tma_lb,
+                            "frac": (lds_lb + tma_lb) / (launch_ms * 1e-3) / 1e9 / peak},
             "peak_source": f"128 B/clk/SM x {sms} SMs x {mhz:.0f} MHz (median SM clock, timed region)"}
 
 

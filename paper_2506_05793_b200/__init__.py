@@ -412,8 +412,8 @@ class FastILU:
 
     def info(self) -> str:
         """Kernel configuration of this handle (fastilu_get_info)."""
-        buf = C.create_string_buffer(512)
-        _check(lib().fastilu_get_info(self._h, buf, 512), "fastilu_get_info", self._h)
+        buf = C.create_string_buffer(1024)
+        _check(lib().fastilu_get_info(self._h, buf, 1024), "fastilu_get_info", self._h)
         return buf.value.decode()
 
     def close(self):

@@ -1903,7 +1903,7 @@ extern "C" fastilu_status fastilu_get_sweep_split(fastilu_handle h, double *t2) 
 
 extern "C" fastilu_status fastilu_get_info(fastilu_handle h, char *buf, int cap) {
   if (!h || !buf || cap < 1) FAIL(FASTILU_ERR_INVALID_ARG);
-  char tmp[512];
+  char tmp[1024];
   if (h->tsell)
     snprintf(tmp, sizeof(tmp),
              "path=tsell W=%d c0=%d WA=%d terms=%zu threads=%d rows/tile=%d grid=%d regs=%d "
@@ -1916,10 +1916,13 @@ extern "C" fastilu_status fastilu_get_info(fastilu_handle h, char *buf, int cap)
     snprintf(tmp + L, sizeof(tmp) - L,
              " staged=1 st_threads=%d st_parts=%d st_rows=%d st_shift=%d st_groups=%d "
              "st_box=32x%dx%d st_stages=%d st_smem_kb=%d st_grid=%d st_init=%d "
-             "st_init_parts=%d st_init_rows=%d",
+             "st_init_parts=%d st_init_rows=%d st_lds=%d st_tma=%lld st_init_lds=%d "
+             "st_init_tma=%lld",
              h->st.threads, h->st.parts, h->st.rows, h->st.shift, h->st.ngroups, h->st.box_cols,
              h->st.box_slices, h->st.stages, h->st.smem / 1024, h->st_grid,
-             h->jit_st_init ? 1 : 0, h->st_init.parts, h->st_init.rows);
+             h->jit_st_init ? 1 : 0, h->st_init.parts, h->st_init.rows, h->st.lds_per_row,
+             h->st.tma_bytes_per_tile, h->jit_st_init ? h->st_init.lds_per_row : 0,
+             h->jit_st_init ? h->st_init.tma_bytes_per_tile : 0LL);
   }
   if (h->tsell) {
   } else if (h->bsr)

@@ -52,8 +52,9 @@ int main(int argc, char **argv) {
     src = sweep_source_staged(T, threads, parts, 2, 0, true, &c, opts | kStagedFromAhat);
   else
     src = sweep_source_staged(T, threads, parts, 2, 0, false, &c, opts);
-  fprintf(stderr, "W=%d c0=%d WA=%d terms=%zu rows=%d smem=%d box=32x%dx%d own=%d\n", T.W, T.c0,
-          T.WA, T.terms.size(), c.rows, c.smem, c.box_cols, c.box_slices, c.own_cols);
+  fprintf(stderr, "W=%d c0=%d WA=%d terms=%zu rows=%d smem=%d box=32x%dx%d own=%d lds=%d tma=%lld\n", T.W, T.c0,
+          T.WA, T.terms.size(), c.rows, c.smem, c.box_cols, c.box_slices, c.own_cols, c.lds_per_row,
+          c.tma_bytes_per_tile);
   fputs(src.c_str(), stdout);
   return 0;
 }

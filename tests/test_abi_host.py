@@ -116,6 +116,12 @@ def test_bench_smem_port_bytes():
     assert abs(r["peak"] - 128 * 100 * 1000e6 / 1e9) < 1e-9
     assert abs(r["achieved"] - (r["lds_bytes"] + r["tma_bytes"]) / 1e-3 / 1e9) < 1e-6
     assert bench.smem_port("path=tsell W=7 terms=3", n, 1.0, 1000.0) is None
+    # with the generator's exact counts (distinct LDS per row over both part-warps, TMA bytes
+    # per tile incl. the own-row boxes) those replace the lower bound, which is kept alongside
+    r2 = bench.smem_port(info + " st_lds=712 st_tma=645120", n, 1.0, 1000.0, 100)
+    assert r2["lds_bytes"] == n * 712 * 8 and r2["tma_bytes"] == (n // 256) * 645120
+    assert r2["lower_bound"]["bytes_per_launch"] == r["bytes_per_launch"]
+    assert r2["frac"] > r["frac"]
 
 
 def test_binding_argument_checks():
