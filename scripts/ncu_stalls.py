@@ -21,7 +21,7 @@ for r in data:
     if len(r) < len(h):
         continue
     src = r[ix["Source"]].split()
-    if not src:
+    if not src or src[0] == "Source":  # repeated header rows (one per function)
         continue
     ninst += 1
     op = (src[1] if src[0].startswith("@") else src[0]).split(".")[0]
