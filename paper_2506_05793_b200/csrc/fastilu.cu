@@ -418,28 +418,77 @@ static fastilu_status setup_tsell(fastilu_handle h, const std::vector<unsigned l
       // ~32 targets per thread: 2 part-warps per slice for W = 63, 4 for W = 115
       const int sparts = ev_sp ? std::max(1, atoi(ev_sp)) : std::max(1, (T.W + 31) / 32);
       const char *ev_sth = std::getenv("FASTILU_TSELL_ST_THREADS");
-      // 256-row tiles (one 512-thread block per SM) for 2 parts, 128-row tiles for more
-      // (shared memory: the stage box grows with the template's upper width); measured
-      // 15.9 vs 16.8 ms (c4, 3 sweeps) and equal for ILU(2)
-      const int sthreads =
-          ev_sth ? std::max(32 * sparts, atoi(ev_sth) / (32 * sparts) * 32 * sparts)
-                 : (sparts <= 2 ? 256 * sparts : 128 * sparts);
       const char *ev_so = std::getenv("FASTILU_TSELL_ST_OPTS");
-      const unsigned sopts = (ev_so ? (unsigned)atoi(ev_so) : (kStagedFastDiv | kStagedOwnL | kStagedLastIssues)) |
-                             (h->opt.omega != 1.0 ? kStagedDamp : 0u);
+      const unsigned damp = h->opt.omega != 1.0 ? kStagedDamp : 0u;
+      const unsigned base_opts = kStagedFastDiv | kStagedOwnL | kStagedLastIssues;
+      // block shape and options of the full sweep, tried in order until one compiles and fits:
+      //  - 2 part-warps per slice (W <= 64, 27-pt ILU(1)): 256-row tiles, one 512-thread block
+      //    per SM, row-major boxes (c4 15.9 vs 16.8 ms for 3 sweeps against 128-row tiles;
+      //    column-major boxes / no presence select measured neutral to 1 % slower,
+      //    profiles/r2j_*);
+      //  - 4 part-warps (27-pt ILU(2)): 160-row tiles, one 640-thread block (20 warps; 102
+      //    registers fit because column-major boxes drop the per-pivot row-index split),
+      //    column-major boxes without the presence selects: c3b full sweep 2.00 -> 1.57 ms
+      //    (profiles/r2j_*); else 128-row tiles / 512 threads, row-major.
+      // FASTILU_TSELL_ST_THREADS / _ST_OPTS override (one candidate).
+      // candidate: {threads, options, part-warps of the two-rows-per-lane kernel (0: one row)}
+      struct Cand { int threads; unsigned opts; int pair_parts; };
+      std::vector<Cand> cands;
+      const char *ev_pair = std::getenv("FASTILU_TSELL_PAIR");  // part-warps, 0 = off
+      const int pparts = ev_pair ? atoi(ev_pair) : 0;
+      if (pparts > 0)
+        cands.push_back({ev_sth ? atoi(ev_sth) / (32 * pparts) * 32 * pparts : 512,
+                         base_opts | kStagedColMajor, pparts});
+      if (ev_sth || ev_so) {
+        const int th = ev_sth ? std::max(32 * sparts, atoi(ev_sth) / (32 * sparts) * 32 * sparts)
+                              : (sparts <= 2 ? 256 * sparts : 128 * sparts);
+        cands.push_back({th, ev_so ? (unsigned)atoi(ev_so) : base_opts, 0});
+      } else {
+        if (sparts >= 4)
+          cands.push_back({160 * sparts, base_opts | kStagedColMajor | kStagedNoLSel, 0});
+        cands.push_back({sparts <= 2 ? 256 * sparts : 128 * sparts, base_opts, 0});
+      }
       const char *ev_smb = std::getenv("FASTILU_TSELL_ST_MINB");
       const int sminb = ev_smb ? atoi(ev_smb) : 0;
       StagedCfg c{};
-      const std::string s0 =
-          sweep_source_staged(T, sthreads, sparts, nst, sminb, false, &c, sopts);
-      const std::string s1 =
-          sweep_source_staged(T, sthreads, sparts, nst, sminb, true, nullptr, sopts);
-      if (std::getenv("FASTILU_DUMP_SRC")) fprintf(stderr, "%s\n", s0.c_str());
-      int sbps = 0;
-      if (!jit_get(s0, "fastilu_tsell_sweep_st", h->device, &h->jit_st, &log) &&
-          !jit_get(s1, "fastilu_tsell_sweep_st_first", h->device, &h->jit_st_first, &log) &&
-          !jit_set_smem(h->jit_st, c.smem) && !jit_set_smem(h->jit_st_first, c.smem) &&
-          !jit_occupancy(h->jit_st, c.threads, c.smem, &sbps) && sbps > 0) {
+      int sbps = 0, sthreads = 0;
+      unsigned sopts = 0;
+      bool ok_st = false;
+      for (const auto &cd : cands) {
+        sthreads = cd.threads;
+        sopts = cd.opts | damp;
+        c = StagedCfg{};
+        std::string s0, s1;
+        if (cd.pair_parts > 0) {
+          // the two-rows kernel; sweep 1 from a stored iterate 0 keeps the one-row "first"
+          // kernel with the same box geometry (it shares the tensor maps), else the full one
+          s0 = sweep_source_pair(T, sthreads, cd.pair_parts, nst, &c, sopts);
+          if (s0.empty()) continue;
+          StagedCfg c1{};
+          s1 = sweep_source_staged(T, c.rows * sparts, sparts, nst, sminb, true, &c1, sopts);
+          if (c1.rows != c.rows || c1.box_slices != c.box_slices || c1.box_cols != c.box_cols ||
+              c1.own_cols != c.own_cols || c1.colmajor != c.colmajor || c1.smem > c.smem)
+            s1 = s0;
+        } else {
+          s0 = sweep_source_staged(T, sthreads, sparts, nst, sminb, false, &c, sopts);
+          s1 = sweep_source_staged(T, sthreads, sparts, nst, sminb, true, nullptr, sopts);
+        }
+        if (std::getenv("FASTILU_DUMP_SRC")) fprintf(stderr, "%s\n", s0.c_str());
+        sbps = 0;
+        if (!jit_get(s0, "fastilu_tsell_sweep_st", h->device, &h->jit_st, &log) &&
+            !jit_get(s1, s1 == s0 ? "fastilu_tsell_sweep_st" : "fastilu_tsell_sweep_st_first",
+                     h->device, &h->jit_st_first, &log) &&
+            !jit_set_smem(h->jit_st, c.smem) && !jit_set_smem(h->jit_st_first, c.smem) &&
+            !jit_occupancy(h->jit_st, c.threads, c.smem, &sbps) && sbps > 0) {
+          int sregs = 0, sloc = 0, dummy = 0;
+          jit_func_info(h->jit_st, &sregs, &sloc, c.threads, &dummy);
+          if (sloc == 0 || &cd == &cands.back()) {  // a spilling candidate is not taken
+            ok_st = true;
+            break;
+          }
+        }
+      }
+      if (ok_st) {
         h->st = c;
         h->st_ntiles = std::max<int64_t>(1, (h->n + c.shift + c.rows - 1) / c.rows);
         // the first sweep with the init fused in
@@ -462,8 +511,14 @@ static fastilu_status setup_tsell(fastilu_handle h, const std::vector<unsigned l
             : sparts == 2 ? 384
             : sparts >= 4 ? 512
                           : sthreads;
+        // column-major boxes for the init-fused sweep: c4 sweep 1 3.03 -> 2.94 ms, c3a 0.379
+        // -> 0.368, c3b 0.838 -> 0.828 (profiles/r2j_*); FASTILU_TSELL_INIT_OPTS overrides
+        const char *ev_io = std::getenv("FASTILU_TSELL_INIT_OPTS");
+        const unsigned iopts =
+            (ev_io ? (unsigned)atoi(ev_io)
+                   : ev_so ? (unsigned)atoi(ev_so) : (base_opts | kStagedColMajor)) | damp;
         const std::string s2 = sweep_source_staged(T, ithreads, iparts, nsi, sminb, true, &ci,
-                                                   sopts | kStagedFromAhat);
+                                                   iopts | kStagedFromAhat);
         int ibps = 0;
         if (!std::getenv("FASTILU_NO_FUSED_INIT") &&
             !jit_get(s2, "fastilu_tsell_sweep_st_init", h->device, &h->jit_st_init, &log) &&
@@ -547,24 +602,30 @@ static fastilu_status setup_tsell(fastilu_handle h, const std::vector<unsigned l
   CU(dalloc(&h->d_partials,  // +2: a split sweep has one partial tile per launch more
             std::max<int64_t>(std::max(std::max(h->t_ntiles, h->st_ntiles), h->st_init_ntiles) + 2,
                               kSumsqBlocks)));
+  // kStagedColMajor kernels take the swapped-dimension maps (box lands column-major)
+  auto tmap = [](const StagedCfg &c, void *out, const double *base, int W, long long nsl,
+                 int box_cols, int box_slices) {
+    return c.colmajor ? jit_tmap_sell_cm(out, base, W, nsl, box_cols, box_slices)
+                      : jit_tmap_sell(out, base, W, nsl, box_cols, box_slices);
+  };
   if (h->jit_st)
     for (int b = 0; b < 2; b++)
-      if (jit_tmap_sell(h->st_tmap[b].b, h->d_vals[b], T.W, h->nsl, h->st.box_cols,
-                        h->st.box_slices)) {
+      if (tmap(h->st, h->st_tmap[b].b, h->d_vals[b], T.W, h->nsl, h->st.box_cols,
+               h->st.box_slices)) {
         if (std::getenv("FASTILU_DEBUG")) fprintf(stderr, "fastilu: tensor map failed\n");
         h->jit_st = h->jit_st_first = h->jit_st_init = nullptr;
       }
-  if (h->jit_st_init && jit_tmap_sell(h->st_tmap_ahat.b, h->d_ahat, T.WA, h->nsl,
-                                      h->st_init.box_cols, h->st_init.box_slices))
+  if (h->jit_st_init && tmap(h->st_init, h->st_tmap_ahat.b, h->d_ahat, T.WA, h->nsl,
+                             h->st_init.box_cols, h->st_init.box_slices))
     h->jit_st_init = nullptr;
   // own-row boxes: {32, own_cols, rows/32} (any valid map when the kernel does not use them)
   if (h->jit_st)
     for (int b = 0; b < 2; b++)
-      if (jit_tmap_sell(h->st_tmap_own[b].b, h->d_vals[b], T.W, h->nsl,
-                        std::max(1, h->st.own_cols), h->st.rows / 32))
+      if (tmap(h->st, h->st_tmap_own[b].b, h->d_vals[b], T.W, h->nsl,
+               std::max(1, h->st.own_cols), h->st.rows / 32))
         h->jit_st = h->jit_st_first = h->jit_st_init = nullptr;
-  if (h->jit_st_init && jit_tmap_sell(h->st_tmap_own_ahat.b, h->d_ahat, T.WA, h->nsl,
-                                      std::max(1, h->st_init.own_cols), h->st_init.rows / 32))
+  if (h->jit_st_init && tmap(h->st_init, h->st_tmap_own_ahat.b, h->d_ahat, T.WA, h->nsl,
+                             std::max(1, h->st_init.own_cols), h->st_init.rows / 32))
     h->jit_st_init = nullptr;
   CU(cudaMemset(h->d_counter, 0, 2 * sizeof(unsigned int)));
   CU(cudaMemcpy(h->d_tmask, mask.data(), 8 * mask.size(), cudaMemcpyHostToDevice));
@@ -1917,12 +1978,13 @@ extern "C" fastilu_status fastilu_get_info(fastilu_handle h, char *buf, int cap)
              " staged=1 st_threads=%d st_parts=%d st_rows=%d st_shift=%d st_groups=%d "
              "st_box=32x%dx%d st_stages=%d st_smem_kb=%d st_grid=%d st_init=%d "
              "st_init_parts=%d st_init_rows=%d st_lds=%d st_tma=%lld st_init_lds=%d "
-             "st_init_tma=%lld",
+             "st_init_tma=%lld st_opts=%u st_init_opts=%u st_pair=%d",
              h->st.threads, h->st.parts, h->st.rows, h->st.shift, h->st.ngroups, h->st.box_cols,
              h->st.box_slices, h->st.stages, h->st.smem / 1024, h->st_grid,
              h->jit_st_init ? 1 : 0, h->st_init.parts, h->st_init.rows, h->st.lds_per_row,
              h->st.tma_bytes_per_tile, h->jit_st_init ? h->st_init.lds_per_row : 0,
-             h->jit_st_init ? h->st_init.tma_bytes_per_tile : 0LL);
+             h->jit_st_init ? h->st_init.tma_bytes_per_tile : 0LL, h->st.opts,
+             h->jit_st_init ? h->st_init.opts : 0u, h->st.pair);
   }
   if (h->tsell) {
   } else if (h->bsr)

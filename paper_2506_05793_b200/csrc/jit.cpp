@@ -220,6 +220,25 @@ int jit_tmap_sell(void *out, const double *base, int W, long long nsl, int box_c
              : 3;
 }
 
+int jit_tmap_sell_cm(void *out, const double *base, int W, long long nsl, int box_cols,
+                     int box_slices) {
+  Api &a = api();
+  if (!a.TensorMapEncodeTiled) return 1;
+  if ((reinterpret_cast<uintptr_t>(out) & 63) || (reinterpret_cast<uintptr_t>(base) & 15))
+    return 2;
+  const cuuint64_t dims[3] = {32, (cuuint64_t)nsl, (cuuint64_t)W};
+  const cuuint64_t strides[2] = {(cuuint64_t)W * 256, 256};
+  const cuuint32_t box[3] = {32, (cuuint32_t)box_slices, (cuuint32_t)box_cols};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return a.TensorMapEncodeTiled(reinterpret_cast<CUtensorMap *>(out),
+                                CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void *)base, dims, strides,
+                                box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS
+             ? 0
+             : 3;
+}
+
 int jit_func_info(void *fn, int *regs, int *local_bytes, int block, int *blocks_per_sm) {
   Api &a = api();
   CUfunction f = (CUfunction)fn;

@@ -31,5 +31,11 @@ int jit_occupancy(void *fn, int block, int smem, int *blocks_per_sm);
 // {32, box_cols, box_slices}; out-of-range boxes are zero-filled.  0 on success.
 int jit_tmap_sell(void *out, const double *base, int W, long long nsl, int box_cols,
                   int box_slices);
+// The same tensor over the SELL layout with the slice and column dimensions swapped (dims {32
+// rows, nsl slices, W columns}, box {32, box_slices, box_cols}): a box lands column-major in
+// shared memory, [column][slice][32 rows] (kStagedColMajor).  Swapped argument order of the box
+// coordinates in the kernel: {0, slice, column}.
+int jit_tmap_sell_cm(void *out, const double *base, int W, long long nsl, int box_cols,
+                     int box_slices);
 
 }  // namespace fastilu

@@ -354,6 +354,12 @@ _VARIANTS = [
      None),
     ("divisions through __ddiv_rn", {"FASTILU_TSELL_STAGED": "1", "FASTILU_TSELL_ST_OPTS": "0"},
      "staged=1"),
+    ("column-major boxes", {"FASTILU_TSELL_STAGED": "1", "FASTILU_TSELL_ST_OPTS": "5888"},
+     "staged=1"),
+    ("column-major boxes, no presence select on l_it / u_jj",
+     {"FASTILU_TSELL_STAGED": "1", "FASTILU_TSELL_ST_OPTS": "14080"}, "staged=1"),
+    ("no presence select, row-major boxes",
+     {"FASTILU_TSELL_STAGED": "1", "FASTILU_TSELL_ST_OPTS": "9984"}, "staged=1"),
 ]
 
 
