@@ -431,22 +431,16 @@ static fastilu_status setup_tsell(fastilu_handle h, const std::vector<unsigned l
       //    column-major boxes without the presence selects: c3b full sweep 2.00 -> 1.57 ms
       //    (profiles/r2j_*); else 128-row tiles / 512 threads, row-major.
       // FASTILU_TSELL_ST_THREADS / _ST_OPTS override (one candidate).
-      // candidate: {threads, options, part-warps of the two-rows-per-lane kernel (0: one row)}
-      struct Cand { int threads; unsigned opts; int pair_parts; };
+      struct Cand { int threads; unsigned opts; };
       std::vector<Cand> cands;
-      const char *ev_pair = std::getenv("FASTILU_TSELL_PAIR");  // part-warps, 0 = off
-      const int pparts = ev_pair ? atoi(ev_pair) : 0;
-      if (pparts > 0)
-        cands.push_back({ev_sth ? atoi(ev_sth) / (32 * pparts) * 32 * pparts : 512,
-                         base_opts | kStagedColMajor, pparts});
       if (ev_sth || ev_so) {
         const int th = ev_sth ? std::max(32 * sparts, atoi(ev_sth) / (32 * sparts) * 32 * sparts)
                               : (sparts <= 2 ? 256 * sparts : 128 * sparts);
-        cands.push_back({th, ev_so ? (unsigned)atoi(ev_so) : base_opts, 0});
+        cands.push_back({th, ev_so ? (unsigned)atoi(ev_so) : base_opts});
       } else {
         if (sparts >= 4)
-          cands.push_back({160 * sparts, base_opts | kStagedColMajor | kStagedNoLSel, 0});
-        cands.push_back({sparts <= 2 ? 256 * sparts : 128 * sparts, base_opts, 0});
+          cands.push_back({160 * sparts, base_opts | kStagedColMajor | kStagedNoLSel});
+        cands.push_back({sparts <= 2 ? 256 * sparts : 128 * sparts, base_opts});
       }
       const char *ev_smb = std::getenv("FASTILU_TSELL_ST_MINB");
       const int sminb = ev_smb ? atoi(ev_smb) : 0;
@@ -458,26 +452,14 @@ static fastilu_status setup_tsell(fastilu_handle h, const std::vector<unsigned l
         sthreads = cd.threads;
         sopts = cd.opts | damp;
         c = StagedCfg{};
-        std::string s0, s1;
-        if (cd.pair_parts > 0) {
-          // the two-rows kernel; sweep 1 from a stored iterate 0 keeps the one-row "first"
-          // kernel with the same box geometry (it shares the tensor maps), else the full one
-          s0 = sweep_source_pair(T, sthreads, cd.pair_parts, nst, &c, sopts);
-          if (s0.empty()) continue;
-          StagedCfg c1{};
-          s1 = sweep_source_staged(T, c.rows * sparts, sparts, nst, sminb, true, &c1, sopts);
-          if (c1.rows != c.rows || c1.box_slices != c.box_slices || c1.box_cols != c.box_cols ||
-              c1.own_cols != c.own_cols || c1.colmajor != c.colmajor || c1.smem > c.smem)
-            s1 = s0;
-        } else {
-          s0 = sweep_source_staged(T, sthreads, sparts, nst, sminb, false, &c, sopts);
-          s1 = sweep_source_staged(T, sthreads, sparts, nst, sminb, true, nullptr, sopts);
-        }
+        const std::string s0 =
+            sweep_source_staged(T, sthreads, sparts, nst, sminb, false, &c, sopts);
+        const std::string s1 =
+            sweep_source_staged(T, sthreads, sparts, nst, sminb, true, nullptr, sopts);
         if (std::getenv("FASTILU_DUMP_SRC")) fprintf(stderr, "%s\n", s0.c_str());
         sbps = 0;
         if (!jit_get(s0, "fastilu_tsell_sweep_st", h->device, &h->jit_st, &log) &&
-            !jit_get(s1, s1 == s0 ? "fastilu_tsell_sweep_st" : "fastilu_tsell_sweep_st_first",
-                     h->device, &h->jit_st_first, &log) &&
+            !jit_get(s1, "fastilu_tsell_sweep_st_first", h->device, &h->jit_st_first, &log) &&
             !jit_set_smem(h->jit_st, c.smem) && !jit_set_smem(h->jit_st_first, c.smem) &&
             !jit_occupancy(h->jit_st, c.threads, c.smem, &sbps) && sbps > 0) {
           int sregs = 0, sloc = 0, dummy = 0;
@@ -1978,13 +1960,13 @@ extern "C" fastilu_status fastilu_get_info(fastilu_handle h, char *buf, int cap)
              " staged=1 st_threads=%d st_parts=%d st_rows=%d st_shift=%d st_groups=%d "
              "st_box=32x%dx%d st_stages=%d st_smem_kb=%d st_grid=%d st_init=%d "
              "st_init_parts=%d st_init_rows=%d st_lds=%d st_tma=%lld st_init_lds=%d "
-             "st_init_tma=%lld st_opts=%u st_init_opts=%u st_pair=%d",
+             "st_init_tma=%lld st_opts=%u st_init_opts=%u",
              h->st.threads, h->st.parts, h->st.rows, h->st.shift, h->st.ngroups, h->st.box_cols,
              h->st.box_slices, h->st.stages, h->st.smem / 1024, h->st_grid,
              h->jit_st_init ? 1 : 0, h->st_init.parts, h->st_init.rows, h->st.lds_per_row,
              h->st.tma_bytes_per_tile, h->jit_st_init ? h->st_init.lds_per_row : 0,
              h->jit_st_init ? h->st_init.tma_bytes_per_tile : 0LL, h->st.opts,
-             h->jit_st_init ? h->st_init.opts : 0u, h->st.pair);
+             h->jit_st_init ? h->st_init.opts : 0u);
   }
   if (h->tsell) {
   } else if (h->bsr)
