@@ -136,7 +136,7 @@ cudaError_t launch_sumsq(const double *x, int64_t n, double *partials, double *d
                          cudaStream_t st);
 
 // ---- restarted GMRES building blocks (config 5)
-constexpr int kDotBlocks = 296;
+constexpr int kDotBlocks = 888;  // 6 x 148: GMRES orthogonalisation grid (max)
 // y[r - Gh] = sum_q aval[q] x[aci[q]] over owned rows [r0, r1) (x extended, local columns)
 cudaError_t launch_spmv(const int64_t *arp, const int32_t *aci, const double *aval,
                         const double *x, double *y, int64_t r0, int64_t r1, int64_t Gh, int G,
@@ -147,6 +147,11 @@ cudaError_t launch_mdot(const double *V, int64_t ldv, int k, const double *w, in
 // w += sign * sum_j c[j] V_j  (c on device)
 cudaError_t launch_maxpy(const double *V, int64_t ldv, int k, const double *c, double *w,
                          int64_t n, double sign, cudaStream_t st);
+// the same, also out[0] = ||w_new||^2 (block partials, then a fixed-order sum); partials:
+// kDotBlocks doubles
+cudaError_t launch_maxpy_nrm(const double *V, int64_t ldv, int k, const double *c, double *w,
+                             int64_t n, double sign, double *partials, double *out,
+                             cudaStream_t st);
 // y = a x + b y
 cudaError_t launch_axpby(double a, const double *x, double b, double *y, int64_t n,
                          cudaStream_t st);

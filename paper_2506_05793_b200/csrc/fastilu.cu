@@ -104,6 +104,7 @@ struct fastilu_handle_s {
   void *jit_st_init = nullptr;  // sweep 1 with iterate 0 computed from ahat (single GPU)
   void *jit_scale = nullptr, *jit_ahat = nullptr;  // template-specialised a2 / a3 (tsell)
   void *jit_jac[2] = {nullptr, nullptr};            // template-specialised a8 / a9 sweeps
+  void *jit_spmv = nullptr;                          // template-specialised y = A x (GMRES)
   StagedCfg st{}, st_init{};
   int st_grid = 0, st_init_grid = 0;
   int64_t st_ntiles = 0, st_init_ntiles = 0;
@@ -544,6 +545,12 @@ static fastilu_status setup_tsell(fastilu_handle h, const std::vector<unsigned l
     if (jit_get(jl, "fastilu_tsell_jac_L", h->device, &h->jit_jac[0], &log) ||
         jit_get(ju, "fastilu_tsell_jac_U", h->device, &h->jit_jac[1], &log))
       h->jit_jac[0] = h->jit_jac[1] = nullptr;
+  }
+  // template-specialised SpMV for GMRES (FASTILU_NO_JIT_SPMV=1 keeps the CSR kernel): the 7-pt
+  // config-5 matrix's CSR SpMV ran at ~2 TB/s (0.92 ms at 256^3, profiles/r2p_*)
+  if (!std::getenv("FASTILU_NO_JIT_SPMV") && T.c0 >= 0) {
+    if (jit_get(spmv_source(T), "fastilu_tsell_spmv", h->device, &h->jit_spmv, &log))
+      h->jit_spmv = nullptr;
   }
   int bps = 0;
   jit_func_info(h->jit_sweep, &h->t_regs, &h->t_spill, threads, &bps);
@@ -1695,8 +1702,8 @@ extern "C" fastilu_status fastilu_gmres(fastilu_handle h, const double *b, doubl
     CU(dalloc(&h->gm_u, n));
     CU(dalloc(&h->gm_r, n));
     CU(dalloc(&h->gm_part, (int64_t)(m + 2) * kDotBlocks));
-    CU(dalloc(&h->gm_c, m + 2));
-    CU(cudaMallocHost((void **)&h->gm_hbuf, sizeof(double) * (m + 2)));
+    CU(dalloc(&h->gm_c, 3 * (m + 2)));  // h1 | h2 | ||w||^2 (device-resident CGS2, 1 GPU)
+    CU(cudaMallocHost((void **)&h->gm_hbuf, sizeof(double) * 3 * (m + 2)));
     h->gm_m = m;
   }
   double *V = h->gm_V, *w = h->gm_w, *u = h->gm_u, *r = h->gm_r;
@@ -1718,6 +1725,15 @@ extern "C" fastilu_status fastilu_gmres(fastilu_handle h, const double *b, doubl
     if (h->comm) {
       fastilu_status cs = comm_vector_halo(h->comm, h->gm_ext, st, true, true);
       if (cs) return cs;
+    }
+    if (h->tsell && h->jit_spmv) {
+      const double *aT = h->d_aT, *xe = h->gm_ext;
+      const unsigned long long *mk = h->d_tmask;
+      long long a0 = h->G, a1 = h->G + n, gh = h->G;
+      void *args[] = {&aT, &mk, &xe, &y, &a0, &a1, &gh};
+      if (n > 0 && jit_launch(h->jit_spmv, (int)((n + 255) / 256), 256, st, args))
+        FAIL(FASTILU_ERR_CUDA);
+      return FASTILU_OK;
     }
     CU(launch_spmv(h->d_arp, h->d_aci, h->d_aval, h->gm_ext, y, h->G, h->G + n, h->G, h->G_spmv,
                    st));
@@ -1745,18 +1761,39 @@ extern "C" fastilu_status fastilu_gmres(fastilu_handle h, const double *b, doubl
     for (; j < m && total < max_iters; j++) {
       if ((fs = apply_impl(h, V + j * ldv, u, ntrisweeps))) return fs;  // u = M^-1 V_j
       if ((fs = spmv(u, w))) return fs;                                   // w = A u
-      if ((fs = dots(j + 1, V, w, hv.data()))) return fs;                 // CGS pass 1
-      for (int q = 0; q <= j; q++) h->gm_hbuf[q] = hv[q];
-      CU(cudaMemcpyAsync(h->gm_c, h->gm_hbuf, sizeof(double) * (j + 1), cudaMemcpyHostToDevice,
-                         st));
-      CU(launch_maxpy(V, ldv, j + 1, h->gm_c, w, n, -1.0, st));
-      if ((fs = dots(j + 1, V, w, h2.data()))) return fs;                 // CGS pass 2
-      for (int q = 0; q <= j; q++) h->gm_hbuf[q] = h2[q];
-      CU(cudaMemcpyAsync(h->gm_c, h->gm_hbuf, sizeof(double) * (j + 1), cudaMemcpyHostToDevice,
-                         st));
-      CU(launch_maxpy(V, ldv, j + 1, h->gm_c, w, n, -1.0, st));
       double hn = 0.0;
-      if ((fs = nrm(w, &hn))) return fs;
+      if (!h->comm) {
+        // one GPU: the projections stay on the device (h1 -> maxpy -> h2 -> maxpy with the
+        // norm fused), the host reads h1, h2, ||w||^2 after ONE synchronisation per iteration
+        double *c1 = h->gm_c, *c2 = h->gm_c + (m + 2), *c3 = h->gm_c + 2 * (m + 2);
+        double *b1 = h->gm_hbuf, *b2 = h->gm_hbuf + (m + 2), *b3 = h->gm_hbuf + 2 * (m + 2);
+        const size_t kb = sizeof(double) * (j + 1);
+        CU(launch_mdot(V, ldv, j + 1, w, n, h->gm_part, c1, st));          // CGS pass 1
+        CU(cudaMemcpyAsync(b1, c1, kb, cudaMemcpyDeviceToHost, st));
+        CU(launch_maxpy(V, ldv, j + 1, c1, w, n, -1.0, st));
+        CU(launch_mdot(V, ldv, j + 1, w, n, h->gm_part, c2, st));          // CGS pass 2
+        CU(cudaMemcpyAsync(b2, c2, kb, cudaMemcpyDeviceToHost, st));
+        CU(launch_maxpy_nrm(V, ldv, j + 1, c2, w, n, -1.0, h->gm_part, c3, st));
+        CU(cudaMemcpyAsync(b3, c3, sizeof(double), cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+        for (int q = 0; q <= j; q++) {
+          hv[q] = b1[q];
+          h2[q] = b2[q];
+        }
+        hn = std::sqrt(b3[0]);
+      } else {
+        if ((fs = dots(j + 1, V, w, hv.data()))) return fs;                 // CGS pass 1
+        for (int q = 0; q <= j; q++) h->gm_hbuf[q] = hv[q];
+        CU(cudaMemcpyAsync(h->gm_c, h->gm_hbuf, sizeof(double) * (j + 1), cudaMemcpyHostToDevice,
+                           st));
+        CU(launch_maxpy(V, ldv, j + 1, h->gm_c, w, n, -1.0, st));
+        if ((fs = dots(j + 1, V, w, h2.data()))) return fs;                 // CGS pass 2
+        for (int q = 0; q <= j; q++) h->gm_hbuf[q] = h2[q];
+        CU(cudaMemcpyAsync(h->gm_c, h->gm_hbuf, sizeof(double) * (j + 1), cudaMemcpyHostToDevice,
+                           st));
+        CU(launch_maxpy(V, ldv, j + 1, h->gm_c, w, n, -1.0, st));
+        if ((fs = nrm(w, &hn))) return fs;
+      }
       for (int q = 0; q <= j; q++) H[(size_t)q * m + j] = hv[q] + h2[q];
       H[(size_t)(j + 1) * m + j] = hn;
       if (hn > 0.0) CU(launch_axpby(1.0 / hn, w, 0.0, V + (j + 1) * ldv, n, st));

@@ -918,39 +918,49 @@ cudaError_t launch_spmv(const int64_t *arp, const int32_t *aci, const double *av
   return cudaGetLastError();
 }
 
-// block b of the grid reduces its row range of every V_j . w (rows strided by the grid)
+// GMRES orthogonalisation (Sec. 7b), HBM-bound: every kernel reads each V_j it needs once.
+// mdot: block b owns chunks of kChunk rows (kRpt rows per thread, 256-row stride); the chunk's w
+// values stay in registers while the block walks j = 0..k-1 (one coalesced read of V_j per
+// chunk), each warp reduces its V_j . w share by shuffles into its own shared-memory slot
+// (fixed order: deterministic), and the block's k partials go to partials[j * grid + b].
+constexpr int kRpt = 8, kChunk = 256 * kRpt, kMaxK = 128;
+static unsigned orth_blocks(int64_t n) {
+  const int64_t chunks = (n + kChunk - 1) / kChunk;
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(chunks, kDotBlocks));
+}
+
 __global__ void __launch_bounds__(256)
 mdot_kernel(const double *__restrict__ V, int64_t ldv, int k, const double *__restrict__ w,
             int64_t n, double *__restrict__ partials) {
-  __shared__ double red[8][64];
+  __shared__ double red[8][kMaxK];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int j0 = 0; j0 < k; j0 += 64) {
-    const int kk = min(64, k - j0);
-    double acc[8];
-    for (int jb = 0; jb < kk; jb += 8) {
+  for (int j = threadIdx.x; j < 8 * kMaxK; j += blockDim.x) (&red[0][0])[j] = 0.0;
+  __syncthreads();
+  for (int64_t c0 = (int64_t)blockIdx.x * kChunk; c0 < n; c0 += (int64_t)gridDim.x * kChunk) {
+    double wv[kRpt];
 #pragma unroll
-      for (int q = 0; q < 8; q++) acc[q] = 0.0;
-      for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-           i += (int64_t)gridDim.x * blockDim.x) {
-        const double wi = w[i];
-#pragma unroll
-        for (int q = 0; q < 8; q++)
-          if (jb + q < kk) acc[q] = fma(V[(int64_t)(j0 + jb + q) * ldv + i], wi, acc[q]);
-      }
-#pragma unroll
-      for (int q = 0; q < 8; q++) {
-        double v = acc[q];
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-        if (lane == 0 && jb + q < kk) red[warp][jb + q] = v;
-      }
+    for (int r = 0; r < kRpt; r++) {
+      const int64_t i = c0 + r * 256 + threadIdx.x;
+      wv[r] = i < n ? w[i] : 0.0;
     }
-    __syncthreads();
-    for (int j = threadIdx.x; j < kk; j += blockDim.x) {
-      double t = 0.0;
-      for (int q = 0; q < (int)(blockDim.x >> 5); q++) t += red[q][j];
-      partials[(int64_t)(j0 + j) * gridDim.x + blockIdx.x] = t;
+#pragma unroll 2
+    for (int j = 0; j < k; j++) {
+      const double *vj = V + (int64_t)j * ldv;
+      double a = 0.0;
+#pragma unroll
+      for (int r = 0; r < kRpt; r++) {
+        const int64_t i = c0 + r * 256 + threadIdx.x;
+        if (i < n) a = fma(vj[i], wv[r], a);
+      }
+      for (int o = 16; o > 0; o >>= 1) a += __shfl_down_sync(0xffffffffu, a, o);
+      if (lane == 0) red[warp][j] += a;
     }
-    __syncthreads();
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < k; j += blockDim.x) {
+    double t = 0.0;
+    for (int q = 0; q < 8; q++) t += red[q][j];
+    partials[(int64_t)j * gridDim.x + blockIdx.x] = t;
   }
 }
 
@@ -974,29 +984,75 @@ __global__ void mdot_reduce_kernel(const double *__restrict__ partials, int nb, 
 cudaError_t launch_mdot(const double *V, int64_t ldv, int k, const double *w, int64_t n,
                         double *partials, double *out, cudaStream_t st) {
   if (k <= 0) return cudaSuccess;
-  mdot_kernel<<<kDotBlocks, 256, 0, st>>>(V, ldv, k, w, n, partials);
-  mdot_reduce_kernel<<<min(k, 64), 256, 0, st>>>(partials, kDotBlocks, k, out);
+  if (k > kMaxK) return cudaErrorInvalidValue;
+  const unsigned nb = orth_blocks(n);
+  mdot_kernel<<<nb, 256, 0, st>>>(V, ldv, k, w, n, partials);
+  mdot_reduce_kernel<<<min(k, 64), 256, 0, st>>>(partials, (int)nb, k, out);
   return cudaGetLastError();
 }
 
-__global__ void maxpy_kernel(const double *__restrict__ V, int64_t ldv, int k,
-                             const double *__restrict__ c, double *__restrict__ w, int64_t n,
-                             double sign) {
-  __shared__ double sc[128];
-  for (int j = threadIdx.x; j < k && j < 128; j += blockDim.x) sc[j] = sign * c[j];
+// w -= sign-scaled V c over kRpt rows per thread (independent FMA chains, the loads of a column
+// issued together); with `partials`, also the block's share of ||w_new||^2 (deterministic: warp
+// shuffles, then a fixed-order sum over the block's warps) for the Arnoldi norm.
+__global__ void __launch_bounds__(256)
+maxpy_kernel(const double *__restrict__ V, int64_t ldv, int k, const double *__restrict__ c,
+             double *__restrict__ w, int64_t n, double sign, double *__restrict__ partials) {
+  __shared__ double sc[kMaxK];
+  __shared__ double red[8];
+  for (int j = threadIdx.x; j < k && j < kMaxK; j += blockDim.x) sc[j] = sign * c[j];
   __syncthreads();
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    double t = w[i];
-    for (int j = 0; j < k; j++) t = fma(sc[j], V[(int64_t)j * ldv + i], t);
-    w[i] = t;
+  double nrm = 0.0;
+  for (int64_t c0 = (int64_t)blockIdx.x * kChunk; c0 < n; c0 += (int64_t)gridDim.x * kChunk) {
+    double t[kRpt];
+#pragma unroll
+    for (int r = 0; r < kRpt; r++) {
+      const int64_t i = c0 + r * 256 + threadIdx.x;
+      t[r] = i < n ? w[i] : 0.0;
+    }
+#pragma unroll 4
+    for (int j = 0; j < k; j++) {
+      const double *vj = V + (int64_t)j * ldv;
+      const double cj = sc[j];
+#pragma unroll
+      for (int r = 0; r < kRpt; r++) {
+        const int64_t i = c0 + r * 256 + threadIdx.x;
+        if (i < n) t[r] = fma(cj, vj[i], t[r]);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < kRpt; r++) {
+      const int64_t i = c0 + r * 256 + threadIdx.x;
+      if (i < n) {
+        w[i] = t[r];
+        nrm = fma(t[r], t[r], nrm);
+      }
+    }
+  }
+  if (!partials) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int o = 16; o > 0; o >>= 1) nrm += __shfl_down_sync(0xffffffffu, nrm, o);
+  if (lane == 0) red[warp] = nrm;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tt = 0.0;
+    for (int q = 0; q < 8; q++) tt += red[q];
+    partials[blockIdx.x] = tt;
   }
 }
 
 cudaError_t launch_maxpy(const double *V, int64_t ldv, int k, const double *c, double *w,
                          int64_t n, double sign, cudaStream_t st) {
   if (k <= 0) return cudaSuccess;
-  maxpy_kernel<<<vec_blocks(n), 256, 0, st>>>(V, ldv, k, c, w, n, sign);
+  maxpy_kernel<<<orth_blocks(n), 256, 0, st>>>(V, ldv, k, c, w, n, sign, nullptr);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_maxpy_nrm(const double *V, int64_t ldv, int k, const double *c, double *w,
+                             int64_t n, double sign, double *partials, double *out,
+                             cudaStream_t st) {
+  const unsigned nb = orth_blocks(n);
+  maxpy_kernel<<<nb, 256, 0, st>>>(V, ldv, k, c, w, n, sign, partials);
+  mdot_reduce_kernel<<<1, 256, 0, st>>>(partials, (int)nb, 1, out);
   return cudaGetLastError();
 }
 
