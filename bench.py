@@ -297,6 +297,13 @@ def run_reference(args, wl):
     print(json.dumps(line), flush=True)
 
 
+def _reorth(f):
+    """Second Gram-Schmidt passes the last GMRES took (DGKS criterion)."""
+    import re
+    m = re.search(r"gmres_reorth=(\d+)", f.info())
+    return int(m.group(1)) if m else None
+
+
 def gmres_arms(args, f, a, ns, stream):
     """BASELINE configs[4] (config 5): FastILU-preconditioned GMRES(60) to a 1e-6 relative
     residual, x0 = 0, b = A x_true with x_true ~ U[0,1) (SURVEY 8(d) "Config 5
@@ -324,7 +331,8 @@ def gmres_arms(args, f, a, ns, stream):
         e1.record(stream)
         torch.cuda.synchronize()
         out["arms"].append({"arm": "A", "ntri": nt, "iterations": it, "relres": rr,
-                            "time_to_solution_ms": e0.elapsed_time(e1)})
+                            "time_to_solution_ms": e0.elapsed_time(e1),
+                            "reorth_passes": _reorth(f)})
     torch.cuda.synchronize()
     e0.record(stream)
     s_fix = f.compute_tol(1e-14, 5000)
@@ -339,7 +347,8 @@ def gmres_arms(args, f, a, ns, stream):
         e1.record(stream)
         torch.cuda.synchronize()
         out["arms"].append({"arm": "B", "ntri": nt, "iterations": it, "relres": rr,
-                            "time_to_solution_ms": e0.elapsed_time(e1)})
+                            "time_to_solution_ms": e0.elapsed_time(e1),
+                            "reorth_passes": _reorth(f)})
     return out, b
 
 

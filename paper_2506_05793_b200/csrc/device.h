@@ -141,9 +141,11 @@ constexpr int kDotBlocks = 888;  // 6 x 148: GMRES orthogonalisation grid (max)
 cudaError_t launch_spmv(const int64_t *arp, const int32_t *aci, const double *aval,
                         const double *x, double *y, int64_t r0, int64_t r1, int64_t Gh, int G,
                         cudaStream_t st);
-// out[j] = V_j . w for j < k (V_j = V + j ldv); partials: k * kDotBlocks doubles; out on device
+// out[j] = V_j . w for j < k (V_j = V + j ldv), and out[k] = extra . w when extra is given (same
+// pass); partials: (k + 1) * kDotBlocks doubles; out on device
 cudaError_t launch_mdot(const double *V, int64_t ldv, int k, const double *w, int64_t n,
-                        double *partials, double *out, cudaStream_t st);
+                        double *partials, double *out, cudaStream_t st,
+                        const double *extra = nullptr);
 // w += sign * sum_j c[j] V_j  (c on device)
 cudaError_t launch_maxpy(const double *V, int64_t ldv, int k, const double *c, double *w,
                          int64_t n, double sign, cudaStream_t st);

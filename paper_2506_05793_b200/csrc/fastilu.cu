@@ -119,6 +119,7 @@ struct fastilu_handle_s {
   // GMRES workspace (allocated on first use)
   double *gm_V = nullptr, *gm_w = nullptr, *gm_ext = nullptr, *gm_u = nullptr, *gm_r = nullptr;
   double *gm_part = nullptr, *gm_c = nullptr, *gm_hbuf = nullptr;  // gm_hbuf pinned host
+  int gm_reorth = 0;  // second Gram-Schmidt passes taken by the last fastilu_gmres
   int gm_m = 0, G_spmv = 32;
   ErrFlags *d_err = nullptr;
   ErrFlags *h_err = nullptr;  // pinned
@@ -1701,12 +1702,14 @@ extern "C" fastilu_status fastilu_gmres(fastilu_handle h, const double *b, doubl
     CU(cudaMemset(h->gm_ext, 0, sizeof(double) * h->E));
     CU(dalloc(&h->gm_u, n));
     CU(dalloc(&h->gm_r, n));
-    CU(dalloc(&h->gm_part, (int64_t)(m + 2) * kDotBlocks));
+    CU(dalloc(&h->gm_part, (int64_t)(m + 3) * kDotBlocks));
     CU(dalloc(&h->gm_c, 3 * (m + 2)));  // h1 | h2 | ||w||^2 (device-resident CGS2, 1 GPU)
     CU(cudaMallocHost((void **)&h->gm_hbuf, sizeof(double) * 3 * (m + 2)));
     h->gm_m = m;
   }
   double *V = h->gm_V, *w = h->gm_w, *u = h->gm_u, *r = h->gm_r;
+  const bool gmres_cgs2 = std::getenv("FASTILU_GMRES_CGS2") != nullptr;
+  h->gm_reorth = 0;
   const int64_t ldv = std::max<int64_t>(n, 1);
   // collective dot products: k local partial sums -> host -> sum over ranks
   auto dots = [&](int k, const double *vecs, const double *vec, double *out) -> fastilu_status {
@@ -1763,24 +1766,36 @@ extern "C" fastilu_status fastilu_gmres(fastilu_handle h, const double *b, doubl
       if ((fs = spmv(u, w))) return fs;                                   // w = A u
       double hn = 0.0;
       if (!h->comm) {
-        // one GPU: the projections stay on the device (h1 -> maxpy -> h2 -> maxpy with the
-        // norm fused), the host reads h1, h2, ||w||^2 after ONE synchronisation per iteration
+        // one GPU: classical Gram-Schmidt with the projections kept on the device and a second
+        // pass only when the first one cancelled (||w'|| < ||w|| / sqrt 2: the Daniel-Gragg-
+        // Kaufman-Stewart criterion, "twice is enough"), so most iterations read V twice and
+        // synchronise once: pass 1 = h1 = V^T w together with ||w||^2, then w -= V h1 with
+        // ||w||^2 fused; FASTILU_GMRES_CGS2=1 always reorthogonalises
         double *c1 = h->gm_c, *c2 = h->gm_c + (m + 2), *c3 = h->gm_c + 2 * (m + 2);
         double *b1 = h->gm_hbuf, *b2 = h->gm_hbuf + (m + 2), *b3 = h->gm_hbuf + 2 * (m + 2);
         const size_t kb = sizeof(double) * (j + 1);
-        CU(launch_mdot(V, ldv, j + 1, w, n, h->gm_part, c1, st));          // CGS pass 1
-        CU(cudaMemcpyAsync(b1, c1, kb, cudaMemcpyDeviceToHost, st));
-        CU(launch_maxpy(V, ldv, j + 1, c1, w, n, -1.0, st));
-        CU(launch_mdot(V, ldv, j + 1, w, n, h->gm_part, c2, st));          // CGS pass 2
-        CU(cudaMemcpyAsync(b2, c2, kb, cudaMemcpyDeviceToHost, st));
-        CU(launch_maxpy_nrm(V, ldv, j + 1, c2, w, n, -1.0, h->gm_part, c3, st));
+        CU(launch_mdot(V, ldv, j + 1, w, n, h->gm_part, c1, st, w));       // CGS pass 1
+        CU(cudaMemcpyAsync(b1, c1, kb + sizeof(double), cudaMemcpyDeviceToHost, st));
+        CU(launch_maxpy_nrm(V, ldv, j + 1, c1, w, n, -1.0, h->gm_part, c3, st));
         CU(cudaMemcpyAsync(b3, c3, sizeof(double), cudaMemcpyDeviceToHost, st));
         CU(cudaStreamSynchronize(st));
         for (int q = 0; q <= j; q++) {
           hv[q] = b1[q];
-          h2[q] = b2[q];
+          h2[q] = 0.0;
         }
-        hn = std::sqrt(b3[0]);
+        const double wn2 = b1[j + 1];
+        double hn2 = b3[0];
+        if (hn2 < 0.5 * wn2 || gmres_cgs2) {                              // CGS pass 2
+          CU(launch_mdot(V, ldv, j + 1, w, n, h->gm_part, c2, st));
+          CU(cudaMemcpyAsync(b2, c2, kb, cudaMemcpyDeviceToHost, st));
+          CU(launch_maxpy_nrm(V, ldv, j + 1, c2, w, n, -1.0, h->gm_part, c3, st));
+          CU(cudaMemcpyAsync(b3, c3, sizeof(double), cudaMemcpyDeviceToHost, st));
+          CU(cudaStreamSynchronize(st));
+          for (int q = 0; q <= j; q++) h2[q] = b2[q];
+          hn2 = b3[0];
+          h->gm_reorth++;
+        }
+        hn = std::sqrt(hn2);
       } else {
         if ((fs = dots(j + 1, V, w, hv.data()))) return fs;                 // CGS pass 1
         for (int q = 0; q <= j; q++) h->gm_hbuf[q] = hv[q];
@@ -2022,6 +2037,10 @@ extern "C" fastilu_status fastilu_get_info(fastilu_handle h, char *buf, int cap)
     const size_t L = strlen(tmp);
     snprintf(tmp + L, sizeof(tmp) - L, " nranks=%d halo_bytes=%lld", h->opt.nranks,
              (long long)comm_halo_bytes(h->comm, h->tsell ? h->T.W : 0, h->tsell ? h->T.c0 : 0));
+  }
+  {
+    const size_t L = strlen(tmp);
+    snprintf(tmp + L, sizeof(tmp) - L, " gmres_reorth=%d", h->gm_reorth);
   }
   snprintf(buf, cap, "%s", tmp);
   return FASTILU_OK;

@@ -930,8 +930,8 @@ static unsigned orth_blocks(int64_t n) {
 }
 
 __global__ void __launch_bounds__(256)
-mdot_kernel(const double *__restrict__ V, int64_t ldv, int k, const double *__restrict__ w,
-            int64_t n, double *__restrict__ partials) {
+mdot_kernel(const double *__restrict__ V, int64_t ldv, int k, const double *__restrict__ extra,
+            const double *__restrict__ w, int64_t n, double *__restrict__ partials) {
   __shared__ double red[8][kMaxK];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int j = threadIdx.x; j < 8 * kMaxK; j += blockDim.x) (&red[0][0])[j] = 0.0;
@@ -945,7 +945,7 @@ mdot_kernel(const double *__restrict__ V, int64_t ldv, int k, const double *__re
     }
 #pragma unroll 2
     for (int j = 0; j < k; j++) {
-      const double *vj = V + (int64_t)j * ldv;
+      const double *vj = (extra && j == k - 1) ? extra : V + (int64_t)j * ldv;
       double a = 0.0;
 #pragma unroll
       for (int r = 0; r < kRpt; r++) {
@@ -982,12 +982,13 @@ __global__ void mdot_reduce_kernel(const double *__restrict__ partials, int nb, 
 }
 
 cudaError_t launch_mdot(const double *V, int64_t ldv, int k, const double *w, int64_t n,
-                        double *partials, double *out, cudaStream_t st) {
+                        double *partials, double *out, cudaStream_t st, const double *extra) {
   if (k <= 0) return cudaSuccess;
-  if (k > kMaxK) return cudaErrorInvalidValue;
+  const int kk = k + (extra ? 1 : 0);  // out[k] = extra . w
+  if (kk > kMaxK) return cudaErrorInvalidValue;
   const unsigned nb = orth_blocks(n);
-  mdot_kernel<<<nb, 256, 0, st>>>(V, ldv, k, w, n, partials);
-  mdot_reduce_kernel<<<min(k, 64), 256, 0, st>>>(partials, (int)nb, k, out);
+  mdot_kernel<<<nb, 256, 0, st>>>(V, ldv, kk, extra, w, n, partials);
+  mdot_reduce_kernel<<<min(kk, 64), 256, 0, st>>>(partials, (int)nb, kk, out);
   return cudaGetLastError();
 }
 

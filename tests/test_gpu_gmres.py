@@ -31,6 +31,30 @@ def test_gmres_matches_oracle(g, ns, nt):
     assert np.linalg.norm(b - oracle.spmv(a, x)) <= 1e-6 * np.linalg.norm(b) * (1 + 1e-9)
 
 
+@pytest.mark.parametrize("cgs2", ["0", "1"])
+def test_gmres_selective_reorthogonalisation(cgs2, monkeypatch):
+    """One GPU: the second Gram-Schmidt pass runs only when the first cancelled (DGKS criterion,
+    DESIGN.md Sec. 7b); FASTILU_GMRES_CGS2=1 always runs it.  Both match the oracle's MGS
+    iteration count within one; the always-CGS2 run reports one pass per iteration."""
+    if cgs2 == "1":
+        monkeypatch.setenv("FASTILU_GMRES_CGS2", "1")
+    a = P.aniso3d_7pt(32)
+    b = oracle.spmv(a, P.x_true(a.n))
+    f = F.FastILU(a.row_ptr, a.col_idx, a.values, 0)
+    f.compute(2)
+    tb = torch.tensor(b, device="cuda")
+    tx = torch.zeros_like(tb)
+    it, rr = f.gmres(tb, tx, restart=20, rtol=1e-8, max_iters=2000, ntrisweeps=3)
+    fo = oracle.compute(a, 0, 2)
+    _, it_o, rr_o = oracle.gmres(a, b, oracle.fastilu_preconditioner(fo, 3), 20, 1e-8, 2000)
+    assert rr <= 1e-8 and abs(it - it_o) <= 1, (it, it_o)
+    reorth = int(f.info().split("gmres_reorth=")[1].split()[0])
+    if cgs2 == "1":
+        assert reorth == it
+    else:
+        assert 0 <= reorth < it
+
+
 def test_gmres_27pt_ilu1_restarts():
     a = P.laplace3d_27pt(20)
     b = oracle.spmv(a, P.x_true(a.n))
