@@ -10,7 +10,10 @@
 #   launches   ncu launch list of one c4 step (per-kernel times)          -> TAG_launches.csv
 #   full       ncu --set full of the step's kernels (-c $NCU_COUNT)       -> TAG_full.ncu-rep
 #   sanitize   compute-sanitizer memcheck/racecheck/synccheck/initcheck on a small ragged grid
-#   ab         A/B of env settings: AB_ENVS="A=1 B=2;A=0" over $WORKLOADS
+#   ab         A/B of env settings: AB_ENVS="A=1 B=2;A=0" over $WORKLOADS (each log line is
+#              preceded by "== workload env"; the round-2 A/B logs under profiles/ keep them)
+#   variants   the template-kernel variant parity tests only (bitwise vs the oracle)
+#   gmres      ncu launch list (time + DRAM bytes) of one GMRES(60) cycle on config 5
 set -u
 TAG=$1; shift
 mkdir -p gpurun_out
@@ -48,6 +51,13 @@ for step in "$@"; do
         echo "== $tool"
         timeout 900 compute-sanitizer --tool $tool --print-limit 20 python tests/sanitize_case.py 2>&1 | tail -25
       done > gpurun_out/${TAG}_sanitize.log 2>&1 ;;
+    variants)
+      timeout 1500 python -m pytest tests/test_gpu_parity.py -q -x -k "variants" 2>&1 | tail -4 \
+        > gpurun_out/${TAG}_variants.log ;;
+    gmres)
+      timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
+        --clock-control none --csv --log-file gpurun_out/${TAG}_gmres_launches.csv \
+        python scripts/profile_gmres.py --iters 60 > gpurun_out/${TAG}_gmres.log 2>&1 ;;
     ab)
       IFS=';' read -ra envs <<< "${AB_ENVS:-}"
       for w in ${WORKLOADS:-c3a_27pt_128_ilu1 c3b_27pt_128_ilu2 c4_27pt_256_ilu1}; do

@@ -45,7 +45,8 @@ int main(int argc, char **argv) {
   if (!build_template(S.rp, S.ci, n, rp, ci, 8, T, mask, asrc)) return 2;
   StagedCfg c{};
   std::string src;
-  const unsigned opts = kStagedFastDiv | kStagedOwnL | kStagedLastIssues;
+  const unsigned opts = getenv("OPTS") ? (unsigned)atoi(getenv("OPTS"))
+                                       : (kStagedFastDiv | kStagedOwnL | kStagedLastIssues);
   if (!strcmp(mode, "async"))
     src = sweep_source(T, threads, parts, 0, true, false, false, true);
   else if (!strcmp(mode, "init"))
