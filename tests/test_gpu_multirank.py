@@ -170,6 +170,66 @@ def test_partition_128_four_ranks_bitwise(overlap, monkeypatch):
     assert hb[0] == 128 * 128 * 32 * 8, hb  # G = one plane (the lowest neighbour is -g^2)
 
 
+def test_partition_256_two_ranks_x_bitwise():
+    """The bench workload (c4: 27-pt 256^3 ILU(1), 3 sweeps + 5/5 Jacobi sweeps) split into two
+    in-process ranks of 128 planes: x (which depends on every factor entry) and the residual
+    history equal the single-GPU run's bitwise / to rounding of the rank-ordered sum.  Only x
+    and the histories come back to the host (the factors are 8 GB)."""
+    kind, g, gz, k, ns, nt, world = "27pt", 256, 256, 1, 3, 5, 2
+    a = P.make(kind, g, gz)
+    b = P.rhs_positive(a.n)
+    f1 = F.FastILU(a.row_ptr, a.col_idx, a.values, k)
+    f1.compute(ns)
+    tb = torch.tensor(b, device="cuda")
+    tx = torch.empty_like(tb)
+    f1.apply(tb, tx, nt)
+    torch.cuda.synchronize()
+    x1 = tx.cpu().numpy()
+    r1 = f1.residual_history()
+    f1.close()
+    del a, tb, tx
+    torch.cuda.empty_cache()
+    plane = g * g
+    grp = F.fastilu_group_create(world)
+    out, errs = [None] * world, [None] * world
+
+    def worker(r):
+        try:
+            torch.cuda.set_device(0)
+            z0, z1 = split_planes(gz, world)[r]
+            need = F.fastilu_required_lead_rows(P.bandwidth(kind, g), k)
+            lp = min(z0, -(-need // plane))
+            blk = P.make(kind, g, gz, planes=(z0 - lp, z1))
+            f = F.FastILU(blk.row_ptr, blk.col_idx, blk.values, k, rank=r, nranks=world,
+                          comm_kind=F.COMM_LOCAL, group=grp, global_n=plane * gz,
+                          row_begin=z0 * plane, n_lead=lp * plane, n=(z1 - z0) * plane)
+            del blk
+            f.compute(ns)
+            xb = torch.tensor(b[z0 * plane:z1 * plane], device="cuda")
+            xr = torch.empty_like(xb)
+            f.apply(xb, xr, nt)
+            torch.cuda.synchronize()
+            out[r] = (xr.cpu().numpy(), f.residual_history(), f.info())
+            f.close()
+        except Exception as e:  # surfaced below
+            errs[r] = e
+
+    th = [threading.Thread(target=worker, args=(r,), daemon=True) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=900)
+    assert not any(t.is_alive() for t in th), "rank threads hung"
+    F.fastilu_group_destroy(grp)
+    for e in errs:
+        if e is not None:
+            raise e
+    assert all("staged=1" in o[2] for o in out)
+    assert np.array_equal(np.concatenate([o[0] for o in out]), x1)
+    for o in out:
+        np.testing.assert_allclose(o[1], r1, rtol=1e-12)
+
+
 def test_nccl_two_processes():
     """The NCCL transport across two GPUs (one process per GPU, torchrun): factors and x of a
     2-rank run are bitwise the single-GPU run's.  Skips on a box with fewer than 2 GPUs."""
