@@ -55,61 +55,20 @@ static __device__ __forceinline__ void st_block(double *__restrict__ p, const do
   for (int h = 0; h < ST / 2; h++) q[h] = make_double2(v[2 * h], 2 * h + 1 < BB ? v[2 * h + 1] : 0.0);
 }
 
-// One CTA takes tiles of blockDim.x consecutive target blocks (grid-stride over tiles).  With
-// STAGE, the tile's block rows (all their blocks, iterate s-1) are first copied to shared memory
-// when they fit in smem_blocks: the L blocks (I,K) every target of row I reads, the target's own
-// old block and the row's diagonal block then come from shared memory; only the pivots' U blocks
-// (K,J) and the divisor blocks of rows J are read from global memory.
-template <int BS, bool STAGE, int MINB>
-__global__ void __launch_bounds__(256, MINB)
-bsr_sweep_kernel(BsrDev B, const double *__restrict__ ahb, const double *__restrict__ old,
-                 double *__restrict__ out, double omega, double *__restrict__ partials,
-                 ErrFlags *err, int smem_blocks) {
+// The within-block tail terms and the update of target block b = (I, J) after its pivot-block
+// terms (accumulators a), shared by the block sweeps: L blocks divide by the old diagonal block
+// of row J, the diagonal block finishes its own LU, U blocks use the L part of row I's diagonal
+// block; residual defects into r2; the new block is stored to out.  lbase: where the tile's own
+// blocks are read (a shared-memory stage or `old`).
+template <int BS>
+static __device__ __forceinline__ void bsr_finish(const BsrDev &B, int64_t b, int I, int J,
+                                                  double (&a)[BS * BS], const double *lbase,
+                                                  const double *__restrict__ old,
+                                                  double *__restrict__ out, double omega,
+                                                  double &r2, ErrFlags *err) {
   constexpr int BB = BS * BS, ST = (BB + 1) & ~1;
-  extern __shared__ __align__(16) double sblk[];
   const bool damp = (omega != 1.0);
   const double om1 = 1.0 - omega;
-  double r2 = 0.0;
-  const int64_t ntiles = (B.nblk + blockDim.x - 1) / blockDim.x;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t b = tile * blockDim.x + threadIdx.x;
-    int64_t s0 = 0;
-    bool staged = false;
-    if (STAGE) {
-      const int64_t bf = tile * blockDim.x;
-      const int64_t bl = min(bf + (int64_t)blockDim.x, B.nblk) - 1;
-      s0 = B.bptr[B.brow[bf]];
-      const int64_t s1 = B.bptr[B.brow[bl] + 1];
-      staged = (s1 - s0) <= smem_blocks;  // uniform over the CTA
-      __syncthreads();                    // the previous tile's readers are done
-      if (staged) {
-        const double2 *src = reinterpret_cast<const double2 *>(old + s0 * ST);
-        double2 *dst = reinterpret_cast<double2 *>(sblk);
-        for (int64_t q = threadIdx.x; q < (s1 - s0) * (ST / 2); q += blockDim.x) dst[q] = src[q];
-      }
-      __syncthreads();
-    }
-    if (b >= B.nblk) continue;
-    const double *lbase = staged ? sblk - s0 * ST : old;  // blocks of the tile's rows
-    const int I = B.brow[b], J = B.bcol[b];
-    double a[BB];
-    ld_block<BB, ST>(ahb + b * ST, a);  // +0.0 for fill entries (R4)
-    const int64_t t1 = B.tptr[b + 1];
-    for (int64_t t = B.tptr[b]; t < t1; t++) {  // pivot blocks K ascending
-      const int2 pr = B.terms[t];
-      double L[BB], U[BB];
-      ld_block_any<BB, ST>(lbase + (int64_t)pr.x * ST, L);
-      ld_block<BB, ST>(old + (int64_t)pr.y * ST, U);
-#pragma unroll
-      for (int d = 0; d < BS; d++)
-#pragma unroll
-        for (int e = 0; e < BS; e++) {
-          double v = a[d * BS + e];
-#pragma unroll
-          for (int c = 0; c < BS; c++) v = __dsub_rn(v, __dmul_rn(L[d * BS + c], U[c * BS + e]));
-          a[d * BS + e] = v;
-        }
-    }
     double o[BB], nv[BB];
     ld_block_any<BB, ST>(lbase + b * ST, o);
     if (J < I) {  // L block: tail k = BS J + c, c < e; divide by u_jj of iterate s-1 (R1)
@@ -171,6 +130,62 @@ bsr_sweep_kernel(BsrDev B, const double *__restrict__ ahb, const double *__restr
         }
     }
     st_block<BB, ST>(out + b * ST, nv);
+}
+
+// One CTA takes tiles of blockDim.x consecutive target blocks (grid-stride over tiles).  With
+// STAGE, the tile's block rows (all their blocks, iterate s-1) are first copied to shared memory
+// when they fit in smem_blocks: the L blocks (I,K) every target of row I reads, the target's own
+// old block and the row's diagonal block then come from shared memory; only the pivots' U blocks
+// (K,J) and the divisor blocks of rows J are read from global memory.
+template <int BS, bool STAGE, int MINB>
+__global__ void __launch_bounds__(256, MINB)
+bsr_sweep_kernel(BsrDev B, const double *__restrict__ ahb, const double *__restrict__ old,
+                 double *__restrict__ out, double omega, double *__restrict__ partials,
+                 ErrFlags *err, int smem_blocks) {
+  constexpr int BB = BS * BS, ST = (BB + 1) & ~1;
+  extern __shared__ __align__(16) double sblk[];
+  double r2 = 0.0;
+  const int64_t ntiles = (B.nblk + blockDim.x - 1) / blockDim.x;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t b = tile * blockDim.x + threadIdx.x;
+    int64_t s0 = 0;
+    bool staged = false;
+    if (STAGE) {
+      const int64_t bf = tile * blockDim.x;
+      const int64_t bl = min(bf + (int64_t)blockDim.x, B.nblk) - 1;
+      s0 = B.bptr[B.brow[bf]];
+      const int64_t s1 = B.bptr[B.brow[bl] + 1];
+      staged = (s1 - s0) <= smem_blocks;  // uniform over the CTA
+      __syncthreads();                    // the previous tile's readers are done
+      if (staged) {
+        const double2 *src = reinterpret_cast<const double2 *>(old + s0 * ST);
+        double2 *dst = reinterpret_cast<double2 *>(sblk);
+        for (int64_t q = threadIdx.x; q < (s1 - s0) * (ST / 2); q += blockDim.x) dst[q] = src[q];
+      }
+      __syncthreads();
+    }
+    if (b >= B.nblk) continue;
+    const double *lbase = staged ? sblk - s0 * ST : old;  // blocks of the tile's rows
+    const int I = B.brow[b], J = B.bcol[b];
+    double a[BB];
+    ld_block<BB, ST>(ahb + b * ST, a);  // +0.0 for fill entries (R4)
+    const int64_t t1 = B.tptr[b + 1];
+    for (int64_t t = B.tptr[b]; t < t1; t++) {  // pivot blocks K ascending
+      const int2 pr = B.terms[t];
+      double L[BB], U[BB];
+      ld_block_any<BB, ST>(lbase + (int64_t)pr.x * ST, L);
+      ld_block<BB, ST>(old + (int64_t)pr.y * ST, U);
+#pragma unroll
+      for (int d = 0; d < BS; d++)
+#pragma unroll
+        for (int e = 0; e < BS; e++) {
+          double v = a[d * BS + e];
+#pragma unroll
+          for (int c = 0; c < BS; c++) v = __dsub_rn(v, __dmul_rn(L[d * BS + c], U[c * BS + e]));
+          a[d * BS + e] = v;
+        }
+    }
+    bsr_finish<BS>(B, b, I, J, a, lbase, old, out, omega, r2, err);
   }
   // deterministic block reduction (fixed shuffle tree, then warps in order)
   __shared__ double wsum[32];
