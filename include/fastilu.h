@@ -175,9 +175,11 @@ fastilu_status fastilu_apply_host(fastilu_handle h, const double *b, double *x, 
 
 /* FastILU-preconditioned restarted GMRES(restart) on A x = b (BASELINE config 5; the consumer of
  * apply in the paper's experiments): right preconditioning with
- * M^-1 = fastilu_apply(., ntrisweeps), x0 = 0, classical Gram-Schmidt: one GPU reorthogonalises
- * when the first pass cancelled (||w'|| < ||w||/sqrt 2; FASTILU_GMRES_CGS2=1: always; the count
- * is reported by fastilu_get_info as gmres_reorth), several ranks always; stop when
+ * M^-1 = fastilu_apply(., ntrisweeps), x0 = 0, classical Gram-Schmidt with the
+ * reorthogonalisation delayed by one iteration (DCGS2: per iteration one pass of dot products and
+ * one update pass over the Krylov basis, one synchronisation / one allreduce over ranks; every
+ * finished column is projected twice -- fastilu_get_info reports gmres_reorth, and gmres_retry
+ * for the explicit re-projections taken after a severe cancellation); stop when
  * ||b - A x|| / ||b|| <= rtol (true residual at restarts) or after max_iters inner iterations.
  * restart in [1, 120].  b, x: DEVICE arrays of the owned rows.  Needs a successful compute.
  * *iters = inner iterations, *relres = final relative residual.  Synchronises. */

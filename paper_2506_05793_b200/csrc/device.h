@@ -149,11 +149,15 @@ cudaError_t launch_mdot(const double *V, int64_t ldv, int k, const double *w, in
 // w += sign * sum_j c[j] V_j  (c on device)
 cudaError_t launch_maxpy(const double *V, int64_t ldv, int k, const double *c, double *w,
                          int64_t n, double sign, cudaStream_t st);
-// the same, also out[0] = ||w_new||^2 (block partials, then a fixed-order sum); partials:
-// kDotBlocks doubles
-cudaError_t launch_maxpy_nrm(const double *V, int64_t ldv, int k, const double *c, double *w,
-                             int64_t n, double sign, double *partials, double *out,
-                             cudaStream_t st);
+// DCGS2 (delayed reorthogonalisation) passes, u = V_p pending: out[2 j] = V_j . u and
+// out[2 j + 1] = V_j . w for j <= p (w may be null: those entries are 0); partials: 2 (p + 1)
+// * kDotBlocks doubles; out on device
+cudaError_t launch_dcgs_dot(const double *V, int64_t ldv, int p, const double *w, int64_t n,
+                            double *partials, double *out, cudaStream_t st);
+// coef (device) = [s_0..s_{p-1}, z_0..z_{p-1}, c_p, 1/rho]: V_p = (V_p - sum s_j V_j) / rho,
+// V_{p+1} = (w - sum z_j V_j - c_p V_p) / rho, in one pass over V_0..V_{p-1}
+cudaError_t launch_dcgs_update(double *V, int64_t ldv, int p, const double *coef, const double *w,
+                               int64_t n, cudaStream_t st);
 // y = a x + b y
 cudaError_t launch_axpby(double a, const double *x, double b, double *y, int64_t n,
                          cudaStream_t st);

@@ -120,6 +120,7 @@ struct fastilu_handle_s {
   double *gm_V = nullptr, *gm_w = nullptr, *gm_ext = nullptr, *gm_u = nullptr, *gm_r = nullptr;
   double *gm_part = nullptr, *gm_c = nullptr, *gm_hbuf = nullptr;  // gm_hbuf pinned host
   int gm_reorth = 0;  // second Gram-Schmidt passes taken by the last fastilu_gmres
+  int gm_retry = 0;   // DCGS2: explicit re-projections after a severe cancellation
   int gm_m = 0, G_spmv = 32;
   ErrFlags *d_err = nullptr;
   ErrFlags *h_err = nullptr;  // pinned
@@ -1675,10 +1676,11 @@ extern "C" fastilu_status fastilu_apply_host(fastilu_handle h, const double *b, 
 
 // --------------------------------------------------------------------------- GMRES (config 5)
 // Restarted GMRES(m) with right preconditioning x = M^-1 y, M^-1 = fastilu_apply (a fixed
-// linear operator: ntri Jacobi sweeps from 0), classical Gram-Schmidt with one
-// reorthogonalisation (CGS2: two batched multi-dot / multi-axpy passes per iteration instead of
-// m sequential MGS dots), Givens rotations on the host, x0 = 0, convergence on the relative
-// residual ||b - A x|| / ||b|| <= rtol.
+// linear operator: ntri Jacobi sweeps from 0), classical Gram-Schmidt with the
+// reorthogonalisation delayed by one step (DCGS2: one batched multi-dot pass and one update pass
+// over V per iteration instead of m sequential MGS dots), Givens rotations on the host, x0 = 0,
+// convergence on the relative residual ||b - A x|| / ||b|| <= rtol (
+// SPEC.md:416-456).
 extern "C" fastilu_status fastilu_gmres(fastilu_handle h, const double *b, double *x,
                                         int restart, double rtol, int max_iters,
                                         int ntrisweeps, int *iters_out, double *relres_out) {
@@ -1702,14 +1704,17 @@ extern "C" fastilu_status fastilu_gmres(fastilu_handle h, const double *b, doubl
     CU(cudaMemset(h->gm_ext, 0, sizeof(double) * h->E));
     CU(dalloc(&h->gm_u, n));
     CU(dalloc(&h->gm_r, n));
-    CU(dalloc(&h->gm_part, (int64_t)(m + 3) * kDotBlocks));
-    CU(dalloc(&h->gm_c, 3 * (m + 2)));  // h1 | h2 | ||w||^2 (device-resident CGS2, 1 GPU)
-    CU(cudaMallocHost((void **)&h->gm_hbuf, sizeof(double) * 3 * (m + 2)));
+    CU(dalloc(&h->gm_part, (int64_t)2 * (m + 3) * kDotBlocks));
+    // dots (2 (m + 2)) | coefficients (2 (m + 2))
+    CU(dalloc(&h->gm_c, 4 * (m + 2)));
+    CU(cudaMallocHost((void **)&h->gm_hbuf, sizeof(double) * 4 * (m + 2)));
     h->gm_m = m;
   }
   double *V = h->gm_V, *w = h->gm_w, *u = h->gm_u, *r = h->gm_r;
-  const bool gmres_cgs2 = std::getenv("FASTILU_GMRES_CGS2") != nullptr;
+  // test hook: re-project every pending vector explicitly once (the severe-cancellation branch)
+  const bool force_reproject = std::getenv("FASTILU_GMRES_FORCE_REPROJECT") != nullptr;
   h->gm_reorth = 0;
+  h->gm_retry = 0;
   const int64_t ldv = std::max<int64_t>(n, 1);
   // collective dot products: k local partial sums -> host -> sum over ranks
   auto dots = [&](int k, const double *vecs, const double *vec, double *out) -> fastilu_status {
@@ -1755,100 +1760,132 @@ extern "C" fastilu_status fastilu_gmres(fastilu_handle h, const double *b, doubl
   if ((fs = nrm(b, &bnorm))) return fs;
   double beta = bnorm;
   int total = 0;
-  std::vector<double> H((size_t)(m + 1) * m), cs(m), sn(m), g(m + 1), hv(m + 2), h2(m + 2);
-  while (bnorm > 0.0 && beta / bnorm > rtol && total < max_iters) {
-    CU(launch_axpby(1.0 / beta, r, 0.0, V, n, st));  // V_0 = r / beta
-    std::fill(g.begin(), g.end(), 0.0);
-    g[0] = beta;
-    int j = 0;
-    for (; j < m && total < max_iters; j++) {
-      if ((fs = apply_impl(h, V + j * ldv, u, ntrisweeps))) return fs;  // u = M^-1 V_j
-      if ((fs = spmv(u, w))) return fs;                                   // w = A u
-      double hn = 0.0;
-      if (!h->comm) {
-        // one GPU: classical Gram-Schmidt with the projections kept on the device and a second
-        // pass only when the first one cancelled (||w'|| < ||w|| / sqrt 2: the Daniel-Gragg-
-        // Kaufman-Stewart criterion, "twice is enough"), so most iterations read V twice and
-        // synchronise once: pass 1 = h1 = V^T w together with ||w||^2, then w -= V h1 with
-        // ||w||^2 fused; FASTILU_GMRES_CGS2=1 always reorthogonalises
-        double *c1 = h->gm_c, *c2 = h->gm_c + (m + 2), *c3 = h->gm_c + 2 * (m + 2);
-        double *b1 = h->gm_hbuf, *b2 = h->gm_hbuf + (m + 2), *b3 = h->gm_hbuf + 2 * (m + 2);
-        const size_t kb = sizeof(double) * (j + 1);
-        CU(launch_mdot(V, ldv, j + 1, w, n, h->gm_part, c1, st, w));       // CGS pass 1
-        CU(cudaMemcpyAsync(b1, c1, kb + sizeof(double), cudaMemcpyDeviceToHost, st));
-        CU(launch_maxpy_nrm(V, ldv, j + 1, c1, w, n, -1.0, h->gm_part, c3, st));
-        CU(cudaMemcpyAsync(b3, c3, sizeof(double), cudaMemcpyDeviceToHost, st));
-        CU(cudaStreamSynchronize(st));
-        for (int q = 0; q <= j; q++) {
-          hv[q] = b1[q];
-          h2[q] = 0.0;
-        }
-        const double wn2 = b1[j + 1];
-        double hn2 = b3[0];
-        if (hn2 < 0.5 * wn2 || gmres_cgs2) {                              // CGS pass 2
-          CU(launch_mdot(V, ldv, j + 1, w, n, h->gm_part, c2, st));
-          CU(cudaMemcpyAsync(b2, c2, kb, cudaMemcpyDeviceToHost, st));
-          CU(launch_maxpy_nrm(V, ldv, j + 1, c2, w, n, -1.0, h->gm_part, c3, st));
-          CU(cudaMemcpyAsync(b3, c3, sizeof(double), cudaMemcpyDeviceToHost, st));
-          CU(cudaStreamSynchronize(st));
-          for (int q = 0; q <= j; q++) h2[q] = b2[q];
-          hn2 = b3[0];
-          h->gm_reorth++;
-        }
-        hn = std::sqrt(hn2);
-      } else {
-        if ((fs = dots(j + 1, V, w, hv.data()))) return fs;                 // CGS pass 1
-        for (int q = 0; q <= j; q++) h->gm_hbuf[q] = hv[q];
-        CU(cudaMemcpyAsync(h->gm_c, h->gm_hbuf, sizeof(double) * (j + 1), cudaMemcpyHostToDevice,
-                           st));
-        CU(launch_maxpy(V, ldv, j + 1, h->gm_c, w, n, -1.0, st));
-        if ((fs = dots(j + 1, V, w, h2.data()))) return fs;                 // CGS pass 2
-        for (int q = 0; q <= j; q++) h->gm_hbuf[q] = h2[q];
-        CU(cudaMemcpyAsync(h->gm_c, h->gm_hbuf, sizeof(double) * (j + 1), cudaMemcpyHostToDevice,
-                           st));
-        CU(launch_maxpy(V, ldv, j + 1, h->gm_c, w, n, -1.0, st));
-        if ((fs = nrm(w, &hn))) return fs;
-      }
-      for (int q = 0; q <= j; q++) H[(size_t)q * m + j] = hv[q] + h2[q];
-      H[(size_t)(j + 1) * m + j] = hn;
-      if (hn > 0.0) CU(launch_axpby(1.0 / hn, w, 0.0, V + (j + 1) * ldv, n, st));
-      for (int q = 0; q < j; q++) {  // previous rotations
-        const double a = H[(size_t)q * m + j], c = H[(size_t)(q + 1) * m + j];
-        H[(size_t)q * m + j] = cs[q] * a + sn[q] * c;
-        H[(size_t)(q + 1) * m + j] = -sn[q] * a + cs[q] * c;
-      }
-      const double a = H[(size_t)j * m + j], c = H[(size_t)(j + 1) * m + j];
-      const double rr = std::hypot(a, c);
-      cs[j] = rr > 0.0 ? a / rr : 1.0;
-      sn[j] = rr > 0.0 ? c / rr : 0.0;
-      H[(size_t)j * m + j] = rr;
-      H[(size_t)(j + 1) * m + j] = 0.0;
-      g[j + 1] = -sn[j] * g[j];
-      g[j] = cs[j] * g[j];
-      total++;
-      if (std::fabs(g[j + 1]) <= rtol * bnorm || hn == 0.0) {
-        j++;
-        break;
-      }
+  std::vector<double> H((size_t)(m + 1) * m), cs(m), sn(m), g(m + 1);
+  // Givens rotation of column j (rows 0..j+1 of Rm) with the previous rotations; new residual
+  // estimate in g[j + 1]
+  auto givens = [&](std::vector<double> &Rm, int j) {
+    for (int q = 0; q < j; q++) {
+      const double a = Rm[(size_t)q * m + j], c = Rm[(size_t)(q + 1) * m + j];
+      Rm[(size_t)q * m + j] = cs[q] * a + sn[q] * c;
+      Rm[(size_t)(q + 1) * m + j] = -sn[q] * a + cs[q] * c;
     }
-    // y = H^-1 g (upper triangular j x j), x += M^-1 (V y)
-    std::vector<double> y(j, 0.0);
-    for (int q = j - 1; q >= 0; q--) {
+    const double a = Rm[(size_t)j * m + j], c = Rm[(size_t)(j + 1) * m + j];
+    const double rr = std::hypot(a, c);
+    cs[j] = rr > 0.0 ? a / rr : 1.0;
+    sn[j] = rr > 0.0 ? c / rr : 0.0;
+    Rm[(size_t)j * m + j] = rr;
+    Rm[(size_t)(j + 1) * m + j] = 0.0;
+    g[j + 1] = -sn[j] * g[j];
+    g[j] = cs[j] * g[j];
+  };
+  // x += M^-1 (V y), y = R^-1 g (upper triangular k x k); then r = b - A x, beta = ||r||
+  auto finish_cycle = [&](const std::vector<double> &Rm, int k) -> fastilu_status {
+    std::vector<double> y(k, 0.0);
+    for (int q = k - 1; q >= 0; q--) {
       double t = g[q];
-      for (int c2 = q + 1; c2 < j; c2++) t -= H[(size_t)q * m + c2] * y[c2];
-      y[q] = t / H[(size_t)q * m + q];
+      for (int c2 = q + 1; c2 < k; c2++) t -= Rm[(size_t)q * m + c2] * y[c2];
+      y[q] = t / Rm[(size_t)q * m + q];
     }
-    for (int q = 0; q < j; q++) h->gm_hbuf[q] = y[q];
-    CU(cudaMemcpyAsync(h->gm_c, h->gm_hbuf, sizeof(double) * j, cudaMemcpyHostToDevice, st));
+    for (int q = 0; q < k; q++) h->gm_hbuf[q] = y[q];
+    CU(cudaMemcpyAsync(h->gm_c, h->gm_hbuf, sizeof(double) * k, cudaMemcpyHostToDevice, st));
     CU(cudaMemsetAsync(w, 0, sizeof(double) * n, st));
-    CU(launch_maxpy(V, ldv, j, h->gm_c, w, n, 1.0, st));
-    if ((fs = apply_impl(h, w, u, ntrisweeps))) return fs;
+    CU(launch_maxpy(V, ldv, k, h->gm_c, w, n, 1.0, st));
+    fastilu_status fs2 = apply_impl(h, w, u, ntrisweeps);
+    if (fs2) return fs2;
     CU(launch_axpby(1.0, u, 1.0, x, n, st));
-    // true residual r = b - A x
-    if ((fs = spmv(x, w))) return fs;
+    if ((fs2 = spmv(x, w))) return fs2;
     CU(cudaMemcpyAsync(r, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
     CU(launch_axpby(-1.0, w, 1.0, r, n, st));
-    if ((fs = nrm(r, &beta))) return fs;
+    return nrm(r, &beta);
+  };
+  // DCGS2 Arnoldi: V_p is the PENDING vector (projected once, not yet
+  // normalised); step p applies B = A M^-1 to it, takes all dots V_j . V_p and V_j . (B V_p),
+  // j <= p, in ONE pass and ONE synchronisation, which (i) finishes the reorthogonalisation of
+  // V_p -- q_p = (V_p - Q s) / rho, rho^2 = ||V_p||^2 - ||s||^2 -- and with it Hessenberg column
+  // p - 1 (H[:p, p-1] += s, H[p, p-1] = rho), and (ii) gives the first projection of B q_p
+  // without applying B again: B q_p = (B V_p - B Q s) / rho with B Q = Q H, so
+  // h_p = (c - H s) / rho and the next pending vector is (B V_p - Q_{p+1} c) / rho, c = [z,
+  // (zeta - s.z) / rho].  A second pass over V does both updates.  The rotated copy R of H drives
+  // the least-squares problem; the residual estimate of column p - 1 is known at step p.
+  std::vector<double> R((size_t)(m + 1) * m), dv(2 * (m + 2)), sv(m + 1), zv(m + 1);
+  while (bnorm > 0.0 && beta / bnorm > rtol && total < max_iters) {
+    CU(cudaMemcpyAsync(V, r, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));  // pending V_0
+    std::fill(H.begin(), H.end(), 0.0);
+    std::fill(R.begin(), R.end(), 0.0);
+    std::fill(g.begin(), g.end(), 0.0);
+    int p = 0, k = 0, retries = 0;
+    for (;;) {
+      const bool last = p == m || (p >= 1 && total + 1 >= max_iters);
+      if (!last) {
+        if ((fs = apply_impl(h, V + p * ldv, u, ntrisweeps))) return fs;  // u = M^-1 V_p
+        if ((fs = spmv(u, w))) return fs;                                   // w = A u
+      }
+      CU(launch_dcgs_dot(V, ldv, p, last ? nullptr : w, n, h->gm_part, h->gm_c, st));
+      CU(cudaMemcpyAsync(h->gm_hbuf, h->gm_c, sizeof(double) * 2 * (p + 1),
+                         cudaMemcpyDeviceToHost, st));
+      CU(cudaStreamSynchronize(st));
+      for (int q = 0; q < 2 * (p + 1); q++) dv[q] = h->gm_hbuf[q];
+      if (h->comm) {
+        ErrFlags dummy{~0ull, ~0ull};
+        if ((fs = comm_allreduce_host(h->comm, dv.data(), 2 * (p + 1), dummy))) return fs;
+      }
+      double ss = 0.0, sz = 0.0;
+      for (int q = 0; q < p; q++) {
+        sv[q] = dv[2 * q];
+        zv[q] = dv[2 * q + 1];
+        ss += sv[q] * sv[q];
+        sz += sv[q] * zv[q];
+      }
+      const double alpha = dv[2 * p], zeta = dv[2 * p + 1], rho2 = alpha - ss;
+      if (p >= 1 && alpha > 0.0 && (rho2 < 0.5 * alpha || (force_reproject && retries == 0)) &&
+          retries < 2) {
+        // the pending vector still leans on Q (severe cancellation in its first projection):
+        // project it explicitly, fold s into column p - 1 and redo the step
+        for (int q = 0; q < p; q++) {
+          h->gm_hbuf[2 * (m + 2) + q] = sv[q];
+          H[(size_t)q * m + p - 1] += sv[q];
+        }
+        CU(cudaMemcpyAsync(h->gm_c + 2 * (m + 2), h->gm_hbuf + 2 * (m + 2), sizeof(double) * p,
+                           cudaMemcpyHostToDevice, st));
+        CU(launch_maxpy(V, ldv, p, h->gm_c + 2 * (m + 2), V + p * ldv, n, -1.0, st));
+        retries++;
+        h->gm_retry++;
+        continue;
+      }
+      retries = 0;
+      const double rho = rho2 > 0.0 ? std::sqrt(rho2) : 0.0;
+      if (p >= 1) {  // column p - 1 is final
+        for (int q = 0; q < p; q++) H[(size_t)q * m + p - 1] += sv[q];
+        H[(size_t)p * m + p - 1] = rho;
+        for (int q = 0; q <= p; q++) R[(size_t)q * m + p - 1] = H[(size_t)q * m + p - 1];
+        givens(R, p - 1);
+        total++;
+        h->gm_reorth++;
+        k = p;
+        if (last || rho == 0.0 || std::fabs(g[p]) <= rtol * bnorm) break;
+      } else {
+        g[0] = rho;  // ||r||
+        if (rho == 0.0) break;
+      }
+      const double cp = (zeta - sz) / rho;
+      for (int q = 0; q <= p; q++) {  // tentative column p: (c - H[0..p, 0..p-1] s) / rho
+        double t = q < p ? zv[q] : cp;
+        for (int l = std::max(0, q - 1); l < p; l++) t -= H[(size_t)q * m + l] * sv[l];
+        H[(size_t)q * m + p] = t / rho;
+      }
+      double *cb = h->gm_hbuf + 2 * (m + 2);
+      for (int q = 0; q < p; q++) {
+        cb[q] = sv[q];
+        cb[p + q] = zv[q];
+      }
+      cb[2 * p] = cp;
+      cb[2 * p + 1] = 1.0 / rho;
+      CU(cudaMemcpyAsync(h->gm_c + 2 * (m + 2), cb, sizeof(double) * (2 * p + 2),
+                         cudaMemcpyHostToDevice, st));
+      CU(launch_dcgs_update(V, ldv, p, h->gm_c + 2 * (m + 2), w, n, st));
+      p++;
+    }
+    if ((fs = finish_cycle(R, k))) return fs;
   }
   CU(cudaEventRecord(h->ev[4], st));
   h->apply_timed = true;
@@ -2040,7 +2077,8 @@ extern "C" fastilu_status fastilu_get_info(fastilu_handle h, char *buf, int cap)
   }
   {
     const size_t L = strlen(tmp);
-    snprintf(tmp + L, sizeof(tmp) - L, " gmres_reorth=%d", h->gm_reorth);
+    snprintf(tmp + L, sizeof(tmp) - L, " gmres_reorth=%d gmres_retry=%d", h->gm_reorth,
+             h->gm_retry);
   }
   snprintf(buf, cap, "%s", tmp);
   return FASTILU_OK;

@@ -992,17 +992,15 @@ cudaError_t launch_mdot(const double *V, int64_t ldv, int k, const double *w, in
   return cudaGetLastError();
 }
 
-// w -= sign-scaled V c over kRpt rows per thread (independent FMA chains, the loads of a column
-// issued together); with `partials`, also the block's share of ||w_new||^2 (deterministic: warp
-// shuffles, then a fixed-order sum over the block's warps) for the Arnoldi norm.
+// w += sign-scaled V c over kRpt rows per thread (independent FMA chains, the loads of a column
+// issued together): the GMRES solution update x = M^-1 (V y) and the explicit re-projection of a
+// pending vector after a severe cancellation.
 __global__ void __launch_bounds__(256)
 maxpy_kernel(const double *__restrict__ V, int64_t ldv, int k, const double *__restrict__ c,
-             double *__restrict__ w, int64_t n, double sign, double *__restrict__ partials) {
+             double *__restrict__ w, int64_t n, double sign) {
   __shared__ double sc[kMaxK];
-  __shared__ double red[8];
   for (int j = threadIdx.x; j < k && j < kMaxK; j += blockDim.x) sc[j] = sign * c[j];
   __syncthreads();
-  double nrm = 0.0;
   for (int64_t c0 = (int64_t)blockIdx.x * kChunk; c0 < n; c0 += (int64_t)gridDim.x * kChunk) {
     double t[kRpt];
 #pragma unroll
@@ -1023,37 +1021,156 @@ maxpy_kernel(const double *__restrict__ V, int64_t ldv, int k, const double *__r
 #pragma unroll
     for (int r = 0; r < kRpt; r++) {
       const int64_t i = c0 + r * 256 + threadIdx.x;
-      if (i < n) {
-        w[i] = t[r];
-        nrm = fma(t[r], t[r], nrm);
-      }
+      if (i < n) w[i] = t[r];
     }
-  }
-  if (!partials) return;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int o = 16; o > 0; o >>= 1) nrm += __shfl_down_sync(0xffffffffu, nrm, o);
-  if (lane == 0) red[warp] = nrm;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double tt = 0.0;
-    for (int q = 0; q < 8; q++) tt += red[q];
-    partials[blockIdx.x] = tt;
   }
 }
 
 cudaError_t launch_maxpy(const double *V, int64_t ldv, int k, const double *c, double *w,
                          int64_t n, double sign, cudaStream_t st) {
   if (k <= 0) return cudaSuccess;
-  maxpy_kernel<<<orth_blocks(n), 256, 0, st>>>(V, ldv, k, c, w, n, sign, nullptr);
+  if (k > kMaxK) return cudaErrorInvalidValue;
+  maxpy_kernel<<<orth_blocks(n), 256, 0, st>>>(V, ldv, k, c, w, n, sign);
   return cudaGetLastError();
 }
 
-cudaError_t launch_maxpy_nrm(const double *V, int64_t ldv, int k, const double *c, double *w,
-                             int64_t n, double sign, double *partials, double *out,
-                             cudaStream_t st) {
-  const unsigned nb = orth_blocks(n);
-  maxpy_kernel<<<nb, 256, 0, st>>>(V, ldv, k, c, w, n, sign, partials);
-  mdot_reduce_kernel<<<1, 256, 0, st>>>(partials, (int)nb, 1, out);
+// ---- DCGS2: classical Gram-Schmidt with the reorthogonalisation delayed by one iteration
+// (DESIGN.md Sec. 7b).  Two passes over V per Arnoldi step: the dots of the pending vector
+// u = V_p and of w = B u against V_0..V_p in one pass, then one pass that finalises
+// q_p = (u - Q s) / rho and forms the next pending vector (w - Q z - q_p c_p) / rho.
+// Block b owns the contiguous rows [b n / grid, (b+1) n / grid) (equal shares), kDRpt rows per
+// thread and chunk.
+constexpr int kDRpt = 4, kDChunk = 256 * kDRpt;
+// one wave: SMs x resident blocks of `func` (at most kDotBlocks), fewer for short vectors
+static unsigned dcgs_blocks(int64_t n, const void *func) {
+  int dev = 0, per_sm = 1;
+  cudaGetDevice(&dev);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, func, 256, 0) != cudaSuccess ||
+      per_sm < 1)
+    per_sm = 1;
+  const int64_t chunks = (n + kDChunk - 1) / kDChunk;
+  const int64_t wave = std::min<int64_t>((int64_t)sm_count(dev) * per_sm, kDotBlocks);
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(chunks, wave));
+}
+
+// out (per block): partials[(2 j + e) * grid + b] = V_j . u (e = 0), V_j . w (e = 1), j <= p.
+// Groups of 4 columns x 2 vectors = 8 per-lane sums are reduced across the warp by a butterfly
+// (each step halves the values a lane carries: 4 + 2 + 1 + 2 shuffles for 8 sums instead of 40);
+// lane 4 t then holds sum t, summed into the warp's shared-memory slot (fixed order: deterministic).
+__global__ void __launch_bounds__(256, 3)
+dcgs_dot_kernel(const double *__restrict__ V, int64_t ldv, int p, const double *__restrict__ w,
+                int64_t n, double *__restrict__ partials) {
+  __shared__ double red[8][2 * kMaxK];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, k = p + 1;
+  for (int j = threadIdx.x; j < 8 * 2 * kMaxK; j += blockDim.x) (&red[0][0])[j] = 0.0;
+  __syncthreads();
+  const int64_t rb = n * (int64_t)blockIdx.x / gridDim.x;
+  const int64_t re = n * (int64_t)(blockIdx.x + 1) / gridDim.x;
+  const double *u = V + (int64_t)p * ldv;
+  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+  const int slot = (lane >> 2) & 7;  // the sum lane 4 t ends up with: column t / 2, vector t % 2
+  for (int64_t c0 = rb; c0 < re; c0 += kDChunk) {
+    double uv[kDRpt], wv[kDRpt];
+#pragma unroll
+    for (int r = 0; r < kDRpt; r++) {
+      const int64_t i = c0 + r * 256 + threadIdx.x;
+      uv[r] = i < re ? u[i] : 0.0;
+      wv[r] = (w && i < re) ? w[i] : 0.0;
+    }
+    for (int j0 = 0; j0 < k; j0 += 4) {
+      double a[8];
+#pragma unroll
+      for (int t = 0; t < 4; t++) {
+        a[2 * t] = a[2 * t + 1] = 0.0;
+        if (j0 + t < k) {
+          const double *vj = V + (int64_t)(j0 + t) * ldv;
+#pragma unroll
+          for (int r = 0; r < kDRpt; r++) {
+            const int64_t i = c0 + r * 256 + threadIdx.x;
+            const double v = i < re ? vj[i] : 0.0;
+            a[2 * t] = fma(v, uv[r], a[2 * t]);
+            a[2 * t + 1] = fma(v, wv[r], a[2 * t + 1]);
+          }
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < 4; t++)
+        a[t] = (b4 ? a[4 + t] : a[t]) + __shfl_xor_sync(0xffffffffu, b4 ? a[t] : a[4 + t], 16);
+#pragma unroll
+      for (int t = 0; t < 2; t++)
+        a[t] = (b3 ? a[2 + t] : a[t]) + __shfl_xor_sync(0xffffffffu, b3 ? a[t] : a[2 + t], 8);
+      a[0] = (b2 ? a[1] : a[0]) + __shfl_xor_sync(0xffffffffu, b2 ? a[0] : a[1], 4);
+      a[0] += __shfl_xor_sync(0xffffffffu, a[0], 2);
+      a[0] += __shfl_xor_sync(0xffffffffu, a[0], 1);
+      if ((lane & 3) == 0 && j0 + (slot >> 1) < k) red[warp][2 * j0 + slot] += a[0];
+    }
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < 2 * k; j += blockDim.x) {
+    double t = 0.0;
+    for (int q = 0; q < 8; q++) t += red[q][j];
+    partials[(int64_t)j * gridDim.x + blockIdx.x] = t;
+  }
+}
+
+cudaError_t launch_dcgs_dot(const double *V, int64_t ldv, int p, const double *w, int64_t n,
+                            double *partials, double *out, cudaStream_t st) {
+  if (p < 0 || p + 1 > kMaxK) return cudaErrorInvalidValue;
+  const unsigned nb = dcgs_blocks(n, (const void *)dcgs_dot_kernel);
+  dcgs_dot_kernel<<<nb, 256, 0, st>>>(V, ldv, p, w, n, partials);
+  mdot_reduce_kernel<<<min(2 * (p + 1), 64), 256, 0, st>>>(partials, (int)nb, 2 * (p + 1), out);
+  return cudaGetLastError();
+}
+
+// coef = [s_0..s_{p-1}, z_0..z_{p-1}, c_p, 1/rho] (device):
+//   q = (V_p - sum_j s_j V_j) / rho -> V_p;   (w - sum_j z_j V_j - c_p q) / rho -> V_{p+1}
+__global__ void __launch_bounds__(256)
+dcgs_update_kernel(double *__restrict__ V, int64_t ldv, int p, const double *__restrict__ coef,
+                   const double *__restrict__ w, int64_t n) {
+  __shared__ double sc[2 * kMaxK + 2];
+  for (int j = threadIdx.x; j < 2 * p + 2; j += blockDim.x) sc[j] = coef[j];
+  __syncthreads();
+  const double cp = sc[2 * p], irho = sc[2 * p + 1];
+  const int64_t rb = n * (int64_t)blockIdx.x / gridDim.x;
+  const int64_t re = n * (int64_t)(blockIdx.x + 1) / gridDim.x;
+  double *u = V + (int64_t)p * ldv, *un = u + ldv;
+  for (int64_t c0 = rb; c0 < re; c0 += kDChunk) {
+    double t1[kDRpt], t2[kDRpt];
+#pragma unroll
+    for (int r = 0; r < kDRpt; r++) {
+      const int64_t i = c0 + r * 256 + threadIdx.x;
+      t1[r] = i < re ? u[i] : 0.0;
+      t2[r] = i < re ? w[i] : 0.0;
+    }
+#pragma unroll 4
+    for (int j = 0; j < p; j++) {
+      const double *vj = V + (int64_t)j * ldv;
+      const double sj = sc[j], zj = sc[p + j];
+#pragma unroll
+      for (int r = 0; r < kDRpt; r++) {
+        const int64_t i = c0 + r * 256 + threadIdx.x;
+        const double v = i < re ? vj[i] : 0.0;
+        t1[r] = fma(-sj, v, t1[r]);
+        t2[r] = fma(-zj, v, t2[r]);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < kDRpt; r++) {
+      const int64_t i = c0 + r * 256 + threadIdx.x;
+      if (i < re) {
+        const double q = t1[r] * irho;
+        u[i] = q;
+        un[i] = fma(-cp, q, t2[r]) * irho;
+      }
+    }
+  }
+}
+
+cudaError_t launch_dcgs_update(double *V, int64_t ldv, int p, const double *coef, const double *w,
+                               int64_t n, cudaStream_t st) {
+  if (p < 0 || p + 1 > kMaxK) return cudaErrorInvalidValue;
+  if (n <= 0) return cudaSuccess;
+  dcgs_update_kernel<<<dcgs_blocks(n, (const void *)dcgs_update_kernel), 256, 0, st>>>(V, ldv, p, coef, w, n);
   return cudaGetLastError();
 }
 
