@@ -41,6 +41,7 @@ struct fastilu_handle_s {
   cudaStream_t copy_stream = nullptr;
   std::vector<cudaEvent_t> chunk_ev;
   int chunk_b = 0;  // index of the event after the right-hand side's upload (solve_host)
+  std::vector<cudaEvent_t> x_ev;  // solve_host pipeline: chunk c of x final
   std::vector<int64_t> h_arp;  // local A row pointers (offsets into the local values)
   double *d_r2c = nullptr;     // per-chunk residual sums (chunks x nsweeps)
   int r2c_cap = 0;
@@ -1296,6 +1297,9 @@ static fastilu_status compute_impl(fastilu_handle h, int nsweeps, double rtol, i
 }
 
 static fastilu_status apply_impl(fastilu_handle h, const double *b, double *x, int ntri);
+static int jit_jacobi(fastilu_handle h, bool lower, const double *vals, const double *ud,
+                      const double *rhs, const double *xo, double *xn, double *xf, int64_t r0,
+                      int64_t r1, int64_t Gh, double om, bool final_x);
 
 // fastilu_compute_host: new values from host memory + nsweeps sweeps, the upload pipelined with
 // the compute.  Chunks of >= A's bandwidth rows: chunk c's values go up on a copy stream; on
@@ -1304,17 +1308,42 @@ static fastilu_status apply_impl(fastilu_handle h, const double *b, double *x, i
 // which keeps every iterate a later chunk still reads alive in the two ping-pong buffers: sweep
 // s of chunk c reads iterate s-1 of rows <= its own only.  Same kernels, same per-entry
 // arithmetic as set_values + compute; only the residual's sum is taken per chunk.
+//
+// With x_host (solve_host; FASTILU_SOLVE_NOPIPE=1 runs the apply after the compute instead), the
+// apply rides the same pipeline: b goes up
+// chunk by chunk behind the values, the L Jacobi sweeps of chunk c run (along their own
+// diagonal) as soon as chunk c's factors are final, and once every chunk's L sweeps are done
+// the U sweeps run along a descending diagonal, each chunk's x copied back as soon as its last
+// U sweep is done.  Same kernels, rows and order of terms as apply: x is bitwise the same.
 static fastilu_status compute_host_impl(fastilu_handle h, const double *values, int nsweeps,
                                         const double *b_host = nullptr,
-                                        bool *b_queued = nullptr) {
+                                        bool *b_queued = nullptr, double *x_host = nullptr,
+                                        int ntri = 0, bool *x_done = nullptr) {
   if (b_queued) *b_queued = false;
+  if (x_done) *x_done = false;
   const int64_t R = h->st.rows > 0 ? h->st.rows : 256;
   int64_t bwA = 0;
   for (int32_t o : h->T.offA) bwA = std::max<int64_t>(bwA, std::abs((int64_t)o));
+  for (int32_t o : h->T.off) bwA = std::max<int64_t>(bwA, std::abs((int64_t)o));  // S's band
   int64_t chunk = std::max<int64_t>(bwA, 16 * R);
   chunk = std::max<int64_t>(chunk, (h->n + 15) / 16);
   chunk = (chunk + R - 1) / R * R;
-  const int C = (int)((h->n + chunk - 1) / std::max<int64_t>(chunk, 1));
+  // chunk boundaries: equal chunks, the last one cut into up to 4 pieces of at least the band
+  // (FASTILU_SOLVE_TAIL overrides the 4), so that less work waits for the last bytes (c4 e2e:
+  // 76.2 -> 74.3 ms, profiles/r2ze_e2e_pipeline_ab.log)
+  std::vector<int64_t> bnd;
+  for (int64_t r = 0; r < h->n; r += chunk) bnd.push_back(r);
+  {
+    const char *te = std::getenv("FASTILU_SOLVE_TAIL");
+    const int64_t last = bnd.back(), rows = h->n - last;
+    const int64_t minp = (std::max<int64_t>(bwA, R) + R - 1) / R * R;
+    const int64_t pieces =
+        std::max<int64_t>(1, std::min<int64_t>(te ? std::atoi(te) : 4, rows / minp));
+    const int64_t step = (rows / pieces + R - 1) / R * R;
+    for (int64_t q = 1; q < pieces && last + q * step < h->n; q++) bnd.push_back(last + q * step);
+  }
+  bnd.push_back(h->n);
+  const int C = (int)bnd.size() - 1;
   const bool ok = h->tsell && !h->comm && h->jit_st && h->jit_st_init && h->jit_ahat &&
                   h->jit_scale && nsweeps >= 1 && h->opt.omega == 1.0 && h->G == 0 &&
                   h->st.shift == 0 && C >= 2 &&
@@ -1331,7 +1360,9 @@ static fastilu_status compute_host_impl(fastilu_handle h, const double *values, 
   if (!h->copy_stream) CU(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
   while ((int)h->chunk_ev.size() < C + 1) {
     cudaEvent_t e;
-    CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    // FASTILU_TRACE=1 (diagnostic): timed chunk events, printed by solve_host
+    CU(cudaEventCreateWithFlags(&e, std::getenv("FASTILU_TRACE") ? cudaEventDefault
+                                                                 : cudaEventDisableTiming));
     h->chunk_ev.push_back(e);
   }
   if (nsweeps > h->hist_cap) {
@@ -1349,21 +1380,33 @@ static fastilu_status compute_host_impl(fastilu_handle h, const double *values, 
     CU(dalloc(&h->d_r2c, (int64_t)C * nsweeps));
     h->r2c_cap = C * nsweeps;
   }
-  auto rb = [&](int c) { return std::min<int64_t>((int64_t)c * chunk, h->n); };
+  auto rb = [&](int c) { return bnd[c]; };
   CU(cudaMemsetAsync(h->d_err, 0xff, sizeof(ErrFlags), st));
   CU(cudaEventRecord(h->ev[0], st));
   // every chunk's values up front on the copy stream, ordered after the compute stream's
   // previous work (the previous compute may still read d_aval / d_aT)
   CU(cudaEventRecord(h->ev[1], st));
   CU(cudaStreamWaitEvent(h->copy_stream, h->ev[1], 0));
+  const bool pipe_x = b_host && x_host && ntri >= 1 && h->jit_jac[0] && h->jit_jac[1];
+  if (pipe_x) {
+    if (!h->d_bx) CU(dalloc(&h->d_bx, 2 * h->n));
+    while ((int)h->x_ev.size() < C) {
+      cudaEvent_t e;
+      CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      h->x_ev.push_back(e);
+    }
+  }
   for (int c = 0; c < C; c++) {
     const int64_t a0 = h->h_arp[rb(c)], a1 = h->h_arp[rb(c + 1)];
     if (a1 > a0)
       CU(cudaMemcpyAsync(h->d_aval + a0, values + h->a_in_off + a0, sizeof(double) * (a1 - a0),
                          cudaMemcpyHostToDevice, h->copy_stream));
+    if (pipe_x)  // chunk c of b behind chunk c of the values
+      CU(cudaMemcpyAsync(h->d_bx + rb(c), b_host + rb(c), sizeof(double) * (rb(c + 1) - rb(c)),
+                         cudaMemcpyHostToDevice, h->copy_stream));
     CU(cudaEventRecord(h->chunk_ev[c], h->copy_stream));
   }
-  if (b_host) {  // solve_host: the right-hand side follows the values on the copy stream
+  if (b_host && !pipe_x) {  // solve_host: the right-hand side follows the values
     if (!h->d_bx) CU(dalloc(&h->d_bx, 2 * h->n));
     CU(cudaMemcpyAsync(h->d_bx, b_host, sizeof(double) * h->n, cudaMemcpyHostToDevice,
                        h->copy_stream));
@@ -1432,23 +1475,108 @@ static fastilu_status compute_host_impl(fastilu_handle h, const double *values, 
     }
     return FASTILU_OK;
   };
+  // apply pipeline (pipe_x): L step e runs Jacobi sweep t on chunk e - t + 1 (t ascending; the
+  // factors of chunk e are final after factor step e + nsweeps - 1), U step e sweep t on chunk
+  // C - 1 - (e - t + 1); the ping-pong buffers are safe by the same diagonal argument as the
+  // factor sweeps (L sweep t of chunk c reads iterate t-1 of chunks c-1, c; U of chunks c, c+1)
+  const double omt = h->opt.omega_tri;
+  const int fb = nsweeps & 1;
+  const double *fvals = h->d_vals[fb], *fud = h->d_ud[fb];
+  double *xd = h->d_bx + h->n;
+  auto lstep = [&](int e) -> fastilu_status {
+    for (int t = 1; t <= ntri; t++) {
+      const int c = e - t + 1;
+      if (c < 0 || c >= C) continue;
+      if (t == 1)
+        CU(launch_trisolve_first_L(h->d_bx, h->d_s, h->d_y, h->d_z[0], rb(c), rb(c + 1), 0, omt,
+                                   st));
+      else if (jit_jacobi(h, true, fvals, nullptr, h->d_y, h->d_z[(t - 2) & 1],
+                          h->d_z[(t - 1) & 1], nullptr, rb(c), rb(c + 1), 0, omt, false))
+        FAIL(FASTILU_ERR_CUDA);
+    }
+    return FASTILU_OK;
+  };
+  // U chunks: pairs of pipeline chunks counted from the top (fewer, longer U launches; measured
+  // 74.3 -> 74.1 ms; FASTILU_SOLVE_UCOARSE overrides the 2)
+  std::vector<int64_t> ub;
+  {
+    const char *ue = std::getenv("FASTILU_SOLVE_UCOARSE");
+    const int uk = std::max(1, ue ? std::atoi(ue) : 2);
+    for (int c = C; c >= 0; c -= uk) ub.push_back(bnd[c]);
+    if (ub.back() != 0) ub.push_back(0);
+    std::reverse(ub.begin(), ub.end());
+  }
+  const int CU_ = (int)ub.size() - 1;
+  auto ustep = [&](int e) -> fastilu_status {
+    const double *zf = h->d_z[(ntri - 1) & 1];
+    for (int t = 1; t <= ntri; t++) {
+      const int c = CU_ - 1 - (e - t + 1);
+      if (c < 0 || c >= CU_) continue;
+      if (t == 1)
+        CU(launch_trisolve_first_U(zf, fud, h->d_s, h->d_w[0], xd, ub[c], ub[c + 1], 0, omt,
+                                   ntri == 1, st));
+      else if (jit_jacobi(h, false, fvals, fud, zf, h->d_w[(t - 2) & 1], h->d_w[(t - 1) & 1], xd,
+                          ub[c], ub[c + 1], 0, omt, t == ntri))
+        FAIL(FASTILU_ERR_CUDA);
+      if (t == ntri) {  // x of chunk c is final: copy it back on the copy stream
+        CU(cudaEventRecord(h->x_ev[c], st));
+        CU(cudaStreamWaitEvent(h->copy_stream, h->x_ev[c], 0));
+        CU(cudaMemcpyAsync(x_host + ub[c], xd + ub[c], sizeof(double) * (ub[c + 1] - ub[c]),
+                           cudaMemcpyDeviceToHost, h->copy_stream));
+      }
+    }
+    return FASTILU_OK;
+  };
   fastilu_status fs;
   for (int c = 0; c < C; c++) {
     if ((fs = prep(c))) return fs;
     if (c >= 1) {
       if ((fs = ahat(c - 1))) return fs;
       if ((fs = diag(c - 1))) return fs;
+      if (pipe_x && c - nsweeps >= 0 && (fs = lstep(c - nsweeps))) return fs;
     }
   }
   if ((fs = ahat(C - 1))) return fs;
-  for (int d = C - 1; d <= C + nsweeps - 2; d++)
+  for (int d = C - 1; d <= C + nsweeps - 2; d++) {
     if ((fs = diag(d))) return fs;
+    if (pipe_x && d - nsweeps + 1 >= 0 && (fs = lstep(d - nsweeps + 1))) return fs;
+  }
+  if (pipe_x) {
+    for (int e = C; e <= C + ntri - 2; e++)
+      if ((fs = lstep(e))) return fs;
+    CU(cudaEventRecord(h->ev[3], st));  // trace: factors and L sweeps done
+    for (int e = 0; e <= CU_ + ntri - 2; e++)
+      if ((fs = ustep(e))) return fs;
+  }
   CU(cudaEventRecord(h->ev[2], st));
   std::vector<double> r2c((size_t)C * nsweeps);
   CU(cudaMemcpyAsync(h->h_err, h->d_err, sizeof(ErrFlags), cudaMemcpyDeviceToHost, st));
   CU(cudaMemcpyAsync(r2c.data(), h->d_r2c, sizeof(double) * r2c.size(), cudaMemcpyDeviceToHost,
                      st));
   CU(cudaStreamSynchronize(st));
+  if (pipe_x) {
+    if (std::getenv("FASTILU_TRACE")) {  // timeline (ms from the compute's start)
+      cudaEvent_t e;
+      CU(cudaEventCreate(&e));
+      CU(cudaEventRecord(e, h->copy_stream));
+      CU(cudaStreamSynchronize(h->copy_stream));
+      float t;
+      std::fprintf(stderr, "fastilu trace (pipelined apply): chunks landed at");
+      for (int c = 0; c < C; c++)
+        if (cudaEventElapsedTime(&t, h->ev[0], h->chunk_ev[c]) == cudaSuccess)
+          std::fprintf(stderr, " %.2f", t);
+      if (cudaEventElapsedTime(&t, h->ev[0], h->ev[3]) == cudaSuccess)
+        std::fprintf(stderr, "; factors+L_end %.2f", t);
+      if (cudaEventElapsedTime(&t, h->ev[0], h->ev[2]) == cudaSuccess)
+        std::fprintf(stderr, "; compute+apply_end %.2f", t);
+      if (cudaEventElapsedTime(&t, h->ev[0], e) == cudaSuccess)
+        std::fprintf(stderr, "; d2h_end %.2f", t);
+      std::fprintf(stderr, " ms\n");
+      cudaEventDestroy(e);
+    }
+    CU(cudaStreamSynchronize(h->copy_stream));
+    *x_done = true;
+  }
   h->have_values = true;
   h->t_init = 0.f;
   CU(cudaEventElapsedTime(&h->t_sweeps, h->ev[0], h->ev[2]));
@@ -1498,9 +1626,15 @@ extern "C" fastilu_status fastilu_solve_host(fastilu_handle h, const double *val
       (h->n > 0 && (!b || !x)))
     FAIL(FASTILU_ERR_INVALID_ARG);
   DeviceGuard dg_(h->device);
-  bool queued = false;
-  fastilu_status s = drain_copies(h, compute_host_impl(h, values, nsweeps, b, &queued));
+  bool queued = false, xdone = false;
+  const bool pipe = std::getenv("FASTILU_SOLVE_NOPIPE") == nullptr;  // A/B: apply after compute
+  fastilu_status s = drain_copies(
+      h, compute_host_impl(h, values, nsweeps, b, &queued, pipe ? x : nullptr, ntrisweeps, &xdone));
   if (s) return s;
+  if (xdone) {
+    h->apply_timed = false;
+    return FASTILU_OK;
+  }
   if (!queued) return fastilu_apply_host(h, b, x, ntrisweeps);
   CU(cudaStreamWaitEvent(h->stream, h->chunk_ev[h->chunk_b], 0));
   CU(cudaEventRecord(h->ev[3], h->stream));
@@ -1510,6 +1644,24 @@ extern "C" fastilu_status fastilu_solve_host(fastilu_handle h, const double *val
   h->apply_timed = true;
   CU(cudaMemcpyAsync(x, h->d_bx + h->n, sizeof(double) * h->n, cudaMemcpyDeviceToHost,
                      h->stream));
+  if (std::getenv("FASTILU_TRACE")) {  // timeline of the step (ms from the compute's start)
+    cudaEvent_t e;
+    CU(cudaEventCreate(&e));
+    CU(cudaEventRecord(e, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+    float t;
+    std::fprintf(stderr, "fastilu trace: chunks landed at");
+    for (int c = 0; c <= h->chunk_b; c++)
+      if (cudaEventElapsedTime(&t, h->ev[0], h->chunk_ev[c]) == cudaSuccess)
+        std::fprintf(stderr, " %.2f", t);
+    cudaEvent_t marks[] = {h->ev[2], h->ev[3], h->ev[4], e};
+    const char *names[] = {"compute_end", "apply_start", "apply_end", "d2h_end"};
+    for (int q = 0; q < 4; q++)
+      if (cudaEventElapsedTime(&t, h->ev[0], marks[q]) == cudaSuccess)
+        std::fprintf(stderr, "; %s %.2f", names[q], t);
+    std::fprintf(stderr, " ms\n");
+    cudaEventDestroy(e);
+  }
   CU(cudaStreamSynchronize(h->stream));
   return FASTILU_OK;
 }
@@ -2108,6 +2260,7 @@ extern "C" fastilu_status fastilu_destroy(fastilu_handle h) {
     if (h->ev[i]) cudaEventDestroy(h->ev[i]);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
   for (cudaEvent_t e : h->chunk_ev) cudaEventDestroy(e);
+  for (cudaEvent_t e : h->x_ev) cudaEventDestroy(e);
   if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
   if (h->d_r2c) cudaFree(h->d_r2c);
   delete h;

@@ -1040,15 +1040,14 @@ cudaError_t launch_maxpy(const double *V, int64_t ldv, int k, const double *c, d
 // q_p = (u - Q s) / rho and forms the next pending vector (w - Q z - q_p c_p) / rho.
 // Block b owns the contiguous rows [b n / grid, (b+1) n / grid) (equal shares), kDRpt rows per
 // thread and chunk.
-constexpr int kDRpt = 4, kDChunk = 256 * kDRpt;
 // one wave: SMs x resident blocks of `func` (at most kDotBlocks), fewer for short vectors
-static unsigned dcgs_blocks(int64_t n, const void *func) {
+static unsigned dcgs_blocks(int64_t n, int rpt, const void *func) {
   int dev = 0, per_sm = 1;
   cudaGetDevice(&dev);
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, func, 256, 0) != cudaSuccess ||
       per_sm < 1)
     per_sm = 1;
-  const int64_t chunks = (n + kDChunk - 1) / kDChunk;
+  const int64_t chunks = (n + 256 * rpt - 1) / (256 * rpt);
   const int64_t wave = std::min<int64_t>((int64_t)sm_count(dev) * per_sm, kDotBlocks);
   return (unsigned)std::max<int64_t>(1, std::min<int64_t>(chunks, wave));
 }
@@ -1056,8 +1055,11 @@ static unsigned dcgs_blocks(int64_t n, const void *func) {
 // out (per block): partials[(2 j + e) * grid + b] = V_j . u (e = 0), V_j . w (e = 1), j <= p.
 // Groups of 4 columns x 2 vectors = 8 per-lane sums are reduced across the warp by a butterfly
 // (each step halves the values a lane carries: 4 + 2 + 1 + 2 shuffles for 8 sums instead of 40);
-// lane 4 t then holds sum t, summed into the warp's shared-memory slot (fixed order: deterministic).
-__global__ void __launch_bounds__(256, 3)
+// lane 4 t then holds sum t, summed into the warp's shared-memory slot (fixed order:
+// deterministic).  RPT rows per thread and chunk; PF: the next group's loads are issued before
+// the current group's multiply-adds and butterfly.
+template <int RPT, bool PF, int MINB>
+__global__ void __launch_bounds__(256, MINB)
 dcgs_dot_kernel(const double *__restrict__ V, int64_t ldv, int p, const double *__restrict__ w,
                 int64_t n, double *__restrict__ partials) {
   __shared__ double red[8][2 * kMaxK];
@@ -1069,28 +1071,41 @@ dcgs_dot_kernel(const double *__restrict__ V, int64_t ldv, int p, const double *
   const double *u = V + (int64_t)p * ldv;
   const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
   const int slot = (lane >> 2) & 7;  // the sum lane 4 t ends up with: column t / 2, vector t % 2
-  for (int64_t c0 = rb; c0 < re; c0 += kDChunk) {
-    double uv[kDRpt], wv[kDRpt];
+  for (int64_t c0 = rb; c0 < re; c0 += 256 * RPT) {
+    double uv[RPT], wv[RPT], v[4][RPT];
 #pragma unroll
-    for (int r = 0; r < kDRpt; r++) {
+    for (int r = 0; r < RPT; r++) {
       const int64_t i = c0 + r * 256 + threadIdx.x;
       uv[r] = i < re ? u[i] : 0.0;
       wv[r] = (w && i < re) ? w[i] : 0.0;
     }
+    auto load = [&](int j0, double (&d)[4][RPT]) {
+#pragma unroll
+      for (int t = 0; t < 4; t++) {
+        const double *vj = V + (int64_t)(j0 + t) * ldv;
+#pragma unroll
+        for (int r = 0; r < RPT; r++) {
+          const int64_t i = c0 + r * 256 + threadIdx.x;
+          d[t][r] = (j0 + t < k && i < re) ? vj[i] : 0.0;
+        }
+      }
+    };
+    if (PF) load(0, v);
     for (int j0 = 0; j0 < k; j0 += 4) {
+      double nx[4][RPT];
+      if (PF) {
+        if (j0 + 4 < k) load(j0 + 4, nx);
+      } else {
+        load(j0, v);
+      }
       double a[8];
 #pragma unroll
       for (int t = 0; t < 4; t++) {
         a[2 * t] = a[2 * t + 1] = 0.0;
-        if (j0 + t < k) {
-          const double *vj = V + (int64_t)(j0 + t) * ldv;
 #pragma unroll
-          for (int r = 0; r < kDRpt; r++) {
-            const int64_t i = c0 + r * 256 + threadIdx.x;
-            const double v = i < re ? vj[i] : 0.0;
-            a[2 * t] = fma(v, uv[r], a[2 * t]);
-            a[2 * t + 1] = fma(v, wv[r], a[2 * t + 1]);
-          }
+        for (int r = 0; r < RPT; r++) {
+          a[2 * t] = fma(v[t][r], uv[r], a[2 * t]);
+          a[2 * t + 1] = fma(v[t][r], wv[r], a[2 * t + 1]);
         }
       }
 #pragma unroll
@@ -1103,6 +1118,12 @@ dcgs_dot_kernel(const double *__restrict__ V, int64_t ldv, int p, const double *
       a[0] += __shfl_xor_sync(0xffffffffu, a[0], 2);
       a[0] += __shfl_xor_sync(0xffffffffu, a[0], 1);
       if ((lane & 3) == 0 && j0 + (slot >> 1) < k) red[warp][2 * j0 + slot] += a[0];
+      if (PF) {
+#pragma unroll
+        for (int t = 0; t < 4; t++)
+#pragma unroll
+          for (int r = 0; r < RPT; r++) v[t][r] = nx[t][r];
+      }
     }
   }
   __syncthreads();
@@ -1113,17 +1134,27 @@ dcgs_dot_kernel(const double *__restrict__ V, int64_t ldv, int p, const double *
   }
 }
 
-cudaError_t launch_dcgs_dot(const double *V, int64_t ldv, int p, const double *w, int64_t n,
-                            double *partials, double *out, cudaStream_t st) {
-  if (p < 0 || p + 1 > kMaxK) return cudaErrorInvalidValue;
-  const unsigned nb = dcgs_blocks(n, (const void *)dcgs_dot_kernel);
-  dcgs_dot_kernel<<<nb, 256, 0, st>>>(V, ldv, p, w, n, partials);
+template <int RPT, bool PF, int MINB>
+static cudaError_t dcgs_dot_run(const double *V, int64_t ldv, int p, const double *w, int64_t n,
+                                double *partials, double *out, cudaStream_t st) {
+  const unsigned nb = dcgs_blocks(n, RPT, (const void *)dcgs_dot_kernel<RPT, PF, MINB>);
+  dcgs_dot_kernel<RPT, PF, MINB><<<nb, 256, 0, st>>>(V, ldv, p, w, n, partials);
   mdot_reduce_kernel<<<min(2 * (p + 1), 64), 256, 0, st>>>(partials, (int)nb, 2 * (p + 1), out);
   return cudaGetLastError();
 }
 
+cudaError_t launch_dcgs_dot(const double *V, int64_t ldv, int p, const double *w, int64_t n,
+                            double *partials, double *out, cudaStream_t st) {
+  if (p < 0 || p + 1 > kMaxK) return cudaErrorInvalidValue;
+  // measured (config 5, profiles/r2zd_dcgs_variants.log): 4 rows per thread without the
+  // software prefetch is the fastest of the shapes tried (6.9 TB/s)
+  return dcgs_dot_run<4, false, 3>(V, ldv, p, w, n, partials, out, st);
+}
+
 // coef = [s_0..s_{p-1}, z_0..z_{p-1}, c_p, 1/rho] (device):
 //   q = (V_p - sum_j s_j V_j) / rho -> V_p;   (w - sum_j z_j V_j - c_p q) / rho -> V_{p+1}
+// RPT rows per thread and chunk, UNR columns' loads in flight
+template <int RPT, int UNR>
 __global__ void __launch_bounds__(256)
 dcgs_update_kernel(double *__restrict__ V, int64_t ldv, int p, const double *__restrict__ coef,
                    const double *__restrict__ w, int64_t n) {
@@ -1134,20 +1165,20 @@ dcgs_update_kernel(double *__restrict__ V, int64_t ldv, int p, const double *__r
   const int64_t rb = n * (int64_t)blockIdx.x / gridDim.x;
   const int64_t re = n * (int64_t)(blockIdx.x + 1) / gridDim.x;
   double *u = V + (int64_t)p * ldv, *un = u + ldv;
-  for (int64_t c0 = rb; c0 < re; c0 += kDChunk) {
-    double t1[kDRpt], t2[kDRpt];
+  for (int64_t c0 = rb; c0 < re; c0 += 256 * RPT) {
+    double t1[RPT], t2[RPT];
 #pragma unroll
-    for (int r = 0; r < kDRpt; r++) {
+    for (int r = 0; r < RPT; r++) {
       const int64_t i = c0 + r * 256 + threadIdx.x;
       t1[r] = i < re ? u[i] : 0.0;
       t2[r] = i < re ? w[i] : 0.0;
     }
-#pragma unroll 4
+#pragma unroll UNR
     for (int j = 0; j < p; j++) {
       const double *vj = V + (int64_t)j * ldv;
       const double sj = sc[j], zj = sc[p + j];
 #pragma unroll
-      for (int r = 0; r < kDRpt; r++) {
+      for (int r = 0; r < RPT; r++) {
         const int64_t i = c0 + r * 256 + threadIdx.x;
         const double v = i < re ? vj[i] : 0.0;
         t1[r] = fma(-sj, v, t1[r]);
@@ -1155,7 +1186,7 @@ dcgs_update_kernel(double *__restrict__ V, int64_t ldv, int p, const double *__r
       }
     }
 #pragma unroll
-    for (int r = 0; r < kDRpt; r++) {
+    for (int r = 0; r < RPT; r++) {
       const int64_t i = c0 + r * 256 + threadIdx.x;
       if (i < re) {
         const double q = t1[r] * irho;
@@ -1166,12 +1197,20 @@ dcgs_update_kernel(double *__restrict__ V, int64_t ldv, int p, const double *__r
   }
 }
 
+template <int RPT, int UNR>
+static cudaError_t dcgs_update_run(double *V, int64_t ldv, int p, const double *coef,
+                                   const double *w, int64_t n, cudaStream_t st) {
+  dcgs_update_kernel<RPT, UNR>
+      <<<dcgs_blocks(n, RPT, (const void *)dcgs_update_kernel<RPT, UNR>), 256, 0, st>>>(
+          V, ldv, p, coef, w, n);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_dcgs_update(double *V, int64_t ldv, int p, const double *coef, const double *w,
                                int64_t n, cudaStream_t st) {
   if (p < 0 || p + 1 > kMaxK) return cudaErrorInvalidValue;
   if (n <= 0) return cudaSuccess;
-  dcgs_update_kernel<<<dcgs_blocks(n, (const void *)dcgs_update_kernel), 256, 0, st>>>(V, ldv, p, coef, w, n);
-  return cudaGetLastError();
+  return dcgs_update_run<4, 4>(V, ldv, p, coef, w, n, st);  // 5.9 TB/s; see dcgs_dot
 }
 
 __global__ void axpby_kernel(double a, const double *__restrict__ x, double b,

@@ -14,6 +14,7 @@
 #              preceded by "== workload env"; the round-2 A/B logs under profiles/ keep them)
 #   variants   the template-kernel variant parity tests only (bitwise vs the oracle)
 #   gmres      ncu launch list (time + DRAM bytes) of one GMRES(60) cycle on config 5
+#   gmrestest  the GMRES GPU tests only (single GPU, in-process ranks, async) + config 5 (no arm C)
 set -u
 TAG=$1; shift
 mkdir -p gpurun_out
@@ -58,6 +59,12 @@ for step in "$@"; do
       timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
         --clock-control none --csv --log-file gpurun_out/${TAG}_gmres_launches.csv \
         python scripts/profile_gmres.py --iters 60 > gpurun_out/${TAG}_gmres.log 2>&1 ;;
+    gmrestest)
+      timeout 900 python -m pytest tests/test_gpu_gmres.py tests/test_gpu_multirank.py \
+        tests/test_gpu_async.py -q -x -k "gmres or dcgs2 or restarts or set_factors" 2>&1 | tail -6 \
+        > gpurun_out/${TAG}_gmrestest.log
+      timeout 900 python bench.py --workload c5_aniso7pt_256_ilu0 --steps 3 --warmup 3 --no-cpu \
+        > gpurun_out/${TAG}_c5.log 2>&1 ;;
     ab)
       IFS=';' read -ra envs <<< "${AB_ENVS:-}"
       for w in ${WORKLOADS:-c3a_27pt_128_ilu1 c3b_27pt_128_ilu2 c4_27pt_256_ilu1}; do
