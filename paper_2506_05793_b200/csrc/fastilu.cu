@@ -39,6 +39,7 @@ struct fastilu_handle_s {
   bool own_stream = false;
   // fastilu_compute_host: value upload pipelined with the compute (copy stream, chunk events)
   cudaStream_t copy_stream = nullptr;
+  cudaStream_t d2h_stream = nullptr;  // solve_host: x back per chunk during the upload
   std::vector<cudaEvent_t> chunk_ev;
   int chunk_b = 0;  // index of the event after the right-hand side's upload (solve_host)
   std::vector<cudaEvent_t> x_ev;  // solve_host pipeline: chunk c of x final
@@ -65,6 +66,9 @@ struct fastilu_handle_s {
   double *d_vals[2] = {nullptr, nullptr}, *d_ud[2] = {nullptr, nullptr}, *d_ahat = nullptr;
   double *d_s = nullptr, *d_ad = nullptr;
   double *d_y = nullptr, *d_z[2] = {nullptr, nullptr}, *d_w[2] = {nullptr, nullptr};
+  double *d_it = nullptr;  // solve_host pipeline: z^1..z^ntri, w^1..w^ntri
+  double *d_vals3 = nullptr, *d_ud3 = nullptr;  // compute_host pipeline: third iterate buffer
+  int it_cap = 0;
   double *d_bx = nullptr;  // apply_host staging (2 n)
   double *d_partials = nullptr, *d_r2 = nullptr;
   int hist_cap = 0;
@@ -113,6 +117,7 @@ struct fastilu_handle_s {
     unsigned char b[128];
   } st_tmap[2], st_tmap_ahat;  // per iterate buffer d_vals[0/1]; over d_ahat
   TMapBuf st_tmap_own[2], st_tmap_own_ahat;  // own-row boxes (kStagedOwnL)
+  TMapBuf st_tmap3, st_tmap_own3;  // over d_vals3
   int t_parts = 1, t_minb = 0, t_sstride = 1;
   bool t_prefetch = true;
   int t_threads = 128, t_grid = 1, t_regs = 0, t_spill = 0, t_rows_tile = 128;
@@ -176,14 +181,15 @@ extern "C" int64_t fastilu_required_lead_rows(int64_t bandwidth, int level_k) {
   return 2 * (int64_t)(level_k + 1) * std::max<int64_t>(bandwidth, 1);
 }
 
-#define CU(x)                                  \
-  do {                                         \
-    cudaError_t e_ = (x);                      \
-    if (e_ != cudaSuccess) {                   \
-      return e_ == cudaErrorMemoryAllocation   \
-                 ? FASTILU_ERR_OOM             \
-                 : FASTILU_ERR_CUDA;           \
-    }                                          \
+#define CU(x)                                                                        \
+  do {                                                                               \
+    cudaError_t e_ = (x);                                                            \
+    if (e_ != cudaSuccess) {                                                         \
+      if (std::getenv("FASTILU_DEBUG"))                                              \
+        fprintf(stderr, "fastilu: %s at %s:%d\n", cudaGetErrorString(e_), __FILE__, \
+                __LINE__);                                                           \
+      return e_ == cudaErrorMemoryAllocation ? FASTILU_ERR_OOM : FASTILU_ERR_CUDA;   \
+    }                                                                                \
   } while (0)
 
 template <class T>
@@ -1381,6 +1387,18 @@ static fastilu_status compute_host_impl(fastilu_handle h, const double *values, 
     h->r2c_cap = C * nsweeps;
   }
   auto rb = [&](int c) { return bnd[c]; };
+  // FASTILU_DEBUG_SYNC=1: synchronise after every step of the pipeline and name a failing one
+  static const bool dbg_sync = std::getenv("FASTILU_DEBUG_SYNC") != nullptr;
+  auto dbg = [&](const char *what, int a, int b2) -> fastilu_status {
+    if (!dbg_sync) return FASTILU_OK;
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+      fprintf(stderr, "fastilu: %s after %s (%d, %d)\n", cudaGetErrorString(e), what, a, b2);
+      return FASTILU_ERR_CUDA;
+    }
+    return FASTILU_OK;
+  };
+
   CU(cudaMemsetAsync(h->d_err, 0xff, sizeof(ErrFlags), st));
   CU(cudaEventRecord(h->ev[0], st));
   // every chunk's values up front on the copy stream, ordered after the compute stream's
@@ -1424,7 +1442,7 @@ static fastilu_status compute_host_impl(fastilu_handle h, const double *values, 
     double *sp = h->d_s, *adp = h->d_ad;
     void *args[] = {&aT, &z0, &z1, &sp, &adp, &ep, (void *)&sh};
     if (jit_launch(h->jit_scale, (int)((z1 - z0 + 255) / 256), 256, st, args)) FAIL(FASTILU_ERR_CUDA);
-    return FASTILU_OK;
+    return dbg("prep", c, 0);
   };
   auto ahat = [&](int c) -> fastilu_status {
     const double *aT = h->d_aT, *sv = h->d_s;
@@ -1434,19 +1452,48 @@ static fastilu_status compute_host_impl(fastilu_handle h, const double *values, 
     long long zown = 0;
     void *args[] = {&aT, &sv, &mk, &z0, &z1, &hp, &ep, (void *)&sh, &zown};
     if (jit_launch(h->jit_ahat, (int)((z1 - z0 + 255) / 256), 256, st, args)) FAIL(FASTILU_ERR_CUDA);
-    return FASTILU_OK;
+    return dbg("ahat", c, 0);
   };
+  // nodiag (nsweeps <= 3): every iterate of the sweeps has its own buffer -- iterate s in
+  // buffer bufi[s] (the last in d_vals[nsweeps & 1] as after compute; a third iterate buffer
+  // for nsweeps = 3) -- so all sweeps of chunk k run as soon as its Â is known, instead of along
+  // the diagonal the two ping-pong buffers need (FASTILU_SOLVE_DIAG=1: the diagonal)
+  const bool nodiag = nsweeps <= 3 && !std::getenv("FASTILU_SOLVE_DIAG");
+  int bufi[4] = {0, 1, 0, 1};  // ping-pong: iterate s in buffer s & 1
+  if (nodiag) {
+    if (nsweeps == 2) bufi[1] = 1, bufi[2] = 0;
+    if (nsweeps == 3) {
+      bufi[1] = 2, bufi[2] = 0, bufi[3] = 1;
+      if (!h->d_vals3) {
+        const int64_t nv = h->nsl * h->T.W * 32;
+        CU(dalloc(&h->d_vals3, nv));
+        CU(cudaMemsetAsync(h->d_vals3, 0, sizeof(double) * nv, st));  // absent slots stay +0.0
+        CU(dalloc(&h->d_ud3, std::max<int64_t>(h->nsl * 32, 1)));
+        const bool cm = h->st.colmajor != 0;
+        if ((cm ? jit_tmap_sell_cm : jit_tmap_sell)(h->st_tmap3.b, h->d_vals3, h->T.W, h->nsl,
+                                                    h->st.box_cols, h->st.box_slices) ||
+            (cm ? jit_tmap_sell_cm : jit_tmap_sell)(h->st_tmap_own3.b, h->d_vals3, h->T.W,
+                                                    h->nsl, std::max(1, h->st.own_cols),
+                                                    h->st.rows / 32))
+          FAIL(FASTILU_ERR_CUDA);
+      }
+    }
+  }
+  auto vbuf = [&](int b) { return b == 2 ? h->d_vals3 : h->d_vals[b]; };
+  auto ubuf = [&](int b) { return b == 2 ? h->d_ud3 : h->d_ud[b]; };
+  auto tmapb = [&](int b) { return b == 2 ? h->st_tmap3.b : h->st_tmap[b].b; };
+  auto tmapo = [&](int b) { return b == 2 ? h->st_tmap_own3.b : h->st_tmap_own[b].b; };
   auto sweep = [&](int sw, int c) -> fastilu_status {
-    const int ib = (sw - 1) & 1, ob = sw & 1;
-    const double *old = h->d_vals[ib], *ahp = h->d_ahat;
-    double *outp = h->d_vals[ob], *udn = h->d_ud[ob], *part = h->d_partials;
+    const int ib = sw >= 2 ? bufi[sw - 1] : 0, ob = bufi[sw];
+    const double *old = vbuf(ib), *ahp = h->d_ahat;
+    double *outp = vbuf(ob), *udn = ubuf(ob), *part = h->d_partials;
     const unsigned long long *mk = h->d_tmask;
     long long a0 = rb(c), a1 = rb(c + 1);
     double om = 1.0;
     unsigned long long *zp = &h->d_err->zero_pivot;
     unsigned int *ctr = h->d_counter;
     void *sargs[] = {&old, &outp, &ahp, &mk, &udn, &a0, &a1, &om, &part, &zp, &ctr,
-                     h->st_tmap[ib].b, h->st_tmap_own[ib].b};
+                     tmapb(ib), tmapo(ib)};
     void *fn = h->jit_st;
     int smem = h->st.smem, thr = h->st.threads, gmax = h->st_grid;
     int64_t Rk = R;
@@ -1464,66 +1511,72 @@ static fastilu_status compute_host_impl(fastilu_handle h, const double *values, 
     if (jit_launch_smem(fn, grid, thr, smem, st, sargs)) FAIL(FASTILU_ERR_CUDA);
     CU(launch_reduce_reset(h->d_partials, (int)nt, h->d_r2c + (int64_t)c * nsweeps + (sw - 1),
                            h->d_counter, st));
-    return FASTILU_OK;
+    return dbg("sweep", sw, c);
   };
   auto diag = [&](int d) -> fastilu_status {  // step d: sweep s on chunk d - s + 1
     for (int sw = 1; sw <= nsweeps; sw++) {
-      const int c = d - sw + 1;
+      const int c = nodiag ? d : d - sw + 1;  // nodiag: all sweeps of chunk d
       if (c < 0 || c >= C) continue;
       fastilu_status fs = sweep(sw, c);
       if (fs) return fs;
     }
     return FASTILU_OK;
   };
-  // apply pipeline (pipe_x): L step e runs Jacobi sweep t on chunk e - t + 1 (t ascending; the
-  // factors of chunk e are final after factor step e + nsweeps - 1), U step e sweep t on chunk
-  // C - 1 - (e - t + 1); the ping-pong buffers are safe by the same diagonal argument as the
-  // factor sweeps (L sweep t of chunk c reads iterate t-1 of chunks c-1, c; U of chunks c, c+1)
+  // apply pipeline (pipe_x), one buffer per Jacobi iterate (z^1..z^ntri, w^1..w^ntri: 2 ntri
+  // vectors, 1.3 GB at c4) so that no iterate a later chunk still reads is overwritten:
+  //  * L of chunk k, as soon as its factors are final: z^1 .. z^ntri of chunk k in turn (sweep t
+  //    of chunk k reads z^{t-1} of chunks k-1 and k, both complete);
+  //  * then the U cone: w^1 of chunk k, w^2 of chunk k-1, ..., w^ntri of chunk k-ntri+1 (sweep t
+  //    of chunk c reads w^{t-1} of chunks c and c+1, and w^t of chunk c needs z of chunks
+  //    c..c+t-1 only), so chunk c's x is final once chunk c + ntri - 1's z is, and goes back at
+  //    once on its own stream (PCIe's other direction, concurrent with the upload).
   const double omt = h->opt.omega_tri;
   const int fb = nsweeps & 1;
   const double *fvals = h->d_vals[fb], *fud = h->d_ud[fb];
   double *xd = h->d_bx + h->n;
-  auto lstep = [&](int e) -> fastilu_status {
-    for (int t = 1; t <= ntri; t++) {
-      const int c = e - t + 1;
-      if (c < 0 || c >= C) continue;
-      if (t == 1)
-        CU(launch_trisolve_first_L(h->d_bx, h->d_s, h->d_y, h->d_z[0], rb(c), rb(c + 1), 0, omt,
-                                   st));
-      else if (jit_jacobi(h, true, fvals, nullptr, h->d_y, h->d_z[(t - 2) & 1],
-                          h->d_z[(t - 1) & 1], nullptr, rb(c), rb(c + 1), 0, omt, false))
-        FAIL(FASTILU_ERR_CUDA);
+  if (pipe_x) {
+    if (!h->d2h_stream) CU(cudaStreamCreateWithFlags(&h->d2h_stream, cudaStreamNonBlocking));
+    if (h->it_cap < ntri) {
+      if (h->d_it) cudaFree(h->d_it);
+      h->d_it = nullptr;
+      h->it_cap = 0;
+      CU(dalloc(&h->d_it, (int64_t)2 * ntri * std::max<int64_t>(h->n, 1)));
+      h->it_cap = ntri;
+    }
+  }
+  auto zt = [&](int t) { return h->d_it + (int64_t)(t - 1) * h->n; };           // z^t
+  auto wt = [&](int t) { return h->d_it + (int64_t)(ntri + t - 1) * h->n; };    // w^t
+  auto usweep = [&](int t, int c) -> fastilu_status {  // w^t of chunk c (+ x when t == ntri)
+    if (t == 1)
+      CU(launch_trisolve_first_U(zt(ntri), fud, h->d_s, wt(1), xd, rb(c), rb(c + 1), 0, omt,
+                                 ntri == 1, st));
+    else if (jit_jacobi(h, false, fvals, fud, zt(ntri), wt(t - 1), wt(t), xd, rb(c), rb(c + 1), 0,
+                        omt, t == ntri))
+      FAIL(FASTILU_ERR_CUDA);
+    if (fastilu_status ds = dbg("usweep", t, c)) return ds;
+    if (t == ntri) {  // x of chunk c is final
+      CU(cudaEventRecord(h->x_ev[c], st));
+      CU(cudaStreamWaitEvent(h->d2h_stream, h->x_ev[c], 0));
+      CU(cudaMemcpyAsync(x_host + rb(c), xd + rb(c), sizeof(double) * (rb(c + 1) - rb(c)),
+                         cudaMemcpyDeviceToHost, h->d2h_stream));
     }
     return FASTILU_OK;
   };
-  // U chunks: pairs of pipeline chunks counted from the top (fewer, longer U launches; measured
-  // 74.3 -> 74.1 ms; FASTILU_SOLVE_UCOARSE overrides the 2)
-  std::vector<int64_t> ub;
-  {
-    const char *ue = std::getenv("FASTILU_SOLVE_UCOARSE");
-    const int uk = std::max(1, ue ? std::atoi(ue) : 2);
-    for (int c = C; c >= 0; c -= uk) ub.push_back(bnd[c]);
-    if (ub.back() != 0) ub.push_back(0);
-    std::reverse(ub.begin(), ub.end());
-  }
-  const int CU_ = (int)ub.size() - 1;
-  auto ustep = [&](int e) -> fastilu_status {
-    const double *zf = h->d_z[(ntri - 1) & 1];
+  // chunk k's factors are final (k = C .. C + ntri - 2: only the rest of the U cone)
+  auto lu_chunk = [&](int k) -> fastilu_status {
+    if (k < C) {
+      CU(launch_trisolve_first_L(h->d_bx, h->d_s, h->d_y, zt(1), rb(k), rb(k + 1), 0, omt, st));
+      for (int t = 2; t <= ntri; t++)
+        if (jit_jacobi(h, true, fvals, nullptr, h->d_y, zt(t - 1), zt(t), nullptr, rb(k),
+                       rb(k + 1), 0, omt, false))
+          FAIL(FASTILU_ERR_CUDA);
+      if (fastilu_status ds = dbg("L", k, 0)) return ds;
+    }
     for (int t = 1; t <= ntri; t++) {
-      const int c = CU_ - 1 - (e - t + 1);
-      if (c < 0 || c >= CU_) continue;
-      if (t == 1)
-        CU(launch_trisolve_first_U(zf, fud, h->d_s, h->d_w[0], xd, ub[c], ub[c + 1], 0, omt,
-                                   ntri == 1, st));
-      else if (jit_jacobi(h, false, fvals, fud, zf, h->d_w[(t - 2) & 1], h->d_w[(t - 1) & 1], xd,
-                          ub[c], ub[c + 1], 0, omt, t == ntri))
-        FAIL(FASTILU_ERR_CUDA);
-      if (t == ntri) {  // x of chunk c is final: copy it back on the copy stream
-        CU(cudaEventRecord(h->x_ev[c], st));
-        CU(cudaStreamWaitEvent(h->copy_stream, h->x_ev[c], 0));
-        CU(cudaMemcpyAsync(x_host + ub[c], xd + ub[c], sizeof(double) * (ub[c + 1] - ub[c]),
-                           cudaMemcpyDeviceToHost, h->copy_stream));
-      }
+      const int c = k - t + 1;
+      if (c < 0 || c >= C) continue;
+      fastilu_status us = usweep(t, c);
+      if (us) return us;
     }
     return FASTILU_OK;
   };
@@ -1533,20 +1586,20 @@ static fastilu_status compute_host_impl(fastilu_handle h, const double *values, 
     if (c >= 1) {
       if ((fs = ahat(c - 1))) return fs;
       if ((fs = diag(c - 1))) return fs;
-      if (pipe_x && c - nsweeps >= 0 && (fs = lstep(c - nsweeps))) return fs;
+      const int k = nodiag ? c - 1 : c - nsweeps;  // chunk whose factors are now final
+      if (pipe_x && k >= 0 && (fs = lu_chunk(k))) return fs;
     }
   }
   if ((fs = ahat(C - 1))) return fs;
   for (int d = C - 1; d <= C + nsweeps - 2; d++) {
     if ((fs = diag(d))) return fs;
-    if (pipe_x && d - nsweeps + 1 >= 0 && (fs = lstep(d - nsweeps + 1))) return fs;
+    const int k = nodiag ? d : d - nsweeps + 1;
+    if (pipe_x && k >= 0 && k < C && (fs = lu_chunk(k))) return fs;
   }
   if (pipe_x) {
-    for (int e = C; e <= C + ntri - 2; e++)
-      if ((fs = lstep(e))) return fs;
     CU(cudaEventRecord(h->ev[3], st));  // trace: factors and L sweeps done
-    for (int e = 0; e <= CU_ + ntri - 2; e++)
-      if ((fs = ustep(e))) return fs;
+    for (int k = C; k <= C + ntri - 2; k++)
+      if ((fs = lu_chunk(k))) return fs;
   }
   CU(cudaEventRecord(h->ev[2], st));
   std::vector<double> r2c((size_t)C * nsweeps);
@@ -1558,8 +1611,8 @@ static fastilu_status compute_host_impl(fastilu_handle h, const double *values, 
     if (std::getenv("FASTILU_TRACE")) {  // timeline (ms from the compute's start)
       cudaEvent_t e;
       CU(cudaEventCreate(&e));
-      CU(cudaEventRecord(e, h->copy_stream));
-      CU(cudaStreamSynchronize(h->copy_stream));
+      CU(cudaEventRecord(e, h->d2h_stream));
+      CU(cudaStreamSynchronize(h->d2h_stream));
       float t;
       std::fprintf(stderr, "fastilu trace (pipelined apply): chunks landed at");
       for (int c = 0; c < C; c++)
@@ -1575,6 +1628,7 @@ static fastilu_status compute_host_impl(fastilu_handle h, const double *values, 
       cudaEventDestroy(e);
     }
     CU(cudaStreamSynchronize(h->copy_stream));
+    CU(cudaStreamSynchronize(h->d2h_stream));
     *x_done = true;
   }
   h->have_values = true;
@@ -1608,6 +1662,7 @@ static fastilu_status compute_host_impl(fastilu_handle h, const double *values, 
 // the caller's buffers when the call returns (the caller may free them).
 static fastilu_status drain_copies(fastilu_handle h, fastilu_status s) {
   if (s != FASTILU_OK && h->copy_stream) cudaStreamSynchronize(h->copy_stream);
+  if (s != FASTILU_OK && h->d2h_stream) cudaStreamSynchronize(h->d2h_stream);
   return s;
 }
 
@@ -2262,6 +2317,10 @@ extern "C" fastilu_status fastilu_destroy(fastilu_handle h) {
   for (cudaEvent_t e : h->chunk_ev) cudaEventDestroy(e);
   for (cudaEvent_t e : h->x_ev) cudaEventDestroy(e);
   if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
+  if (h->d2h_stream) cudaStreamDestroy(h->d2h_stream);
+  if (h->d_it) cudaFree(h->d_it);
+  if (h->d_vals3) cudaFree(h->d_vals3);
+  if (h->d_ud3) cudaFree(h->d_ud3);
   if (h->d_r2c) cudaFree(h->d_r2c);
   delete h;
   return FASTILU_OK;

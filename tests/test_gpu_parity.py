@@ -455,14 +455,14 @@ def test_compute_host_new_values_and_errors():
 def test_solve_host_equals_compute_and_apply(nt, om_tri, pipe, monkeypatch):
     """fastilu_solve_host (values + b uploaded on the copy stream in chunks, the last one cut into
     pieces of at least the band) = compute + apply, bitwise.  Default: the apply runs chunk by
-    chunk inside the upload pipeline (L sweeps behind the factor sweeps, U sweeps along a
-    descending diagonal over pairs of chunks, x copied back per U chunk); FASTILU_SOLVE_NOPIPE=1
-    runs it after the compute; "tail" uses 8 tail pieces and single-chunk U steps."""
+    chunk inside the upload pipeline (a chunk's L sweeps as soon as its factors are final, the U
+    sweeps along their dependency cone right behind, one buffer per Jacobi iterate, x copied
+    back per chunk); FASTILU_SOLVE_NOPIPE=1 runs it after the compute; "tail" uses 8 tail
+    pieces."""
     if pipe is False:
         monkeypatch.setenv("FASTILU_SOLVE_NOPIPE", "1")
     if pipe == "tail":
         monkeypatch.setenv("FASTILU_SOLVE_TAIL", "8")
-        monkeypatch.setenv("FASTILU_SOLVE_UCOARSE", "1")
     a = P.laplace3d_27pt(24, gz=70)
     b = P.rhs_positive(a.n)
     f = F.FastILU(a.row_ptr, a.col_idx, a.values, 1, omega_tri=om_tri)
