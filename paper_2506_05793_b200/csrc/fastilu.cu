@@ -1315,12 +1315,13 @@ static int jit_jacobi(fastilu_handle h, bool lower, const double *vals, const do
 // s of chunk c reads iterate s-1 of rows <= its own only.  Same kernels, same per-entry
 // arithmetic as set_values + compute; only the residual's sum is taken per chunk.
 //
-// With x_host (solve_host; FASTILU_SOLVE_NOPIPE=1 runs the apply after the compute instead), the
-// apply rides the same pipeline: b goes up
-// chunk by chunk behind the values, the L Jacobi sweeps of chunk c run (along their own
-// diagonal) as soon as chunk c's factors are final, and once every chunk's L sweeps are done
-// the U sweeps run along a descending diagonal, each chunk's x copied back as soon as its last
-// U sweep is done.  Same kernels, rows and order of terms as apply: x is bitwise the same.
+// With nsweeps <= 3 every factor iterate has its own buffer and all sweeps of a chunk run at
+// once (no diagonal).  With x_host (solve_host; FASTILU_SOLVE_NOPIPE=1 runs the apply after the
+// compute instead), the apply rides the same pipeline: b goes up chunk by chunk behind the
+// values, a chunk's L Jacobi sweeps run as soon as its factors are final and the U sweeps follow
+// their dependency cone right behind (one buffer per Jacobi iterate), each chunk's x copied back
+// as soon as its last U sweep is done.  Same kernels, rows and order of terms as apply: x is
+// bitwise the same.
 static fastilu_status compute_host_impl(fastilu_handle h, const double *values, int nsweeps,
                                         const double *b_host = nullptr,
                                         bool *b_queued = nullptr, double *x_host = nullptr,
