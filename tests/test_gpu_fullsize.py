@@ -106,6 +106,16 @@ def test_config4_27pt_256():
     assert f.info().startswith("path=tsell")
     # first and last planes (TMA zero-fill below plane 0, the last tile's tail) and the middle
     check_planes(a, b, "27pt", g, k, ns, nt, [0, 128, 255], vals, rp, ci, x)
+    # the e2e entry bench.py times (fastilu_solve_host: values + b uploaded in chunks, the sweeps,
+    # the Jacobi L sweeps and the U cone pipelined behind the upload, x copied back per chunk)
+    # returns the same x, bitwise, and leaves the same factors
+    av = torch.from_numpy(a.values).pin_memory().numpy()
+    bh = torch.from_numpy(b).pin_memory().numpy()
+    xh = torch.empty(a.n, dtype=torch.float64).pin_memory().numpy()
+    f.solve_host(av, ns, bh, nt, out=xh)
+    assert np.array_equal(xh, x)
+    v2, _ = f.factors()
+    assert np.array_equal(v2, vals)
 
 
 def test_config2_7pt_128_exact():
