@@ -84,6 +84,10 @@ cudaError_t launch_trisolve_first_L(const double *b, const double *s, double *y,
                                     int64_t r0, int64_t r1, int64_t G, double omega,
                                     cudaStream_t st);
 // w1 = omega * z / u_ii; if final: x[r - G] = s * w1
+// ntri = 1 in one pass: x[r - G] = s o (omega (omega (s o b)) / u_ii), bitwise first_L + first_U
+cudaError_t launch_trisolve_first_LU(const double *b, const double *s, const double *udiag,
+                                     double *x, int64_t r0, int64_t r1, int64_t G, double omega,
+                                     cudaStream_t st);
 cudaError_t launch_trisolve_first_U(const double *z, const double *udiag, const double *s,
                                     double *w, double *x, int64_t r0, int64_t r1, int64_t G,
                                     double omega, bool final, cudaStream_t st);

@@ -1406,7 +1406,46 @@ static fastilu_status compute_host_impl(fastilu_handle h, const double *values, 
   // previous work (the previous compute may still read d_aval / d_aT)
   CU(cudaEventRecord(h->ev[1], st));
   CU(cudaStreamWaitEvent(h->copy_stream, h->ev[1], 0));
-  const bool pipe_x = b_host && x_host && ntri >= 1 && h->jit_jac[0] && h->jit_jac[1];
+  // The buffers this call adds are allocated before its uploads and kernels are queued; without
+  // the memory for them it falls back (to the diagonal / to the apply after the compute).
+  // nodiag (nsweeps <= 3): every iterate of the sweeps has its own buffer -- iterate s in
+  // buffer bufi[s] (the last in d_vals[nsweeps & 1] as after compute; a third iterate buffer
+  // for nsweeps = 3) -- so all sweeps of chunk k run as soon as its Â is known, instead of along
+  // the diagonal the two ping-pong buffers need (FASTILU_SOLVE_DIAG=1: the diagonal)
+  bool nodiag = nsweeps <= 3 && !std::getenv("FASTILU_SOLVE_DIAG");
+  if (nodiag && nsweeps == 3 && !h->d_vals3) {
+    const int64_t nv = h->nsl * h->T.W * 32;
+    if (dalloc(&h->d_vals3, nv) != cudaSuccess ||
+        dalloc(&h->d_ud3, std::max<int64_t>(h->nsl * 32, 1)) != cudaSuccess) {
+      (void)cudaGetLastError();
+      if (h->d_vals3) cudaFree(h->d_vals3);
+      h->d_vals3 = nullptr;
+      h->d_ud3 = nullptr;
+      nodiag = false;
+    } else {
+      CU(cudaMemsetAsync(h->d_vals3, 0, sizeof(double) * nv, st));  // absent slots stay +0.0
+      const bool cm = h->st.colmajor != 0;
+      if ((cm ? jit_tmap_sell_cm : jit_tmap_sell)(h->st_tmap3.b, h->d_vals3, h->T.W, h->nsl,
+                                                  h->st.box_cols, h->st.box_slices) ||
+          (cm ? jit_tmap_sell_cm : jit_tmap_sell)(h->st_tmap_own3.b, h->d_vals3, h->T.W,
+                                                  h->nsl, std::max(1, h->st.own_cols),
+                                                  h->st.rows / 32))
+        FAIL(FASTILU_ERR_CUDA);
+    }
+  }
+  bool pipe_x = b_host && x_host && ntri >= 1 && h->jit_jac[0] && h->jit_jac[1];
+  if (pipe_x && h->it_cap < ntri) {  // one buffer per Jacobi iterate
+    if (h->d_it) cudaFree(h->d_it);
+    h->d_it = nullptr;
+    h->it_cap = 0;
+    if (dalloc(&h->d_it, (int64_t)2 * ntri * std::max<int64_t>(h->n, 1)) != cudaSuccess) {
+      (void)cudaGetLastError();
+      h->d_it = nullptr;
+      pipe_x = false;
+    } else {
+      h->it_cap = ntri;
+    }
+  }
   if (pipe_x) {
     if (!h->d_bx) CU(dalloc(&h->d_bx, 2 * h->n));
     while ((int)h->x_ev.size() < C) {
@@ -1455,31 +1494,9 @@ static fastilu_status compute_host_impl(fastilu_handle h, const double *values, 
     if (jit_launch(h->jit_ahat, (int)((z1 - z0 + 255) / 256), 256, st, args)) FAIL(FASTILU_ERR_CUDA);
     return dbg("ahat", c, 0);
   };
-  // nodiag (nsweeps <= 3): every iterate of the sweeps has its own buffer -- iterate s in
-  // buffer bufi[s] (the last in d_vals[nsweeps & 1] as after compute; a third iterate buffer
-  // for nsweeps = 3) -- so all sweeps of chunk k run as soon as its Â is known, instead of along
-  // the diagonal the two ping-pong buffers need (FASTILU_SOLVE_DIAG=1: the diagonal)
-  const bool nodiag = nsweeps <= 3 && !std::getenv("FASTILU_SOLVE_DIAG");
   int bufi[4] = {0, 1, 0, 1};  // ping-pong: iterate s in buffer s & 1
-  if (nodiag) {
-    if (nsweeps == 2) bufi[1] = 1, bufi[2] = 0;
-    if (nsweeps == 3) {
-      bufi[1] = 2, bufi[2] = 0, bufi[3] = 1;
-      if (!h->d_vals3) {
-        const int64_t nv = h->nsl * h->T.W * 32;
-        CU(dalloc(&h->d_vals3, nv));
-        CU(cudaMemsetAsync(h->d_vals3, 0, sizeof(double) * nv, st));  // absent slots stay +0.0
-        CU(dalloc(&h->d_ud3, std::max<int64_t>(h->nsl * 32, 1)));
-        const bool cm = h->st.colmajor != 0;
-        if ((cm ? jit_tmap_sell_cm : jit_tmap_sell)(h->st_tmap3.b, h->d_vals3, h->T.W, h->nsl,
-                                                    h->st.box_cols, h->st.box_slices) ||
-            (cm ? jit_tmap_sell_cm : jit_tmap_sell)(h->st_tmap_own3.b, h->d_vals3, h->T.W,
-                                                    h->nsl, std::max(1, h->st.own_cols),
-                                                    h->st.rows / 32))
-          FAIL(FASTILU_ERR_CUDA);
-      }
-    }
-  }
+  if (nodiag && nsweeps == 2) bufi[1] = 1, bufi[2] = 0;
+  if (nodiag && nsweeps == 3) bufi[1] = 2, bufi[2] = 0, bufi[3] = 1;
   auto vbuf = [&](int b) { return b == 2 ? h->d_vals3 : h->d_vals[b]; };
   auto ubuf = [&](int b) { return b == 2 ? h->d_ud3 : h->d_ud[b]; };
   auto tmapb = [&](int b) { return b == 2 ? h->st_tmap3.b : h->st_tmap[b].b; };
@@ -1535,16 +1552,8 @@ static fastilu_status compute_host_impl(fastilu_handle h, const double *values, 
   const int fb = nsweeps & 1;
   const double *fvals = h->d_vals[fb], *fud = h->d_ud[fb];
   double *xd = h->d_bx + h->n;
-  if (pipe_x) {
-    if (!h->d2h_stream) CU(cudaStreamCreateWithFlags(&h->d2h_stream, cudaStreamNonBlocking));
-    if (h->it_cap < ntri) {
-      if (h->d_it) cudaFree(h->d_it);
-      h->d_it = nullptr;
-      h->it_cap = 0;
-      CU(dalloc(&h->d_it, (int64_t)2 * ntri * std::max<int64_t>(h->n, 1)));
-      h->it_cap = ntri;
-    }
-  }
+  if (pipe_x && !h->d2h_stream)
+    CU(cudaStreamCreateWithFlags(&h->d2h_stream, cudaStreamNonBlocking));
   auto zt = [&](int t) { return h->d_it + (int64_t)(t - 1) * h->n; };           // z^t
   auto wt = [&](int t) { return h->d_it + (int64_t)(ntri + t - 1) * h->n; };    // w^t
   auto usweep = [&](int t, int c) -> fastilu_status {  // w^t of chunk c (+ x when t == ntri)
@@ -1771,6 +1780,10 @@ static fastilu_status apply_impl(fastilu_handle h, const double *b, double *x, i
   const double om = h->opt.omega_tri;
   const double *vals = h->vals_cur;
   const double *ud = h->ud_cur;
+  if (ntri == 1) {  // one sweep each: x = s o (w (w y) / u_ii), one pass (no halo needed)
+    CU(launch_trisolve_first_LU(b, h->d_s, ud, x, r0, r1, h->G, om, st));
+    return FASTILU_OK;
+  }
   // a8: L sweeps.  t = 1: z1 = w y with y = s o b (z0 = 0)
   CU(launch_trisolve_first_L(b, h->d_s, h->d_y, h->d_z[0], r0, r1, h->G, om, st));
   // multi-GPU template path: the vector halo of a sweep flies on the comm's halo stream while

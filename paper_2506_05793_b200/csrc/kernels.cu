@@ -563,6 +563,31 @@ cudaError_t launch_trisolve_first_L(const double *b, const double *s, double *y,
   return cudaGetLastError();
 }
 
+// ntri = 1: the first L and the first U sweep in one pass, x = s o (w (w (s o b)) / u_ii) with
+// the same rounded operations in the same order as first_L then first_U (bitwise the same x;
+// y and z are not stored: nothing reads them after a one-sweep apply)
+__global__ void first_LU_kernel(const double *__restrict__ b, const double *__restrict__ s,
+                                const double *__restrict__ ud, double *__restrict__ x, int64_t r0,
+                                int64_t r1, int64_t G, double omega) {
+  for (int64_t r = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < r1;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const double si = s[r];
+    const double yi = __dmul_rn(si, b[r - G]);
+    const double zi = (omega == 1.0) ? yi : __dmul_rn(omega, yi);
+    const double u = __ddiv_rn(zi, ud[r]);
+    const double wi = (omega == 1.0) ? u : __dmul_rn(omega, u);
+    x[r - G] = __dmul_rn(si, wi);
+  }
+}
+
+cudaError_t launch_trisolve_first_LU(const double *b, const double *s, const double *udiag,
+                                     double *x, int64_t r0, int64_t r1, int64_t G, double omega,
+                                     cudaStream_t st) {
+  if (r1 <= r0) return cudaSuccess;
+  first_LU_kernel<<<vec_blocks(r1 - r0), 256, 0, st>>>(b, s, udiag, x, r0, r1, G, omega);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_trisolve_first_U(const double *z, const double *udiag, const double *s,
                                     double *w, double *x, int64_t r0, int64_t r1, int64_t G,
                                     double omega, bool final, cudaStream_t st) {

@@ -150,6 +150,14 @@ def test_few_trisweeps(nt):
     full_check(P.laplace3d_7pt(12), 0, 2, nt)
 
 
+@pytest.mark.parametrize("om_tri", [1.0, 0.7])
+def test_one_trisweep_fused(om_tri):
+    """ntri = 1 runs the first L and U sweeps as one pass (first_LU_kernel): x bitwise the
+    oracle's one-sweep apply, damped or not, on the template and the CSR path."""
+    full_check(P.laplace3d_27pt(9), 1, 3, 1, omega_tri=om_tri)
+    full_check(P.random_sparse(300, 0.03, seed=5), 1, 3, 1, omega_tri=om_tri)
+
+
 def test_zero_and_many_sweeps():
     full_check(P.laplace3d_27pt(6), 1, 0, 3)
     full_check(P.laplace3d_27pt(6), 1, 40, 30)  # converged to the exact ILU
