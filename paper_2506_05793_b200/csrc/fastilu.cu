@@ -1351,9 +1351,12 @@ static fastilu_status compute_host_impl(fastilu_handle h, const double *values, 
   }
   bnd.push_back(h->n);
   const int C = (int)bnd.size() - 1;
-  const bool ok = h->tsell && !h->comm && h->jit_st && h->jit_st_init && h->jit_ahat &&
-                  h->jit_scale && nsweeps >= 1 && h->opt.omega == 1.0 && h->G == 0 &&
-                  h->st.shift == 0 && C >= 2 &&
+  // staged template sweeps (init fused into sweep 1), or the register-pivot template sweeps
+  // (narrow templates: iterate 0 stored by the init kernel, diagonal schedule)
+  const bool staged_ok = h->jit_st && h->jit_st_init && h->jit_ahat && h->st.shift == 0;
+  const bool regp = !staged_ok && h->jit_sweep != nullptr;
+  const bool ok = h->tsell && !h->comm && (staged_ok || regp) && h->jit_scale && nsweeps >= 1 &&
+                  h->opt.omega == 1.0 && h->G == 0 && C >= 2 &&
                   !std::getenv("FASTILU_NO_PIPELINE");
   if (!ok) {
     fastilu_status us = upload_values(h, values, false);
@@ -1412,7 +1415,7 @@ static fastilu_status compute_host_impl(fastilu_handle h, const double *values, 
   // buffer bufi[s] (the last in d_vals[nsweeps & 1] as after compute; a third iterate buffer
   // for nsweeps = 3) -- so all sweeps of chunk k run as soon as its Â is known, instead of along
   // the diagonal the two ping-pong buffers need (FASTILU_SOLVE_DIAG=1: the diagonal)
-  bool nodiag = nsweeps <= 3 && !std::getenv("FASTILU_SOLVE_DIAG");
+  bool nodiag = nsweeps <= 3 && !regp && !std::getenv("FASTILU_SOLVE_DIAG");
   if (nodiag && nsweeps == 3 && !h->d_vals3) {
     const int64_t nv = h->nsl * h->T.W * 32;
     if (dalloc(&h->d_vals3, nv) != cudaSuccess ||
@@ -1485,6 +1488,11 @@ static fastilu_status compute_host_impl(fastilu_handle h, const double *values, 
     return dbg("prep", c, 0);
   };
   auto ahat = [&](int c) -> fastilu_status {
+    if (regp) {  // Â and iterate 0 of chunk c (its neighbours' scales exist now)
+      CU(launch_tsell_init(tdev(h), h->d_aT, h->d_s, h->d_ad, rb(c), rb(c + 1), h->d_ahat,
+                           h->d_vals[0], h->d_ud[0], h->d_err, sh, st, true));
+      return dbg("init", c, 0);
+    }
     const double *aT = h->d_aT, *sv = h->d_s;
     const unsigned long long *mk = h->d_tmask;
     long long z0 = rb(c), z1 = rb(c + 1);
@@ -1502,6 +1510,26 @@ static fastilu_status compute_host_impl(fastilu_handle h, const double *values, 
   auto tmapb = [&](int b) { return b == 2 ? h->st_tmap3.b : h->st_tmap[b].b; };
   auto tmapo = [&](int b) { return b == 2 ? h->st_tmap_own3.b : h->st_tmap_own[b].b; };
   auto sweep = [&](int sw, int c) -> fastilu_status {
+    if (regp) {  // iterate s - 1 in d_vals[(s-1) & 1] (iterate 0 from the init kernel)
+      const int ib = (sw - 1) & 1, ob = sw & 1;
+      const double *old = h->d_vals[ib], *ahp = h->d_ahat, *udo = h->d_ud[ib];
+      double *outp = h->d_vals[ob], *udn = h->d_ud[ob], *part = h->d_partials;
+      const unsigned long long *mk = h->d_tmask;
+      long long a0 = rb(c), a1 = rb(c + 1);
+      double om = 1.0;
+      unsigned long long *zp = &h->d_err->zero_pivot;
+      unsigned int *ctr = h->d_counter;
+      int sstr = h->t_sstride;
+      const int64_t spt = h->t_rows_tile / 32, ss = h->t_sstride;
+      const int64_t ntl = ((a1 - a0 + 31) / 32 + spt * ss - 1) / (spt * ss) * ss;
+      void *fn = (sw == 1 && h->jit_sweep_first) ? h->jit_sweep_first : h->jit_sweep;
+      void *args[] = {&old, &outp, &ahp, &mk, &udo, &udn, &a0, &a1, &om, &part, &zp, &ctr, &sstr};
+      if (jit_launch(fn, (int)std::min<int64_t>(h->t_grid, ntl), h->t_threads, st, args))
+        FAIL(FASTILU_ERR_CUDA);
+      CU(launch_reduce_reset(h->d_partials, (int)ntl,
+                             h->d_r2c + (int64_t)c * nsweeps + (sw - 1), h->d_counter, st));
+      return dbg("sweep", sw, c);
+    }
     const int ib = sw >= 2 ? bufi[sw - 1] : 0, ob = bufi[sw];
     const double *old = vbuf(ib), *ahp = h->d_ahat;
     double *outp = vbuf(ob), *udn = ubuf(ob), *part = h->d_partials;

@@ -150,6 +150,25 @@ def test_few_trisweeps(nt):
     full_check(P.laplace3d_7pt(12), 0, 2, nt)
 
 
+@pytest.mark.parametrize("kind,k,ns,nt", [("7pt", 0, 2, 5), ("aniso7pt", 0, 2, 1),
+                                           ("7pt", 0, 3, 2)])
+def test_solve_host_register_pivot_path(kind, k, ns, nt):
+    """Narrow templates (7-pt ILU(0), W = 7) pipeline through the register-pivot sweeps (iterate
+    0 stored by the init kernel, diagonal schedule): solve_host's x and factors are bitwise those
+    of compute + apply and the oracle's."""
+    a = P.make(kind, 40, 90)
+    b = P.rhs_positive(a.n)
+    f = F.FastILU(a.row_ptr, a.col_idx, a.values, k)
+    x1 = f.solve_host(a.values, ns, b, nt)
+    v1, _ = f.factors()
+    f.compute(ns)
+    assert np.array_equal(x1, f.apply_host(b, nt))
+    assert np.array_equal(v1, f.factors()[0])
+    fo = oracle.compute(a, k, ns)
+    assert np.array_equal(v1, fo.vals)
+    assert np.array_equal(x1, oracle.apply(fo, b, nt))
+
+
 @pytest.mark.parametrize("om_tri", [1.0, 0.7])
 def test_one_trisweep_fused(om_tri):
     """ntri = 1 runs the first L and U sweeps as one pass (first_LU_kernel): x bitwise the
