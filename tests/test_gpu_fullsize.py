@@ -122,3 +122,12 @@ def test_config2_7pt_128_exact():
     g, k, ns, nt = 128, 0, 3, 5
     a, b, f, vals, s, rp, ci, x = run_full("7pt", g, k, ns, nt)
     check_planes(a, b, "7pt", g, k, ns, nt, [0, 77, 127], vals, rp, ci, x)
+
+
+def test_config5_aniso7pt_256():
+    """BASELINE configs[4] at full size: anisotropic 7-pt 256^3 ILU(0), 2 sweeps + 5/5 Jacobi
+    (the register-pivot template path), sampled planes bitwise against the windowed oracle."""
+    g, k, ns, nt = 256, 0, 2, 5
+    a, b, f, vals, s, rp, ci, x = run_full("aniso7pt", g, k, ns, nt)
+    assert f.info().startswith("path=tsell")
+    check_planes(a, b, "aniso7pt", g, k, ns, nt, [0, 131, 255], vals, rp, ci, x)
