@@ -351,63 +351,6 @@ __global__ void bsr_ahat_kernel(BsrDev B, const int64_t *__restrict__ arp,
   }
 }
 
-// The same sweep with the term loop software-pipelined: the next term's block indices and its
-// two blocks are loaded before the current term's products (two gathers in flight per thread
-// instead of one); same terms, same order, bitwise the same.
-template <int BS, int MINB>
-__global__ void __launch_bounds__(256, MINB)
-bsr_sweep_pf_kernel(BsrDev B, const double *__restrict__ ahb, const double *__restrict__ old,
-                    double *__restrict__ out, double omega, double *__restrict__ partials,
-                    ErrFlags *err) {
-  constexpr int BB = BS * BS, ST = (BB + 1) & ~1;
-  double r2 = 0.0;
-  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < B.nblk;
-       b += (int64_t)gridDim.x * blockDim.x) {
-    const int I = B.brow[b], J = B.bcol[b];
-    double a[BB];
-    ld_block<BB, ST>(ahb + b * ST, a);
-    const int64_t t0 = B.tptr[b], t1 = B.tptr[b + 1];
-    double L[BB], U[BB];
-    if (t0 < t1) {
-      const int2 pr = B.terms[t0];
-      ld_block_any<BB, ST>(old + (int64_t)pr.x * ST, L);
-      ld_block<BB, ST>(old + (int64_t)pr.y * ST, U);
-    }
-    for (int64_t t = t0; t < t1; t++) {  // pivot blocks K ascending
-      double Ln[BB], Un[BB];
-      if (t + 1 < t1) {
-        const int2 pn = B.terms[t + 1];
-        ld_block_any<BB, ST>(old + (int64_t)pn.x * ST, Ln);
-        ld_block<BB, ST>(old + (int64_t)pn.y * ST, Un);
-      }
-#pragma unroll
-      for (int d = 0; d < BS; d++)
-#pragma unroll
-        for (int e = 0; e < BS; e++) {
-          double v = a[d * BS + e];
-#pragma unroll
-          for (int c = 0; c < BS; c++) v = __dsub_rn(v, __dmul_rn(L[d * BS + c], U[c * BS + e]));
-          a[d * BS + e] = v;
-        }
-      if (t + 1 < t1) {
-#pragma unroll
-        for (int q = 0; q < BB; q++) L[q] = Ln[q], U[q] = Un[q];
-      }
-    }
-    bsr_finish<BS>(B, b, I, J, a, old, old, out, omega, r2, err);
-  }
-  __shared__ double wsum[32];
-  double v = r2;
-  for (int q = 16; q > 0; q >>= 1) v += __shfl_down_sync(0xffffffffu, v, q);
-  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = v;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); w++) t += wsum[w];
-    partials[blockIdx.x] = t;
-  }
-}
-
 #define FASTILU_BS_DISPATCH(BSV, CALL) \
   switch (BSV) {                       \
     case 2: { constexpr int BS = 2; CALL; } break; \
@@ -447,9 +390,6 @@ static cudaError_t launch_bsr_t(const BsrDev &B, const double *ahb, const double
   if (smem) {
     FASTILU_BS_DISPATCH(B.bs, (bsr_sweep_kernel<BS, true, MINB><<<grid, threads, smem, st>>>(
                                   B, ahb, old, out, omega, partials, err, sb)))
-  } else if (std::getenv("FASTILU_BSR_PF")) {  // A/B: software-pipelined term loop
-    FASTILU_BS_DISPATCH(B.bs, (bsr_sweep_pf_kernel<BS, MINB><<<grid, threads, 0, st>>>(
-                                  B, ahb, old, out, omega, partials, err)))
   } else {
     FASTILU_BS_DISPATCH(B.bs, (bsr_sweep_kernel<BS, false, MINB><<<grid, threads, 0, st>>>(
                                   B, ahb, old, out, omega, partials, err, 0)))
